@@ -1,0 +1,188 @@
+/*
+ * fkk.h -- C-ABI of the B200-native fKK-EC hot path (arxiv 2005.07132).
+ *
+ * The method (PAPER.md = /root/reference/PAPER.md, cited as PAPER.md:<line> (section, Eq.)):
+ *   inputs  : a CARS cube I (N spectra x M channels, "M spectra ... N frequency
+ *             increments" -- letters swapped here to BASELINE.json's N pixels x M channels) and one
+ *             surrogate reference spectrum I_ref;
+ *   output  : K_CARS = chi^(3)/chi_nr per pixel (Eq. 2), complex; its imaginary part
+ *             is the Raman-to-NRB ratio.
+ *   paths   : fkk_transform      -- factorized fKK + fPEC + fSEC + reconstruction (Eqs. 6-23,
+ *                                   PAPER.md:61-164), a collective over the pixel shards;
+ *             fkk_apply_trained_basis -- ML:fKK-EC (Eqs. 24-25), local;
+ *             kk_direct_batch    -- conventional per-spectrum KK + PEC + SEC (Eqs. 3-5,
+ *                                   PAPER.md:36-55), local;
+ *             fkk_svd            -- the truncated SVD alone.
+ *
+ * Conventions:
+ *   - cube layout: row-major N x M, each spectrum contiguous; the frequency axis is uniform and
+ *     ascending (a descending axis flips the Hilbert sign, reading A2);
+ *   - log-ratio a = f * 1/2 ln(max(I/I_ref, ratio_floor)) (Eq. 6/10, readings A15/A16);
+ *   - Hilbert: centred pad to L (REFLECT default, ZERO optional), multiplier -i sgn, DC and Nyquist
+ *     zeroed, H{cos} = sin (readings A2-A4);
+ *   - ALS: lambda = 1e4, p = 1e-3, 10 fp64 solves, w^0 = 1 (readings A6/A7);
+ *   - SG trend: order 2, window 2 floor(0.375 M) + 1, polynomial edges (reading A8);
+ *   - fPEC ridge lambda = ridge_rel * lambda_max(X^T X) (reading A11); q = sorted unique union of
+ *     per-column argmax/argmin, ties to the lowest global pixel index (reading A12).
+ *
+ * Memory: every pointer named d_* is DEVICE memory (cudaMalloc / torch CUDA tensor) owned by the
+ * caller; h_* is host memory owned by the caller.  Inputs are read-only.  All work is enqueued on
+ * the plan's stream (fkk_plan_set_stream); calls that return host data synchronise that stream.
+ * Errors: every function returns fkk_status and never throws; fkk_last_error(plan) gives a
+ * message.  Device-detected errors (non-positive reference, non-finite input) of an asynchronous
+ * call are returned by the next fkk_plan_sync() or synchronous call on the same plan.  On error
+ * the contents of output buffers are unspecified.  A plan is not thread-safe.
+ */
+#ifndef FKK_H
+#define FKK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FKK_OK = 0,
+  FKK_ERR_INVALID_ARG = 1,        /* null pointer, bad shape/size/alignment, k out of range */
+  FKK_ERR_NONFINITE_INPUT = 2,    /* NaN/Inf in the cube */
+  FKK_ERR_BAD_REFERENCE = 3,      /* I_ref <= 0 or non-finite (Eq. 3 needs ln(I/I_ref)) */
+  FKK_ERR_NUMERICAL = 4,          /* eigensolver / Cholesky failure ("increase ridge_rel") */
+  FKK_ERR_INCOMPATIBLE_BASIS = 5, /* trained basis M or L differs from the plan */
+  FKK_ERR_STATE = 6,              /* call order / plan state error */
+  FKK_ERR_CUDA = 7,               /* CUDA runtime error */
+  FKK_ERR_NCCL = 8,               /* NCCL error */
+  FKK_ERR_OOM = 9,                /* workspace allocation failed */
+  FKK_ERR_NOT_IMPLEMENTED = 10
+} fkk_status;
+
+typedef enum { FKK_PAD_REFLECT = 0, FKK_PAD_ZERO = 1 } fkk_pad_mode;
+typedef enum { FKK_OUT_COMPLEX64 = 0, FKK_OUT_IMAG_F32 = 1 } fkk_out_layout;
+typedef enum { FKK_IN_F32 = 0, FKK_IN_F64 = 1 } fkk_in_dtype;
+/* Dense contractions (Gram, projection, reconstruction): tcgen05 3xTF32 (default) or an
+ * exact-fp32 CUDA-core variant kept as a measured comparison. */
+typedef enum { FKK_GEMM_3XTF32 = 0, FKK_GEMM_FP32_SIMT = 1 } fkk_gemm_impl;
+typedef enum { FKK_F_ONE = 0, FKK_F_EQ9 = 1 } fkk_f_mode;
+
+typedef struct fkk_plan* fkk_plan_t;
+typedef struct fkk_basis* fkk_basis_t;
+
+typedef struct {
+  int32_t n_freq;            /* M: 8 <= M <= 4096, M % 4 == 0 (16-B rows for vector loads) */
+  int64_t max_rows;          /* max spectra per call on this rank (workspace sizing), >= 1 */
+  int32_t rank_k;            /* k: 1 <= k <= min(M, 128, N_global) retained singular triplets */
+  int32_t fft_len;           /* L: 0 -> 2*nextpow2(M); else a power of two >= M, <= 8192 */
+  int32_t pad_mode;          /* fkk_pad_mode, default FKK_PAD_REFLECT (reading A3) */
+  double ratio_floor;        /* clamp of I/I_ref before ln, default 1e-6 (reading A16) */
+  int32_t f_mode;            /* fkk_f_mode: f(omega) of Eq. 9 or f == 1 (default) */
+  double f_alpha, f_sigma_g; /* Eq. 9 Poisson multiplier and Gaussian sigma */
+  double als_lambda;         /* ALS smoothness, default 1e4 */
+  double als_p;              /* ALS asymmetry, default 1e-3 */
+  int32_t als_iters;         /* ALS solves, default 10 */
+  int32_t sg_window;         /* 0 -> 2*floor(0.375*M)+1 (odd, <= M) */
+  int32_t sg_order;          /* must be 2 */
+  double ridge_rel;          /* fPEC ridge: lambda = ridge_rel * lambda_max(X^T X), default 1e-3 */
+  double ml_ridge_rel;       /* ML ridge: lambda_ml = ml_ridge_rel * s_1^2, default 0 */
+  int32_t gemm_impl;         /* fkk_gemm_impl */
+  int32_t out_layout;        /* fkk_out_layout */
+  int32_t in_dtype;          /* fkk_in_dtype of the cube and of I_ref */
+  int32_t device;            /* CUDA device ordinal */
+  int32_t world_size, rank;  /* pixel shards: this rank owns a contiguous block of rows */
+  const uint8_t* nccl_id;    /* 128-byte ncclUniqueId from fkk_get_nccl_unique_id; NULL iff world_size == 1 */
+  int32_t loopback_shards;   /* >1: run the Gram/projection per virtual shard on one GPU and combine
+                                in the multi-rank order (partition-invariance test mode) */
+} fkk_plan_desc;
+
+/* Fill *d with the defaults above for the given M, k and max_rows. */
+void fkk_plan_desc_init(fkk_plan_desc* d, int32_t n_freq, int32_t rank_k, int64_t max_rows);
+
+fkk_status fkk_get_nccl_unique_id(uint8_t out[128]);
+fkk_status fkk_plan_create(const fkk_plan_desc* d, fkk_plan_t* out);  /* allocates all workspace */
+fkk_status fkk_plan_destroy(fkk_plan_t p);
+const char* fkk_last_error(fkk_plan_t p);          /* valid until the next call on p; p may be NULL */
+fkk_status fkk_plan_set_stream(fkk_plan_t p, void* cuda_stream);   /* NULL -> plan-owned stream */
+fkk_status fkk_plan_sync(fkk_plan_t p);            /* synchronise; report deferred device errors */
+
+/* fkk_svd -- truncated SVD A ~ U S V^T of the log-ratio matrix through the Gram
+ * matrix G = A^T A (all-reduced over ranks).  Collective.  d_icars: n_rows x M (this rank's rows);
+ * d_iref: M.  d_V_out: M x k fp32, column-major (each right singular vector contiguous), sign rule:
+ * the entry of largest |.| is positive.  h_s_out: k singular values (host, descending).  Syncs. */
+fkk_status fkk_svd(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref,
+                   float* d_V_out, double* h_s_out);
+
+/* fkk_transform -- full fKK-EC (F0..F11): Eq. 23
+ *   K = exp[US (V^T/f + H{Phi_PEC} - V_SEC^T)] exp[i US (H{V^T/f} - Phi_PEC)].
+ * Collective.  d_out: n_rows x M complex64 (re, im interleaved) or fp32 Im only (out_layout).
+ * basis_out (nullable): receives a trained basis (caller frees with fkk_basis_destroy). */
+fkk_status fkk_transform(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref,
+                         void* d_out, fkk_basis_t* basis_out);
+
+/* fkk_apply_trained_basis -- ML:fKK-EC (Eqs. 24-25): US_new = A_new W with
+ * W = V diag(s^2/(s^2 + lambda_ml)), then Eq. 23 with the trained B.  Local (no collective).
+ * Uses the trained reference and f stored in the basis. */
+fkk_status fkk_apply_trained_basis(fkk_plan_t p, fkk_basis_t b, const void* d_icars,
+                                   int64_t n_rows, void* d_out);
+
+/* kk_direct_batch -- conventional per-spectrum KK + PEC + SEC (Eq. 5 in the log domain,
+ * PAPER.md:53): a = 1/2 ln(I/I_ref); phi = H{a}; phi_err = ALS(phi); a' = a + H{phi_err};
+ * phi' = phi - phi_err; K' = e^{a'} e^{i phi'}; K_CARS = K' / SGtrend(Re K').  Local. */
+fkk_status kk_direct_batch(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref,
+                           void* d_out);
+
+/* Host-buffer variants (end-to-end: host->device copies, compute, device->host copies, all on the
+ * plan's stream; they synchronise before returning).  h_* may be pageable or pinned. */
+fkk_status fkk_transform_host(fkk_plan_t p, const void* h_icars, int64_t n_rows, const void* h_iref,
+                              void* h_out, fkk_basis_t* basis_out);
+fkk_status fkk_apply_trained_basis_host(fkk_plan_t p, fkk_basis_t b, const void* h_icars,
+                                        int64_t n_rows, void* h_out);
+fkk_status kk_direct_batch_host(fkk_plan_t p, const void* h_icars, int64_t n_rows,
+                                const void* h_iref, void* h_out);
+
+fkk_status fkk_basis_destroy(fkk_basis_t b);
+/* Basis metadata: M, k, L.  Any pointer may be NULL. */
+fkk_status fkk_basis_info(fkk_basis_t b, int32_t* n_freq, int32_t* rank_k, int32_t* fft_len);
+
+/* Stage tensors of the last fkk_transform / fkk_svd on p (stage-wise parity):
+ *   G: M x M fp64 | S: k fp64 | V: M x k fp64 column-major | US: n_rows x k fp32 row-major |
+ *   Q: nq int64 (global pixel indices, ascending) | HV: k x M fp64 | PHI_ERR: nq x M fp64 |
+ *   PHI_PEC: k x M fp64 | V_SEC: k x M fp64 | B: k x M x 2 fp32 (amp, ph interleaved) |
+ *   LAMBDA: 1 fp64 (fPEC ridge) | F: M fp64.
+ * fkk_stage_size returns the byte size; fkk_get_stage copies min(bytes, size) bytes. */
+typedef enum {
+  FKK_STAGE_G = 0, FKK_STAGE_S, FKK_STAGE_V, FKK_STAGE_US, FKK_STAGE_Q, FKK_STAGE_HV,
+  FKK_STAGE_PHI_ERR, FKK_STAGE_PHI_PEC, FKK_STAGE_V_SEC, FKK_STAGE_B, FKK_STAGE_LAMBDA, FKK_STAGE_F
+} fkk_stage;
+size_t fkk_stage_size(fkk_plan_t p, int32_t stage);
+fkk_status fkk_get_stage(fkk_plan_t p, int32_t stage, void* dst, size_t bytes, int32_t dst_is_device);
+
+/* Test hook: F5..F11 with caller-supplied V (d_V: M x k fp32 column-major), s (host) and q (host,
+ * global pixel indices, ascending, nq <= 2k), skipping the SVD and the q selection. */
+fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref,
+                              const float* d_V, const double* h_s, const int64_t* h_q, int32_t nq,
+                              void* d_out);
+
+/* Per-stage device times (ms) of the last call, measured with CUDA events on the plan stream when
+ * timing is enabled.  names/ms arrays of length cap; returns the number of stages written. */
+fkk_status fkk_enable_timing(fkk_plan_t p, int32_t on);
+int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap);
+/* Number of kernel launches issued by the last call (the bench reports it). */
+int64_t fkk_last_launch_count(fkk_plan_t p);
+
+/* ---------------- host-only helpers (no GPU needed; exercised by the CPU tests) ---------------- */
+/* Top-k eigenpairs of a symmetric M x M fp64 matrix (row-major; only the lower triangle is read):
+ * Householder tridiagonalisation, Sturm bisection, inverse iteration, back-transformation.
+ * V: M x k column-major, lam: k descending.  Sign rule as fkk_svd. */
+fkk_status fkk_host_eig_topk(const double* G, int32_t M, int32_t k, double* V, double* lam);
+/* Rows [*row0, *row1) owned by `rank` of `world` for n_global rows (contiguous, ragged last). */
+void fkk_shard_range(int64_t n_global, int32_t world, int32_t rank, int64_t* row0, int64_t* row1);
+/* Merge per-rank column extremes into q (reading A12).  vals/idx: world x k x 2 arrays, [..][..][0]
+ * = max, [1] = min, idx = global pixel index.  Writes the sorted unique union to q_out (capacity
+ * 2k) and returns its length. */
+int32_t fkk_merge_extremes(const float* vals, const int64_t* idx, int32_t world, int32_t k,
+                           int64_t* q_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FKK_H */

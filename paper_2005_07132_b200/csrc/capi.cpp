@@ -1,0 +1,928 @@
+// C-ABI of the fKK-EC hot path (include/fkk.h): plan / workspace / stream management, the stage
+// orchestration of the factorized path (F0..F11), ML reuse (F12)
+// and the direct path (D1..D5), NCCL for the pixel-sharded collectives.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/fkk.h"
+#include "fkk_internal.h"
+
+using fkk::Status;
+
+// ------------------------------------------------------------------------------------------------
+// NCCL, resolved at run time (only when world_size > 1), so the library loads without it.
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) { h = dlopen(n, RTLD_NOW | RTLD_GLOBAL); if (h) break; }
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+#define FKK_SYM(field, name) field = reinterpret_cast<decltype(field)>(dlsym(h, name)); if (!field) { err = "missing NCCL symbol " name; return false; }
+    FKK_SYM(GetUniqueId, "ncclGetUniqueId");
+    FKK_SYM(CommInitRank, "ncclCommInitRank");
+    FKK_SYM(CommDestroy, "ncclCommDestroy");
+    FKK_SYM(CommAbort, "ncclCommAbort");
+    FKK_SYM(AllReduce, "ncclAllReduce");
+    FKK_SYM(AllGather, "ncclAllGather");
+    FKK_SYM(GetErrorString, "ncclGetErrorString");
+#undef FKK_SYM
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Status(FKK_ERR_NCCL, std::string("NCCL ") + what + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  if (count == 0) count = 1;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Status(FKK_ERR_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed: " + cudaGetErrorString(e));
+  }
+  return static_cast<T*>(p);
+}
+
+int ilog2i(int L) { int r = 0; while ((1 << r) < L) ++r; return r; }
+int next_pow2(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------
+// Trained basis (ML:fKK-EC model: f, S, V, Phi_PEC, V_SEC -> W and B)
+// ------------------------------------------------------------------------------------------------
+struct fkk_basis {
+  int M = 0, k = 0, kp = 0, L = 0, pad = 0, device = 0;
+  double ratio_floor = 1e-6;
+  float* inv_ref = nullptr;
+  double* ref64 = nullptr;
+  double* f64 = nullptr;
+  float* W = nullptr;    // M x kp, D_f V diag(s^2/(s^2+lam_ml))
+  float* Bi = nullptr;   // k x M x 2
+  double* V64 = nullptr;
+  std::vector<double> s;
+  ~fkk_basis() {
+    cudaFree(inv_ref); cudaFree(ref64); cudaFree(f64); cudaFree(W); cudaFree(Bi); cudaFree(V64);
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
+// Plan
+// ------------------------------------------------------------------------------------------------
+struct fkk_plan {
+  fkk_plan_desc d{};
+  int M = 0, k = 0, kp = 0, L = 0, log2L = 0, sg_half = 0, in_f64 = 0, pad_zero = 0;
+  size_t in_elem = 4;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // device workspace (factorized)
+  int* flags = nullptr;
+  int* h_flags = nullptr;   // pinned
+  float* inv_ref = nullptr;
+  double* ref64 = nullptr;
+  float2* tw32 = nullptr;
+  double2* tw64 = nullptr;
+  float* A = nullptr;
+  double* gram_part = nullptr;
+  int gram_nsplit_cap = 0;
+  double* G = nullptr;
+  double* colsum = nullptr;
+  double* f64 = nullptr;
+  float* f32 = nullptr;
+  double* V64 = nullptr;
+  float* W = nullptr;
+  float* US = nullptr;
+  float* ext_val = nullptr;
+  int64_t* ext_idx = nullptr;
+  float* ext_out_val = nullptr;
+  int64_t* ext_out_idx = nullptr;
+  int64_t* q_dev = nullptr;
+  double *X = nullptr, *Vt_f = nullptr, *Hv = nullptr, *P = nullptr, *Phi_err = nullptr, *XtX = nullptr,
+         *XtPhi = nullptr, *Phi_pec = nullptr, *HPhi = nullptr, *tmp = nullptr, *Vsec = nullptr, *ridge_work = nullptr,
+         *lam = nullptr, *basis_als_state = nullptr;
+  float* Bi = nullptr;
+  // direct path (lazy)
+  int64_t direct_batch = 0;
+  float *phi = nullptr, *phierr = nullptr;
+  double* als_state = nullptr;
+  // host-buffer variants (lazy)
+  void* d_in_cube = nullptr;
+  size_t d_in_cube_bytes = 0;
+  void* d_out_cube = nullptr;
+  size_t d_out_cube_bytes = 0;
+  void* d_ref_buf = nullptr;
+  // last-call host state
+  std::vector<double> h_s;
+  std::vector<int64_t> h_q;
+  int64_t last_rows = 0, last_row0 = 0, last_global_rows = 0;
+  bool have_transform = false;
+  // timing
+  bool timing = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  std::vector<std::string> t_names;
+  std::vector<float> t_ms;
+  int64_t launches = 0;
+
+  ~fkk_plan() {
+    if (stream) cudaStreamSynchronize(stream);
+    void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
+                    ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
+                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, phi, phierr, als_state, d_in_cube,
+                    d_out_cube, d_ref_buf};
+    for (void* p : ptrs) if (p) cudaFree(p);
+    if (h_flags) cudaFreeHost(h_flags);
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  int nq_cap() const { return 2 * k; }
+
+  void mark(const char* name) {
+    if (!timing) return;
+    cudaEvent_t e;
+    FKK_CUDA_CHECK(cudaEventCreate(&e));
+    FKK_CUDA_CHECK(cudaEventRecord(e, stream));
+    marks.emplace_back(name, e);
+  }
+  void begin_call() {
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    marks.clear();
+    fkk::g_launches = 0;
+    FKK_CUDA_CHECK(cudaSetDevice(d.device));
+    mark("start");
+  }
+  void end_call() {
+    launches = fkk::g_launches;
+    t_names.clear();
+    t_ms.clear();
+    if (!timing || marks.size() < 2) return;
+    FKK_CUDA_CHECK(cudaEventSynchronize(marks.back().second));
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      FKK_CUDA_CHECK(cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second));
+      t_names.push_back(marks[i].first);
+      t_ms.push_back(ms);
+    }
+  }
+
+  // deferred device errors: reads the pinned flag word after the stream drained
+  void check_flags_sync() {
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(stream));
+    const int f = *h_flags;
+    if (f) {
+      FKK_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+      if (f & 1) throw Status(FKK_ERR_BAD_REFERENCE, "reference spectrum has a non-positive or non-finite value");
+      if (f & 2) throw Status(FKK_ERR_NONFINITE_INPUT, "non-finite value in the input cube");
+      if (f & 4) throw Status(FKK_ERR_NUMERICAL, "ridge system not positive definite (increase ridge_rel)");
+    }
+  }
+
+  void ensure_direct() {
+    if (phi) return;
+    direct_batch = std::min<int64_t>(std::max<int64_t>(d.max_rows, 2), 131072);
+    direct_batch = ((direct_batch + 31) / 32) * 32;
+    phi = dalloc<float>((size_t)direct_batch * M);
+    phierr = dalloc<float>((size_t)direct_batch * M);
+    als_state = dalloc<double>((size_t)3 * M * direct_batch);
+  }
+};
+
+namespace {
+
+void validate_desc(const fkk_plan_desc* d) {
+  if (!d) throw Status(FKK_ERR_INVALID_ARG, "desc is NULL");
+  if (d->n_freq < 8 || d->n_freq > 4096 || d->n_freq % 4) throw Status(FKK_ERR_INVALID_ARG, "n_freq must be in [8, 4096] and a multiple of 4");
+  if (d->max_rows < 1) throw Status(FKK_ERR_INVALID_ARG, "max_rows must be >= 1");
+  if (d->rank_k < 1 || d->rank_k > std::min(d->n_freq, 128)) throw Status(FKK_ERR_INVALID_ARG, "rank_k must be in [1, min(M, 128)]");
+  if (d->fft_len) {
+    if (d->fft_len < d->n_freq || (d->fft_len & (d->fft_len - 1)) || d->fft_len > 8192)
+      throw Status(FKK_ERR_INVALID_ARG, "fft_len must be a power of two in [M, 8192]");
+  }
+  if (d->pad_mode != FKK_PAD_REFLECT && d->pad_mode != FKK_PAD_ZERO) throw Status(FKK_ERR_INVALID_ARG, "bad pad_mode");
+  if (!(d->ratio_floor > 0)) throw Status(FKK_ERR_INVALID_ARG, "ratio_floor must be > 0");
+  if (d->f_mode != FKK_F_ONE && d->f_mode != FKK_F_EQ9) throw Status(FKK_ERR_INVALID_ARG, "bad f_mode");
+  if (!(d->als_lambda > 0) || !(d->als_p > 0 && d->als_p < 0.5) || d->als_iters < 1)
+    throw Status(FKK_ERR_INVALID_ARG, "ALS needs lambda > 0, 0 < p < 0.5, iters >= 1");
+  if (d->sg_order != 2) throw Status(FKK_ERR_INVALID_ARG, "sg_order must be 2");
+  if (d->sg_window && (d->sg_window % 2 == 0 || d->sg_window < 5 || d->sg_window > d->n_freq))
+    throw Status(FKK_ERR_INVALID_ARG, "sg_window must be odd, >= 5 and <= M");
+  if (!(d->ridge_rel >= 0) || !(d->ml_ridge_rel >= 0)) throw Status(FKK_ERR_INVALID_ARG, "ridge weights must be >= 0");
+  if (d->gemm_impl != FKK_GEMM_3XTF32 && d->gemm_impl != FKK_GEMM_FP32_SIMT) throw Status(FKK_ERR_INVALID_ARG, "bad gemm_impl");
+  if (d->out_layout != FKK_OUT_COMPLEX64 && d->out_layout != FKK_OUT_IMAG_F32) throw Status(FKK_ERR_INVALID_ARG, "bad out_layout");
+  if (d->in_dtype != FKK_IN_F32 && d->in_dtype != FKK_IN_F64) throw Status(FKK_ERR_INVALID_ARG, "bad in_dtype");
+  if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) throw Status(FKK_ERR_INVALID_ARG, "bad world_size/rank");
+  if ((d->world_size > 1) != (d->nccl_id != nullptr)) throw Status(FKK_ERR_INVALID_ARG, "nccl_id must be given iff world_size > 1");
+  if (d->loopback_shards < 0 || d->loopback_shards > 64) throw Status(FKK_ERR_INVALID_ARG, "loopback_shards must be in [0, 64]");
+}
+
+void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
+  validate_desc(d);
+  p->d = *d;
+  p->M = d->n_freq;
+  p->k = d->rank_k;
+  p->kp = p->k <= 16 ? 16 : (p->k <= 32 ? 32 : (p->k <= 64 ? 64 : 128));
+  p->L = d->fft_len ? d->fft_len : 2 * next_pow2(p->M);
+  p->log2L = ilog2i(p->L);
+  const int win = d->sg_window ? d->sg_window : 2 * (int)std::floor(0.375 * p->M) + 1;
+  p->sg_half = (std::min(win, p->M % 2 ? p->M : p->M - 1) - 1) / 2;
+  p->in_f64 = d->in_dtype == FKK_IN_F64;
+  p->in_elem = p->in_f64 ? 8 : 4;
+  p->pad_zero = d->pad_mode == FKK_PAD_ZERO;
+  FKK_CUDA_CHECK(cudaSetDevice(d->device));
+  FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  p->own_stream = true;
+  const int M = p->M, k = p->k, kp = p->kp;
+  const int64_t n = d->max_rows;
+  p->flags = dalloc<int>(4);
+  FKK_CUDA_CHECK(cudaMemset(p->flags, 0, 4 * sizeof(int)));
+  FKK_CUDA_CHECK(cudaMallocHost(&p->h_flags, 4 * sizeof(int)));
+  p->inv_ref = dalloc<float>(M);
+  p->ref64 = dalloc<double>(M);
+  // twiddles exp(-2 pi i j / L), fp64 on the host
+  {
+    std::vector<float2> t32(p->L / 2);
+    std::vector<double2> t64(p->L / 2);
+    for (int j = 0; j < p->L / 2; ++j) {
+      const double a = -2.0 * M_PI * (double)j / (double)p->L;
+      t64[j] = make_double2(std::cos(a), std::sin(a));
+      t32[j] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    p->tw32 = dalloc<float2>(p->L / 2);
+    p->tw64 = dalloc<double2>(p->L / 2);
+    FKK_CUDA_CHECK(cudaMemcpy(p->tw32, t32.data(), t32.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    FKK_CUDA_CHECK(cudaMemcpy(p->tw64, t64.data(), t64.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  p->A = dalloc<float>((size_t)n * M);
+  p->gram_nsplit_cap = fkk::gram_num_splits(n, M);
+  p->gram_part = dalloc<double>((size_t)p->gram_nsplit_cap * fkk::gram_num_tiles(M) * 128 * 128);
+  p->G = dalloc<double>((size_t)M * M);
+  p->colsum = dalloc<double>(M);
+  p->f64 = dalloc<double>(M);
+  p->f32 = dalloc<float>(M);
+  p->V64 = dalloc<double>((size_t)M * k);
+  p->W = dalloc<float>((size_t)M * kp);
+  p->US = dalloc<float>((size_t)n * k);
+  const int nblk = fkk::project_num_blocks(n);
+  p->ext_val = dalloc<float>((size_t)nblk * k * 2);
+  p->ext_idx = dalloc<int64_t>((size_t)nblk * k * 2);
+  p->ext_out_val = dalloc<float>((size_t)64 * k * 2);
+  p->ext_out_idx = dalloc<int64_t>((size_t)64 * k * 2);
+  const int nqc = p->nq_cap();
+  p->q_dev = dalloc<int64_t>(nqc);
+  p->X = dalloc<double>((size_t)nqc * k);
+  p->Vt_f = dalloc<double>((size_t)k * M);
+  p->Hv = dalloc<double>((size_t)k * M);
+  p->P = dalloc<double>((size_t)nqc * M);
+  p->Phi_err = dalloc<double>((size_t)nqc * M);
+  p->XtX = dalloc<double>((size_t)k * k);
+  p->XtPhi = dalloc<double>((size_t)k * M);
+  p->Phi_pec = dalloc<double>((size_t)k * M);
+  p->HPhi = dalloc<double>((size_t)k * M);
+  p->tmp = dalloc<double>((size_t)k * M);
+  p->Vsec = dalloc<double>((size_t)k * M);
+  p->ridge_work = dalloc<double>((size_t)3 * k * k);
+  p->lam = dalloc<double>(1);
+  p->basis_als_state = dalloc<double>((size_t)3 * M * (((nqc + 31) / 32) * 32));
+  p->Bi = dalloc<float>((size_t)k * M * 2);
+  if (d->world_size > 1) {
+    std::string e;
+    if (!g_nccl.load(e)) throw Status(FKK_ERR_NCCL, e);
+    ncclUniqueId id;
+    std::memcpy(&id, d->nccl_id, sizeof(id));
+    nccl_check(g_nccl.CommInitRank(&p->comm, d->world_size, id, d->rank), "CommInitRank");
+  }
+}
+
+struct Shard { int64_t row0, rows; };
+
+// Rows of all ranks (global row offset of this rank, global N): allgather of n_rows.
+void exchange_rows(fkk_plan* p, int64_t n_rows, int64_t& row0, int64_t& n_global) {
+  if (p->d.world_size == 1) { row0 = 0; n_global = n_rows; return; }
+  int64_t* buf = dalloc<int64_t>(p->d.world_size + 1);
+  std::vector<int64_t> h(p->d.world_size);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(buf + p->d.world_size, &n_rows, sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  nccl_check(g_nccl.AllGather(buf + p->d.world_size, buf, 1, ncclInt64, p->comm, p->stream), "AllGather(rows)");
+  FKK_CUDA_CHECK(cudaMemcpyAsync(h.data(), buf, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  cudaFree(buf);
+  row0 = 0;
+  n_global = 0;
+  for (int r = 0; r < p->d.world_size; ++r) { if (r < p->d.rank) row0 += h[r]; n_global += h[r]; }
+}
+
+void check_cube_args(fkk_plan* p, const void* cube, int64_t n_rows, const void* ref, const void* out) {
+  if (!cube && n_rows > 0) throw Status(FKK_ERR_INVALID_ARG, "cube pointer is NULL");
+  if (!out && n_rows > 0) throw Status(FKK_ERR_INVALID_ARG, "output pointer is NULL");
+  if (!ref) throw Status(FKK_ERR_INVALID_ARG, "reference pointer is NULL");
+  if (n_rows < 0 || n_rows > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be in [0, max_rows]");
+  if (!aligned16(cube) || !aligned16(out)) throw Status(FKK_ERR_INVALID_ARG, "cube and output must be 16-byte aligned");
+}
+
+// F0..F4: log-ratio, Gram (all-reduced), eig -> V64 (device), s (host).
+void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_iref, int64_t n_global) {
+  cudaStream_t s = p->stream;
+  const int M = p->M, k = p->k;
+  fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
+  fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
+  if (p->d.f_mode == FKK_F_EQ9) {
+    FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
+    fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);
+    if (p->d.world_size > 1) nccl_check(g_nccl.AllReduce(p->colsum, p->colsum, M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(colsum)");
+    fkk::launch_noise_scale_from_sums(p->colsum, M, 1.0 / (double)std::max<int64_t>(n_global, 1), p->d.f_alpha, p->d.f_sigma_g, p->f64, p->f32, s);
+  } else {
+    fkk::launch_fill(p->f64, 1.0, M, s);
+    fkk::launch_fill_f(p->f32, 1.0f, M, s);
+  }
+  p->mark("logratio");
+  // Gram: per (virtual) shard in rank order, fp64 partial sums
+  const int shards = std::max(1, p->d.loopback_shards);
+  for (int sh = 0; sh < shards; ++sh) {
+    int64_t r0, r1;
+    fkk_shard_range(n_rows, shards, sh, &r0, &r1);
+    const int ns = std::min(p->gram_nsplit_cap, fkk::gram_num_splits(std::max<int64_t>(r1 - r0, 1), M));
+    fkk::launch_gram_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->gram_part, ns, s);
+    fkk::launch_gram_reduce(p->gram_part, ns, M, p->G, sh > 0, s);
+  }
+  if (p->d.world_size > 1)
+    nccl_check(g_nccl.AllReduce(p->G, p->G, (size_t)M * M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(G)");
+  if (p->d.f_mode == FKK_F_EQ9) fkk::launch_scale_gram(p->G, p->f64, M, s);
+  p->mark("gram");
+  // eig on the host (fp64)
+  std::vector<double> hG((size_t)M * M), hV((size_t)M * k), hl(k);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(hG.data(), p->G, hG.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  p->check_flags_sync();
+  if (fkk::host_eig_topk(hG.data(), M, k, hV.data(), hl.data()) != 0) throw Status(FKK_ERR_NUMERICAL, "eigensolver failed");
+  p->h_s.assign(k, 0.0);
+  for (int i = 0; i < k; ++i) p->h_s[i] = std::sqrt(std::max(hl[i], 0.0));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(p->V64, hV.data(), hV.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // hV is a stack buffer
+  p->mark("eig");
+}
+
+// F5..F11 given V64 (device) and s (host); q computed unless given (h_q != nullptr).
+void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_q_in, int nq_in, void* d_out) {
+  cudaStream_t s = p->stream;
+  const int M = p->M, k = p->k, kp = p->kp;
+  // W = D_f V (fp32) and projection
+  fkk::launch_cast_w(p->V64, p->f64, nullptr, M, k, kp, p->W, s);
+  const int shards = std::max(1, p->d.loopback_shards);
+  std::vector<float> hv;
+  std::vector<int64_t> hi;
+  const int nparts = shards * p->d.world_size;
+  for (int sh = 0; sh < shards; ++sh) {
+    int64_t r0, r1;
+    fkk_shard_range(n_rows, shards, sh, &r0, &r1);
+    fkk::launch_project_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->W, k, kp, p->US + r0 * (int64_t)k, p->ext_val,
+                             p->ext_idx, row0 + r0, s);
+    if (r1 > r0)
+      fkk::launch_extremes_reduce(p->ext_val, p->ext_idx, fkk::project_num_blocks(r1 - r0), k,
+                                  p->ext_out_val + (size_t)sh * k * 2, p->ext_out_idx + (size_t)sh * k * 2, s);
+    else {
+      std::vector<float> ev(k * 2);
+      std::vector<int64_t> ei(k * 2, INT64_MAX);
+      for (int c = 0; c < k; ++c) { ev[2 * c] = -INFINITY; ev[2 * c + 1] = INFINITY; }
+      FKK_CUDA_CHECK(cudaMemcpyAsync(p->ext_out_val + (size_t)sh * k * 2, ev.data(), ev.size() * 4, cudaMemcpyHostToDevice, s));
+      FKK_CUDA_CHECK(cudaMemcpyAsync(p->ext_out_idx + (size_t)sh * k * 2, ei.data(), ei.size() * 8, cudaMemcpyHostToDevice, s));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+  }
+  p->mark("project");
+  std::vector<int64_t> q;
+  if (h_q_in) {
+    q.assign(h_q_in, h_q_in + nq_in);
+  } else {
+    // merge the per-shard (and per-rank) extremes into q (reading A12)
+    const size_t per = (size_t)k * 2;
+    float* gv = p->ext_out_val;
+    int64_t* gi = p->ext_out_idx;
+    if (p->d.world_size > 1) {
+      // each rank contributes its `shards` blocks; gather them after the local ones
+      float* tv = dalloc<float>(per * shards * p->d.world_size);
+      int64_t* ti = dalloc<int64_t>(per * shards * p->d.world_size);
+      nccl_check(g_nccl.AllGather(p->ext_out_val, tv, per * shards, ncclFloat32, p->comm, s), "AllGather(ext val)");
+      nccl_check(g_nccl.AllGather(p->ext_out_idx, ti, per * shards, ncclInt64, p->comm, s), "AllGather(ext idx)");
+      hv.resize(per * nparts);
+      hi.resize(per * nparts);
+      FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), tv, hv.size() * 4, cudaMemcpyDeviceToHost, s));
+      FKK_CUDA_CHECK(cudaMemcpyAsync(hi.data(), ti, hi.size() * 8, cudaMemcpyDeviceToHost, s));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+      cudaFree(tv);
+      cudaFree(ti);
+    } else {
+      hv.resize(per * nparts);
+      hi.resize(per * nparts);
+      FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), gv, hv.size() * 4, cudaMemcpyDeviceToHost, s));
+      FKK_CUDA_CHECK(cudaMemcpyAsync(hi.data(), gi, hi.size() * 8, cudaMemcpyDeviceToHost, s));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    q.resize(2 * k);
+    const int nq = fkk_merge_extremes(hv.data(), hi.data(), nparts, k, q.data());
+    q.resize(nq);
+  }
+  const int nq = (int)q.size();
+  if (nq < 1 || nq > p->nq_cap()) throw Status(FKK_ERR_INVALID_ARG, "q must have 1..2k entries");
+  p->h_q = q;
+  // X = US[q] (rows owned by this rank; others contribute zeros and are summed over ranks)
+  std::vector<int64_t> ql(nq);
+  for (int i = 0; i < nq; ++i) ql[i] = (q[i] >= row0 && q[i] < row0 + n_rows) ? q[i] - row0 : -1;
+  FKK_CUDA_CHECK(cudaMemcpyAsync(p->q_dev, ql.data(), nq * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  fkk::launch_gather_rows(p->US, k, p->q_dev, nq, p->X, s);
+  FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // ql is a stack buffer
+  if (p->d.world_size > 1)
+    nccl_check(g_nccl.AllReduce(p->X, p->X, (size_t)nq * k, ncclFloat64, ncclSum, p->comm, s), "AllReduce(X)");
+  p->mark("select_q");
+  // ---- basis (F6..F10), fp64
+  fkk::launch_vt_over_f(p->V64, p->f64, M, k, p->Vt_f, s);
+  fkk::launch_hilbert_rows_f64(p->Vt_f, k, M, M, p->Hv, p->L, p->pad_zero, p->tw64, s);          // Eq. 11
+  fkk::launch_dgemm_small(nq, M, k, p->X, k, 0, p->Hv, M, 0, p->P, M, 0.0, s);                    // Eq. 16 argument
+  fkk::launch_als_rows(p->P, 1, nq, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->basis_als_state,
+                       p->Phi_err, 1, s);                                                         // D{.}
+  fkk::launch_dgemm_small(k, k, nq, p->X, k, 1, p->X, k, 0, p->XtX, k, 0.0, s);                   // X^T X
+  fkk::launch_dgemm_small(k, M, nq, p->X, k, 1, p->Phi_err, M, 0, p->XtPhi, M, 0.0, s);           // X^T Phi_err
+  fkk::launch_ridge(p->XtX, k, p->XtPhi, M, p->d.ridge_rel, p->Phi_pec, p->lam, p->ridge_work, p->flags, s);  // Eq. 17
+  fkk::launch_hilbert_rows_f64(p->Phi_pec, k, M, M, p->HPhi, p->L, p->pad_zero, p->tw64, s);      // Eq. 18
+  fkk::launch_add_f64(p->Vt_f, p->HPhi, p->tmp, (int64_t)k * M, s);
+  fkk::launch_sg_rows_f64(p->tmp, k, M, p->sg_half, p->Vsec, s);                                  // Eq. 22
+  fkk::launch_assemble_B(p->Vt_f, p->HPhi, p->Vsec, p->Hv, p->Phi_pec, k, M, p->Bi, s);           // Eq. 23
+  p->mark("basis");
+  // ---- reconstruction (F11)
+  fkk::launch_reconstruct_simt(p->US, n_rows, k, p->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  p->mark("reconstruct");
+  p->last_rows = n_rows;
+  p->last_row0 = row0;
+  p->have_transform = true;
+}
+
+fkk_basis* export_basis(fkk_plan* p) {
+  auto b = std::make_unique<fkk_basis>();
+  cudaStream_t s = p->stream;
+  const int M = p->M, k = p->k, kp = p->kp;
+  b->M = M; b->k = k; b->kp = kp; b->L = p->L; b->pad = p->pad_zero; b->device = p->d.device;
+  b->ratio_floor = p->d.ratio_floor;
+  b->s = p->h_s;
+  b->inv_ref = dalloc<float>(M);
+  b->ref64 = dalloc<double>(M);
+  b->f64 = dalloc<double>(M);
+  b->W = dalloc<float>((size_t)M * kp);
+  b->Bi = dalloc<float>((size_t)k * M * 2);
+  b->V64 = dalloc<double>((size_t)M * k);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(b->inv_ref, p->inv_ref, M * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(b->ref64, p->ref64, M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(b->f64, p->f64, M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(b->Bi, p->Bi, (size_t)k * M * 2 * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(b->V64, p->V64, (size_t)M * k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // W_ml = D_f V diag(s^2/(s^2 + lam_ml)), lam_ml = ml_ridge_rel * s_1^2 (Eq. 25 closed form)
+  std::vector<double> c(k);
+  const double lam_ml = p->d.ml_ridge_rel * (k > 0 ? p->h_s[0] * p->h_s[0] : 0.0);
+  for (int i = 0; i < k; ++i) {
+    const double s2 = p->h_s[i] * p->h_s[i];
+    c[i] = s2 + lam_ml > 0 ? s2 / (s2 + lam_ml) : 0.0;
+  }
+  double* dc = dalloc<double>(k);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(dc, c.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  fkk::launch_cast_w(p->V64, p->f64, dc, M, k, kp, b->W, s);
+  FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(dc);
+  return b.release();
+}
+
+fkk_status fail(fkk_plan* p, int code, const std::string& msg) {
+  if (p) p->err = msg;
+  return (fkk_status)code;
+}
+
+template <typename F>
+fkk_status guarded(fkk_plan* p, F&& f) {
+  if (!p) return FKK_ERR_INVALID_ARG;
+  try {
+    p->err.clear();
+    f();
+    return FKK_OK;
+  } catch (const Status& e) {
+    return fail(p, e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(p, FKK_ERR_STATE, e.what());
+  }
+}
+
+void direct_run(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_iref, void* d_out) {
+  cudaStream_t s = p->stream;
+  const int M = p->M;
+  if (fkk::direct_finish_smem(M, p->L) > 227 * 1024) throw Status(FKK_ERR_NOT_IMPLEMENTED, "direct path: M/L too large for one CTA");
+  p->ensure_direct();
+  fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
+  const size_t oel = p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8;
+  for (int64_t b0 = 0; b0 < n_rows; b0 += p->direct_batch) {
+    const int64_t nb = std::min<int64_t>(p->direct_batch, n_rows - b0);
+    const char* in = static_cast<const char*>(d_icars) + (size_t)b0 * M * p->in_elem;
+    char* out = static_cast<char*>(d_out) + (size_t)b0 * M * oel;
+    fkk::launch_direct_phase(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->pad_zero,
+                             p->tw32, p->phi, p->flags, s);
+    p->mark("kk_phase");
+    fkk::launch_als_rows(p->phi, 0, nb, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->als_state, p->phierr, 0, s);
+    p->mark("als");
+    fkk::launch_direct_finish(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->pad_zero,
+                              p->tw32, p->phi, p->phierr, p->sg_half, out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+    p->mark("pec_sec");
+  }
+}
+
+void apply_run(fkk_plan* p, fkk_basis* b, const void* d_icars, int64_t n_rows, void* d_out) {
+  if (b->M != p->M || b->L != p->L || b->pad != p->pad_zero || b->k > p->k)
+    throw Status(FKK_ERR_INCOMPATIBLE_BASIS, "trained basis M/L/pad/k incompatible with the plan");
+  cudaStream_t s = p->stream;
+  const int M = p->M;
+  fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, b->inv_ref, b->ref64, (float)b->ratio_floor, p->A, p->flags, s);
+  p->mark("logratio");
+  fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
+  p->mark("project");
+  fkk::launch_reconstruct_simt(p->US, n_rows, b->k, b->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  p->mark("reconstruct");
+}
+
+void* ensure_dev(void*& buf, size_t& have, size_t need) {
+  if (have < need) {
+    if (buf) cudaFree(buf);
+    buf = dalloc<char>(need);
+    have = need;
+  }
+  return buf;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------------------
+extern "C" {
+
+void fkk_plan_desc_init(fkk_plan_desc* d, int32_t n_freq, int32_t rank_k, int64_t max_rows) {
+  if (!d) return;
+  std::memset(d, 0, sizeof(*d));
+  d->n_freq = n_freq;
+  d->rank_k = rank_k;
+  d->max_rows = max_rows;
+  d->fft_len = 0;
+  d->pad_mode = FKK_PAD_REFLECT;
+  d->ratio_floor = 1e-6;
+  d->f_mode = FKK_F_ONE;
+  d->f_alpha = 0.0;
+  d->f_sigma_g = 1.0;
+  d->als_lambda = 1e4;
+  d->als_p = 1e-3;
+  d->als_iters = 10;
+  d->sg_window = 0;
+  d->sg_order = 2;
+  d->ridge_rel = 1e-3;
+  d->ml_ridge_rel = 0.0;
+  d->gemm_impl = FKK_GEMM_FP32_SIMT;
+  d->out_layout = FKK_OUT_COMPLEX64;
+  d->in_dtype = FKK_IN_F32;
+  d->device = 0;
+  d->world_size = 1;
+  d->rank = 0;
+  d->nccl_id = nullptr;
+  d->loopback_shards = 0;
+}
+
+fkk_status fkk_get_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return FKK_ERR_INVALID_ARG;
+  std::string e;
+  if (!g_nccl.load(e)) return FKK_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return FKK_ERR_NCCL;
+  std::memcpy(out, &id, 128);
+  return FKK_OK;
+}
+
+static thread_local std::string g_create_err;
+
+fkk_status fkk_plan_create(const fkk_plan_desc* d, fkk_plan_t* out) {
+  if (!out) return FKK_ERR_INVALID_ARG;
+  *out = nullptr;
+  auto p = std::make_unique<fkk_plan>();
+  try {
+    create_plan(d, p.get());
+  } catch (const Status& e) {
+    g_create_err = e.what();
+    return (fkk_status)e.code;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return FKK_ERR_STATE;
+  }
+  *out = p.release();
+  return FKK_OK;
+}
+
+fkk_status fkk_plan_destroy(fkk_plan_t p) {
+  delete p;
+  return FKK_OK;
+}
+
+const char* fkk_last_error(fkk_plan_t p) { return p ? p->err.c_str() : g_create_err.c_str(); }
+
+fkk_status fkk_plan_set_stream(fkk_plan_t p, void* cuda_stream) {
+  return guarded(p, [&] {
+    if (p->own_stream && p->stream) { FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream)); cudaStreamDestroy(p->stream); }
+    if (cuda_stream) { p->stream = static_cast<cudaStream_t>(cuda_stream); p->own_stream = false; }
+    else { FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)); p->own_stream = true; }
+  });
+}
+
+fkk_status fkk_plan_sync(fkk_plan_t p) {
+  return guarded(p, [&] { p->check_flags_sync(); });
+}
+
+fkk_status fkk_svd(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, float* d_V_out,
+                   double* h_s_out) {
+  return guarded(p, [&] {
+    check_cube_args(p, d_icars, n_rows, d_iref, d_V_out);
+    if (!h_s_out) throw Status(FKK_ERR_INVALID_ARG, "h_s_out is NULL");
+    p->begin_call();
+    int64_t row0, ng;
+    exchange_rows(p, n_rows, row0, ng);
+    if (ng < p->k) throw Status(FKK_ERR_INVALID_ARG, "rank_k exceeds the global number of spectra");
+    svd_stage(p, d_icars, n_rows, d_iref, ng);
+    // fp32 column-major copy of V (the f-unscaled right singular vectors)
+    std::vector<double> hv((size_t)p->M * p->k);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), p->V64, hv.size() * 8, cudaMemcpyDeviceToHost, p->stream));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    std::vector<float> hf(hv.begin(), hv.end());
+    FKK_CUDA_CHECK(cudaMemcpyAsync(d_V_out, hf.data(), hf.size() * 4, cudaMemcpyHostToDevice, p->stream));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+    std::copy(p->h_s.begin(), p->h_s.end(), h_s_out);
+    p->end_call();
+  });
+}
+
+fkk_status fkk_transform(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, void* d_out,
+                         fkk_basis_t* basis_out) {
+  return guarded(p, [&] {
+    check_cube_args(p, d_icars, n_rows, d_iref, d_out);
+    if (basis_out) *basis_out = nullptr;
+    p->begin_call();
+    int64_t row0, ng;
+    exchange_rows(p, n_rows, row0, ng);
+    if (ng < p->k) throw Status(FKK_ERR_INVALID_ARG, "rank_k exceeds the global number of spectra");
+    p->last_global_rows = ng;
+    svd_stage(p, d_icars, n_rows, d_iref, ng);
+    transform_rest(p, n_rows, row0, nullptr, 0, d_out);
+    p->check_flags_sync();
+    if (basis_out) *basis_out = export_basis(p);
+    p->end_call();
+  });
+}
+
+fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, const float* d_V,
+                              const double* h_s, const int64_t* h_q, int32_t nq, void* d_out) {
+  return guarded(p, [&] {
+    check_cube_args(p, d_icars, n_rows, d_iref, d_out);
+    if (!d_V || !h_s || !h_q || nq < 1 || nq > p->nq_cap()) throw Status(FKK_ERR_INVALID_ARG, "bad V/s/q");
+    p->begin_call();
+    int64_t row0, ng;
+    exchange_rows(p, n_rows, row0, ng);
+    cudaStream_t s = p->stream;
+    const int M = p->M, k = p->k;
+    fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
+    fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
+    if (p->d.f_mode == FKK_F_EQ9) {
+      FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
+      fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);
+      if (p->d.world_size > 1) nccl_check(g_nccl.AllReduce(p->colsum, p->colsum, M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(colsum)");
+      fkk::launch_noise_scale_from_sums(p->colsum, M, 1.0 / (double)std::max<int64_t>(ng, 1), p->d.f_alpha, p->d.f_sigma_g, p->f64, p->f32, s);
+    } else {
+      fkk::launch_fill(p->f64, 1.0, M, s);
+      fkk::launch_fill_f(p->f32, 1.0f, M, s);
+    }
+    std::vector<float> hv((size_t)M * k);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), d_V, hv.size() * 4, cudaMemcpyDeviceToHost, s));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::vector<double> hd(hv.begin(), hv.end());
+    FKK_CUDA_CHECK(cudaMemcpyAsync(p->V64, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice, s));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    p->h_s.assign(h_s, h_s + k);
+    transform_rest(p, n_rows, row0, h_q, nq, d_out);
+    p->check_flags_sync();
+    p->end_call();
+  });
+}
+
+fkk_status fkk_apply_trained_basis(fkk_plan_t p, fkk_basis_t b, const void* d_icars, int64_t n_rows, void* d_out) {
+  return guarded(p, [&] {
+    if (!b) throw Status(FKK_ERR_INVALID_ARG, "basis is NULL");
+    check_cube_args(p, d_icars, n_rows, b->ref64, d_out);
+    p->begin_call();
+    apply_run(p, b, d_icars, n_rows, d_out);
+    p->end_call();
+  });
+}
+
+fkk_status kk_direct_batch(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, void* d_out) {
+  return guarded(p, [&] {
+    check_cube_args(p, d_icars, n_rows, d_iref, d_out);
+    p->begin_call();
+    direct_run(p, d_icars, n_rows, d_iref, d_out);
+    p->end_call();
+  });
+}
+
+fkk_status fkk_transform_host(fkk_plan_t p, const void* h_icars, int64_t n_rows, const void* h_iref, void* h_out,
+                              fkk_basis_t* basis_out) {
+  return guarded(p, [&] {
+    if (!h_icars || !h_iref || !h_out) throw Status(FKK_ERR_INVALID_ARG, "NULL host buffer");
+    if (n_rows < 0 || n_rows > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be in [0, max_rows]");
+    const size_t in_bytes = (size_t)n_rows * p->M * p->in_elem;
+    const size_t out_bytes = (size_t)n_rows * p->M * (p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8);
+    void* din = ensure_dev(p->d_in_cube, p->d_in_cube_bytes, in_bytes);
+    void* dout = ensure_dev(p->d_out_cube, p->d_out_cube_bytes, out_bytes);
+    if (!p->d_ref_buf) p->d_ref_buf = dalloc<double>(p->M);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(din, h_icars, in_bytes, cudaMemcpyHostToDevice, p->stream));
+    FKK_CUDA_CHECK(cudaMemcpyAsync(p->d_ref_buf, h_iref, (size_t)p->M * p->in_elem, cudaMemcpyHostToDevice, p->stream));
+    fkk_status st = fkk_transform(p, din, n_rows, p->d_ref_buf, dout, basis_out);
+    if (st != FKK_OK) throw Status(st, p->err);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, p->stream));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+fkk_status kk_direct_batch_host(fkk_plan_t p, const void* h_icars, int64_t n_rows, const void* h_iref, void* h_out) {
+  return guarded(p, [&] {
+    if (!h_icars || !h_iref || !h_out) throw Status(FKK_ERR_INVALID_ARG, "NULL host buffer");
+    if (n_rows < 0 || n_rows > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be in [0, max_rows]");
+    const size_t in_bytes = (size_t)n_rows * p->M * p->in_elem;
+    const size_t out_bytes = (size_t)n_rows * p->M * (p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8);
+    void* din = ensure_dev(p->d_in_cube, p->d_in_cube_bytes, in_bytes);
+    void* dout = ensure_dev(p->d_out_cube, p->d_out_cube_bytes, out_bytes);
+    if (!p->d_ref_buf) p->d_ref_buf = dalloc<double>(p->M);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(din, h_icars, in_bytes, cudaMemcpyHostToDevice, p->stream));
+    FKK_CUDA_CHECK(cudaMemcpyAsync(p->d_ref_buf, h_iref, (size_t)p->M * p->in_elem, cudaMemcpyHostToDevice, p->stream));
+    fkk_status st = kk_direct_batch(p, din, n_rows, p->d_ref_buf, dout);
+    if (st != FKK_OK) throw Status(st, p->err);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, p->stream));
+    p->check_flags_sync();
+  });
+}
+
+fkk_status fkk_apply_trained_basis_host(fkk_plan_t p, fkk_basis_t b, const void* h_icars, int64_t n_rows, void* h_out) {
+  return guarded(p, [&] {
+    if (!b || !h_icars || !h_out) throw Status(FKK_ERR_INVALID_ARG, "NULL argument");
+    if (n_rows < 0 || n_rows > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be in [0, max_rows]");
+    const size_t in_bytes = (size_t)n_rows * p->M * p->in_elem;
+    const size_t out_bytes = (size_t)n_rows * p->M * (p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8);
+    void* din = ensure_dev(p->d_in_cube, p->d_in_cube_bytes, in_bytes);
+    void* dout = ensure_dev(p->d_out_cube, p->d_out_cube_bytes, out_bytes);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(din, h_icars, in_bytes, cudaMemcpyHostToDevice, p->stream));
+    fkk_status st = fkk_apply_trained_basis(p, b, din, n_rows, dout);
+    if (st != FKK_OK) throw Status(st, p->err);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, p->stream));
+    p->check_flags_sync();
+  });
+}
+
+fkk_status fkk_basis_destroy(fkk_basis_t b) {
+  delete b;
+  return FKK_OK;
+}
+
+fkk_status fkk_basis_info(fkk_basis_t b, int32_t* n_freq, int32_t* rank_k, int32_t* fft_len) {
+  if (!b) return FKK_ERR_INVALID_ARG;
+  if (n_freq) *n_freq = b->M;
+  if (rank_k) *rank_k = b->k;
+  if (fft_len) *fft_len = b->L;
+  return FKK_OK;
+}
+
+size_t fkk_stage_size(fkk_plan_t p, int32_t stage) {
+  if (!p) return 0;
+  const size_t M = p->M, k = p->k, nq = p->h_q.size();
+  switch (stage) {
+    case FKK_STAGE_G: return M * M * 8;
+    case FKK_STAGE_S: return k * 8;
+    case FKK_STAGE_V: return M * k * 8;
+    case FKK_STAGE_US: return (size_t)p->last_rows * k * 4;
+    case FKK_STAGE_Q: return nq * 8;
+    case FKK_STAGE_HV: case FKK_STAGE_PHI_PEC: case FKK_STAGE_V_SEC: return k * M * 8;
+    case FKK_STAGE_PHI_ERR: return nq * M * 8;
+    case FKK_STAGE_B: return k * M * 2 * 4;
+    case FKK_STAGE_LAMBDA: return 8;
+    case FKK_STAGE_F: return M * 8;
+    default: return 0;
+  }
+}
+
+fkk_status fkk_get_stage(fkk_plan_t p, int32_t stage, void* dst, size_t bytes, int32_t dst_is_device) {
+  return guarded(p, [&] {
+    if (!dst) throw Status(FKK_ERR_INVALID_ARG, "dst is NULL");
+    const size_t n = std::min(bytes, fkk_stage_size(p, stage));
+    const void* src = nullptr;
+    bool host_src = false;
+    switch (stage) {
+      case FKK_STAGE_G: src = p->G; break;
+      case FKK_STAGE_S: src = p->h_s.data(); host_src = true; break;
+      case FKK_STAGE_V: src = p->V64; break;
+      case FKK_STAGE_US: src = p->US; break;
+      case FKK_STAGE_Q: src = p->h_q.data(); host_src = true; break;
+      case FKK_STAGE_HV: src = p->Hv; break;
+      case FKK_STAGE_PHI_ERR: src = p->Phi_err; break;
+      case FKK_STAGE_PHI_PEC: src = p->Phi_pec; break;
+      case FKK_STAGE_V_SEC: src = p->Vsec; break;
+      case FKK_STAGE_B: src = p->Bi; break;
+      case FKK_STAGE_LAMBDA: src = p->lam; break;
+      case FKK_STAGE_F: src = p->f64; break;
+      default: throw Status(FKK_ERR_INVALID_ARG, "unknown stage");
+    }
+    cudaMemcpyKind kind = host_src ? (dst_is_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost)
+                                   : (dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, kind, p->stream));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+fkk_status fkk_enable_timing(fkk_plan_t p, int32_t on) {
+  if (!p) return FKK_ERR_INVALID_ARG;
+  p->timing = on != 0;
+  return FKK_OK;
+}
+
+int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap) {
+  if (!p) return 0;
+  int32_t n = std::min<int32_t>(cap, (int32_t)p->t_ms.size());
+  for (int32_t i = 0; i < n; ++i) {
+    if (names) names[i] = p->t_names[i].c_str();
+    if (ms) ms[i] = p->t_ms[i];
+  }
+  return n;
+}
+
+int64_t fkk_last_launch_count(fkk_plan_t p) { return p ? p->launches : 0; }
+
+fkk_status fkk_host_eig_topk(const double* G, int32_t M, int32_t k, double* V, double* lam) {
+  if (!G || !V || !lam || M < 1 || k < 1 || k > M) return FKK_ERR_INVALID_ARG;
+  try {
+    return fkk::host_eig_topk(G, M, k, V, lam) == 0 ? FKK_OK : FKK_ERR_NUMERICAL;
+  } catch (...) {
+    return FKK_ERR_NUMERICAL;
+  }
+}
+
+void fkk_shard_range(int64_t n_global, int32_t world, int32_t rank, int64_t* row0, int64_t* row1) {
+  if (world < 1) world = 1;
+  const int64_t base = n_global / world, rem = n_global % world;
+  const int64_t r0 = rank * base + std::min<int64_t>(rank, rem);
+  const int64_t len = base + (rank < rem ? 1 : 0);
+  if (row0) *row0 = r0;
+  if (row1) *row1 = r0 + len;
+}
+
+int32_t fkk_merge_extremes(const float* vals, const int64_t* idx, int32_t world, int32_t k, int64_t* q_out) {
+  std::vector<int64_t> q;
+  q.reserve(2 * k);
+  for (int c = 0; c < k; ++c) {
+    float bM = -INFINITY, bm = INFINITY;
+    int64_t iM = INT64_MAX, im = INT64_MAX;
+    for (int r = 0; r < world; ++r) {
+      const size_t o = ((size_t)r * k + c) * 2;
+      if (idx[o] != INT64_MAX && (vals[o] > bM || (vals[o] == bM && idx[o] < iM))) { bM = vals[o]; iM = idx[o]; }
+      if (idx[o + 1] != INT64_MAX && (vals[o + 1] < bm || (vals[o + 1] == bm && idx[o + 1] < im))) { bm = vals[o + 1]; im = idx[o + 1]; }
+    }
+    if (iM != INT64_MAX) q.push_back(iM);
+    if (im != INT64_MAX) q.push_back(im);
+  }
+  std::sort(q.begin(), q.end());
+  q.erase(std::unique(q.begin(), q.end()), q.end());
+  std::copy(q.begin(), q.end(), q_out);
+  return (int32_t)q.size();
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal declarations of the fKK-EC runtime: kernel launchers (one per .cu file) and the host
+// eigensolver.  Everything here is C++; the public surface is include/fkk.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace fkk {
+
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FKK_CUDA_CHECK(expr)                                                                     \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      throw ::fkk::Status(7, std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " +     \
+                                 __FILE__ + ":" + std::to_string(__LINE__) + " (" #expr ")");    \
+  } while (0)
+
+// Launch counter (the bench reports kernel launches per call).
+extern thread_local int64_t g_launches;
+inline void count_launch(int n = 1) { g_launches += n; }
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Status(7, std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
+  count_launch();
+}
+
+// ---- reference / log-ratio prerequisites (k_misc.cu)
+// inv_ref[j] = 1/I_ref[j] (fp32), ref64[j] = I_ref[j] (fp64); flags |= 1 if any I_ref <= 0 or non-finite.
+void launch_prep_ref(const void* d_iref, int in_f64, int M, float* inv_ref, double* ref64, int* flags, cudaStream_t s);
+// A0 = 1/2 ln(max(I/I_ref, floor)) (fp32, n x M); flags |= 2 on non-finite input.
+void launch_logratio(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
+                     float floor, float* A, int* flags, cudaStream_t s);
+void launch_colsum(const void* I, int in_f64, int64_t n, int M, double* colsum, cudaStream_t s);
+void launch_noise_scale_from_sums(const double* colsum, int M, double inv_n, double alpha, double sg, double* f64,
+                                  float* f32, cudaStream_t s);
+void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
+void launch_fill_f(float* p, float v, int64_t n, cudaStream_t s);
+void launch_scale_gram(double* G, const double* f, int M, cudaStream_t s);
+void launch_cast_w(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* W,
+                   cudaStream_t s);
+void launch_gather_rows(const float* US, int k, const int64_t* q_local, int nq, double* X, cudaStream_t s);
+void launch_extremes_reduce(const float* ext_val, const int64_t* ext_idx, int nblk, int k, float* out_val,
+                            int64_t* out_idx, cudaStream_t s);
+void launch_add_f64(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
+
+// ---- direct path (k_direct.cu)
+void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
+                         float floor, int L, int pad_zero, const float2* tw, float* phi, int* flags, cudaStream_t s);
+// ALS on rows of y (fp32 or fp64, row-major n x M) -> z (fp32 or fp64); state: 3*M*nb doubles, nb = 32*ceil(n/32)
+void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, double* state,
+                     void* z, int z_f64, cudaStream_t s);
+void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
+                          float floor, int L, int pad_zero, const float2* tw, const float* phi, const float* phierr,
+                          int sg_half, void* out, int out_imag_only, cudaStream_t s);
+size_t direct_finish_smem(int M, int L);
+
+// ---- factorized path
+// Gram partials (k_gram.cu): 128 x 128 tiles of the upper triangle, nsplit row segments each.
+int gram_num_tiles(int M);
+int gram_num_splits(int64_t n, int M);
+void launch_gram_simt(const float* A, int64_t n, int M, double* partials, int nsplit, cudaStream_t s);
+void launch_gram_reduce(const double* partials, int nsplit, int M, double* G, int accumulate, cudaStream_t s);
+// Projection US = A0 W (k_project.cu) with per-block column extremes [blk][c][2].
+int project_num_blocks(int64_t n);
+void launch_project_simt(const float* A, int64_t n, int M, const float* W, int k, int kp, float* US, float* ext_val,
+                         int64_t* ext_idx, int64_t row_offset, cudaStream_t s);
+// Reconstruction K = exp(US B_amp) e^{i US B_ph} (k_reconstruct.cu); Bi: k x M x 2 (amp, ph).
+void launch_reconstruct_simt(const float* US, int64_t n, int k, const float* Bi, int M, void* out, int out_imag_only,
+                             cudaStream_t s);
+// Basis (k_basis.cu): all fp64, tiny.
+void launch_hilbert_rows_f64(const double* X, int rows, int M, int ldx, double* out, int L, int pad_zero,
+                             const double2* tw, cudaStream_t s);
+void launch_sg_rows_f64(const double* X, int rows, int M, int h, double* out, cudaStream_t s);
+// C[m x n] = alpha * op(A) op(B) (+ beta C); row-major; op = transpose if flag.
+void launch_dgemm_small(int m, int n, int kk, const double* A, int lda, int ta, const double* B, int ldb, int tb,
+                        double* C, int ldc, double beta, cudaStream_t s);
+void launch_vt_over_f(const double* V /* M x k col-major */, const double* f, int M, int k, double* Vt_f,
+                      cudaStream_t s);
+// ridge: solve (C + lam I) Phi = R with lam = ridge_rel * lambda_max(C); writes lam to lam_out.
+void launch_ridge(const double* C, int k, const double* R, int ncol, double ridge_rel, double* Phi, double* lam_out,
+                  double* work, int* flags, cudaStream_t s);
+void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vsec, const double* Hv,
+                       const double* Phi_pec, int k, int M, float* Bi, cudaStream_t s);
+
+// ---- host eigensolver (host_eig.cpp): returns 0 on success
+int host_eig_topk(const double* G, int M, int k, double* V /* k vectors of length M */, double* lam);
+
+}  // namespace fkk

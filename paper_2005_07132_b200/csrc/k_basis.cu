@@ -1,0 +1,234 @@
+// Basis-level steps F6..F10 of fKK-EC, all fp64 (k <= 128 rows of length M; latency-bound, tiny):
+//   hilbert_rows : H{.} row-wise (Eq. 11 H{V^T/f}, Eq. 18 H{Phi_PEC}), fp64 FFT in smem
+//   sg_rows      : trendline M{.} row-wise (Eq. 22), fp64 moment prefix sums
+//   dgemm_small  : P = X H{V^T/f} (Eq. 16), X^T X and X^T Phi_err (Eq. 17)
+//   ridge        : Phi_PEC^T = (X^T X + lam I)^{-1} X^T Phi_err, lam = ridge_rel lambda_max(X^T X)
+//                  (Eq. 17, reading A11); lambda_max by normalised repeated squaring, Cholesky solve
+//   assemble_B   : B_amp = V^T/f + H{Phi_PEC} - V_SEC^T, B_ph = H{V^T/f} - Phi_PEC^T (Eq. 23)
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "device_common.cuh"
+#include <algorithm>
+
+#include "fkk_internal.h"
+
+namespace fkk {
+
+namespace {
+
+__global__ void __launch_bounds__(256) hilbert_rows_f64_kernel(const double* __restrict__ X, int rows, int M, int ldx,
+                                                               double* __restrict__ out, int L, int log2L,
+                                                               int pad_zero, const double2* __restrict__ tw_g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cplx<double>* tw = reinterpret_cast<cplx<double>*>(smem);
+  cplx<double>* x = tw + (L >> 1);
+  for (int j = threadIdx.x; j < (L >> 1); j += blockDim.x) { double2 t = tw_g[j]; tw[j].x = t.x; tw[j].y = t.y; }
+  const int r0 = 2 * blockIdx.x, r1 = r0 + 1;
+  const double* x0 = X + (int64_t)r0 * ldx;
+  const double* x1 = (r1 < rows) ? X + (int64_t)r1 * ldx : x0;
+  __syncthreads();
+  pad_pair<double, double>(x, x0, x1, M, L, pad_zero);
+  hilbert_pair_inplace<double>(x, tw, L, log2L);
+  const int pl = (L - M) >> 1;
+  const double invL = 1.0 / (double)L;
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    out[(int64_t)r0 * M + j] = x[pl + j].x * invL;
+    if (r1 < rows) out[(int64_t)r1 * M + j] = x[pl + j].y * invL;
+  }
+}
+
+__global__ void __launch_bounds__(256) sg_rows_f64_kernel(const double* __restrict__ X, int M, int h,
+                                                          double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* P0 = reinterpret_cast<double*>(smem);
+  double* P1 = P0 + (M + 1);
+  double* P2 = P1 + (M + 1);
+  double* wsum = P2 + (M + 1);
+  const double* y = X + (int64_t)blockIdx.x * M;
+  block_prefix3(y, M, P0, P1, P2, wsum);
+  for (int j = threadIdx.x; j < M; j += blockDim.x) out[(int64_t)blockIdx.x * M + j] = sg_point(P0, P1, P2, M, h, j);
+}
+
+__global__ void dgemm_small_kernel(int m, int n, int kk, const double* __restrict__ A, int lda, int ta,
+                                   const double* __restrict__ B, int ldb, int tb, double* __restrict__ C, int ldc,
+                                   double beta) {
+  const int64_t total = (int64_t)m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    double s = 0.0;
+    for (int t = 0; t < kk; ++t) {
+      const double a = ta ? A[(int64_t)t * lda + i] : A[(int64_t)i * lda + t];
+      const double b = tb ? B[(int64_t)j * ldb + t] : B[(int64_t)t * ldb + j];
+      s = fma(a, b, s);
+    }
+    C[(int64_t)i * ldc + j] = (beta == 0.0 ? 0.0 : beta * C[(int64_t)i * ldc + j]) + s;
+  }
+}
+
+// Single CTA: lambda_max(C) by normalised repeated squaring, then the Cholesky factor of C + lam I
+// in Lw (lower, row-major k x k).  work: 2 k x k buffers.
+__global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __restrict__ C, int k, double ridge_rel,
+                                                            double* __restrict__ Lw, double* __restrict__ work,
+                                                            double* __restrict__ lam_out, int* __restrict__ flags) {
+  __shared__ double red[32];
+  __shared__ double sh_scal[2];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int kk = k * k;
+  double* B0 = work;
+  double* B1 = work + kk;
+  // trace
+  double t = 0.0;
+  for (int i = tid; i < k; i += nt) t += C[i * k + i];
+  t = warp_sum(t);
+  if (lane == 0) red[wid] = t;
+  __syncthreads();
+  if (tid == 0) { double s = 0; for (int w2 = 0; w2 < nt / 32; ++w2) s += red[w2]; sh_scal[0] = s; }
+  __syncthreads();
+  const double tr = sh_scal[0];
+  double loglam = log(tr > 0 ? tr : 1e-300);
+  for (int e = tid; e < kk; e += nt) B0[e] = C[e] / tr;
+  __syncthreads();
+  double wgt = 0.5;
+  for (int it = 0; it < 40; ++it) {
+    for (int e = tid; e < kk; e += nt) {
+      const int i = e / k, j = e % k;
+      double s = 0.0;
+      for (int q = 0; q < k; ++q) s = fma(B0[i * k + q], B0[q * k + j], s);
+      B1[e] = s;
+    }
+    __syncthreads();
+    double tl = 0.0;
+    for (int i = tid; i < k; i += nt) tl += B1[i * k + i];
+    tl = warp_sum(tl);
+    if (lane == 0) red[wid] = tl;
+    __syncthreads();
+    if (tid == 0) { double s = 0; for (int w2 = 0; w2 < nt / 32; ++w2) s += red[w2]; sh_scal[1] = s; }
+    __syncthreads();
+    const double c = sh_scal[1] > 0 ? sh_scal[1] : 1e-300;
+    loglam += wgt * log(c);
+    wgt *= 0.5;
+    for (int e = tid; e < kk; e += nt) B0[e] = B1[e] / c;
+    __syncthreads();
+  }
+  // lambda_max(B_T) ~ ||B_T||_F (between lambda_max and sqrt(rank) lambda_max); weight 2^-40
+  double fr = 0.0;
+  for (int e = tid; e < kk; e += nt) fr += B0[e] * B0[e];
+  fr = warp_sum(fr);
+  if (lane == 0) red[wid] = fr;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0; for (int w2 = 0; w2 < nt / 32; ++w2) s += red[w2];
+    const double lmax = exp(loglam + 2.0 * wgt * log(sqrt(s > 0 ? s : 1e-300)));
+    sh_scal[0] = ridge_rel * lmax;
+    lam_out[0] = sh_scal[0];
+  }
+  __syncthreads();
+  const double lam = sh_scal[0];
+  for (int e = tid; e < kk; e += nt) { const int i = e / k, j = e % k; Lw[e] = (j <= i) ? C[e] + (i == j ? lam : 0.0) : 0.0; }
+  __syncthreads();
+  // right-looking Cholesky, lower triangle
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const double d = Lw[j * k + j];
+      if (!(d > 0.0)) { atomicOr(flags, 4); Lw[j * k + j] = 1e-300; }
+      else Lw[j * k + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double djj = Lw[j * k + j];
+    for (int i = j + 1 + tid; i < k; i += nt) Lw[i * k + j] /= djj;
+    __syncthreads();
+    const int rem = k - j - 1;
+    for (int e = tid; e < rem * rem; e += nt) {
+      const int i = j + 1 + e / rem, c = j + 1 + e % rem;
+      if (c <= i) Lw[i * k + c] -= Lw[i * k + j] * Lw[c * k + j];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void ridge_solve_kernel(const double* __restrict__ Lw, int k, const double* __restrict__ R, int ncol,
+                                   double* __restrict__ Phi) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncol) return;
+  // forward L y = r, backward L^T x = y; y/x stored in Phi column j
+  for (int i = 0; i < k; ++i) {
+    double s = R[(int64_t)i * ncol + j];
+    for (int q = 0; q < i; ++q) s -= Lw[i * k + q] * Phi[(int64_t)q * ncol + j];
+    Phi[(int64_t)i * ncol + j] = s / Lw[i * k + i];
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double s = Phi[(int64_t)i * ncol + j];
+    for (int q = i + 1; q < k; ++q) s -= Lw[q * k + i] * Phi[(int64_t)q * ncol + j];
+    Phi[(int64_t)i * ncol + j] = s / Lw[i * k + i];
+  }
+}
+
+__global__ void assemble_B_kernel(const double* Vt_f, const double* HPhi, const double* Vsec, const double* Hv,
+                                  const double* Phi, int k, int M, float* Bi) {
+  const int64_t total = (int64_t)k * M;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    Bi[2 * e] = (float)(Vt_f[e] + HPhi[e] - Vsec[e]);
+    Bi[2 * e + 1] = (float)(Hv[e] - Phi[e]);
+  }
+}
+
+__global__ void vt_over_f_kernel(const double* V, const double* f, int M, int k, double* Vt_f) {
+  const int64_t total = (int64_t)k * M;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % M);
+    Vt_f[e] = V[e] / f[j];
+  }
+}
+
+inline int ilog2(int L) { int r = 0; while ((1 << r) < L) ++r; return r; }
+
+}  // namespace
+
+void launch_hilbert_rows_f64(const double* X, int rows, int M, int ldx, double* out, int L, int pad_zero,
+                             const double2* tw, cudaStream_t s) {
+  if (rows <= 0) return;
+  const size_t smem = (size_t)(L / 2 + L) * sizeof(double2);
+  cudaFuncSetAttribute(hilbert_rows_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  hilbert_rows_f64_kernel<<<(rows + 1) / 2, 256, smem, s>>>(X, rows, M, ldx, out, L, ilog2(L), pad_zero, tw);
+  check_launch("hilbert_rows_f64");
+}
+
+void launch_sg_rows_f64(const double* X, int rows, int M, int h, double* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  const size_t smem = (size_t)(3 * (M + 1) + 96) * sizeof(double);
+  cudaFuncSetAttribute(sg_rows_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  sg_rows_f64_kernel<<<rows, 256, smem, s>>>(X, M, h, out);
+  check_launch("sg_rows_f64");
+}
+
+void launch_dgemm_small(int m, int n, int kk, const double* A, int lda, int ta, const double* B, int ldb, int tb,
+                        double* C, int ldc, double beta, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return;
+  const int64_t total = (int64_t)m * n;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  dgemm_small_kernel<<<grid, 256, 0, s>>>(m, n, kk, A, lda, ta, B, ldb, tb, C, ldc, beta);
+  check_launch("dgemm_small");
+}
+
+void launch_ridge(const double* C, int k, const double* R, int ncol, double ridge_rel, double* Phi, double* lam_out,
+                  double* work, int* flags, cudaStream_t s) {
+  double* Lw = work;
+  ridge_factor_kernel<<<1, 1024, 0, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags);
+  check_launch("ridge_factor");
+  ridge_solve_kernel<<<(ncol + 127) / 128, 128, 0, s>>>(Lw, k, R, ncol, Phi);
+  check_launch("ridge_solve");
+}
+
+void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vsec, const double* Hv,
+                       const double* Phi_pec, int k, int M, float* Bi, cudaStream_t s) {
+  assemble_B_kernel<<<256, 256, 0, s>>>(Vt_f, HPhi, Vsec, Hv, Phi_pec, k, M, Bi);
+  check_launch("assemble_B");
+}
+
+void launch_vt_over_f(const double* V, const double* f, int M, int k, double* Vt_f, cudaStream_t s) {
+  vt_over_f_kernel<<<256, 256, 0, s>>>(V, f, M, k, Vt_f);
+  check_launch("vt_over_f");
+}
+
+}  // namespace fkk

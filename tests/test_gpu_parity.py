@@ -1,0 +1,191 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the same seeded cubes.
+
+Tolerances (BASELINE.json north_star):
+  direct KK           max_n ||K_gpu - K_or||_inf / ||K_or||_inf <= 1e-5
+  factorized, stages  G, s, US relative <= 1e-5; F6..F11 from the GPU's (V, s, q): Im K <= 1e-4
+  factorized, e2e     max|Im K_gpu - Im K_or| / max|Im K_or| <= 1e-3 (q must agree)
+"""
+import numpy as np
+import pytest
+
+from oracle import fkk_oracle as O
+from synth import CONFIGS, generate
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda(cuda_ok):
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def fkk():
+    from paper_2005_07132_b200 import fkk
+    return fkk
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _rel_inf(K, R):
+    return np.max(np.max(np.abs(K - R), axis=1) / np.max(np.abs(R), axis=1))
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    I, Iref, _ = generate(CONFIGS["cfg1"])
+    return I, Iref
+
+
+# ------------------------------------------------------------------------- direct path -----------
+@pytest.mark.parametrize("pad", ["reflect", "zero"])
+@pytest.mark.parametrize("rows", [1, 33, 301])
+def test_direct_cfg1_f64_input(torch_cuda, fkk, cfg1, pad, rows):
+    I, Iref = cfg1
+    I = I[:rows]
+    p = O.Params(pad=pad)
+    K_or = O.kk_direct(I, Iref, p)
+    plan = fkk.Plan(512, 12, rows, pad=pad, in_dtype="f64")
+    K = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    assert _rel_inf(K, K_or) <= 1e-5
+
+
+def test_direct_cfg2_sample_f32(torch_cuda, fkk):
+    I, Iref, _ = generate(CONFIGS["cfg2"])
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(I.shape[0], 200, replace=False))
+    plan = fkk.Plan(1000, 40, I.shape[0])
+    K = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    K_or = O.kk_direct(I[rows].astype(np.float64), Iref.astype(np.float64), O.Params())
+    assert _rel_inf(K[rows], K_or) <= 1e-5
+    # imag-only layout gives the same Im part
+    plan_i = fkk.Plan(1000, 40, 4096, imag_only=True)
+    Ki = plan_i.direct(_dev(torch_cuda, I[:4096]), _dev(torch_cuda, Iref)).cpu().numpy()
+    assert np.array_equal(Ki, K[:4096].imag)
+
+
+def test_direct_passthrough_and_scale(torch_cuda, fkk):
+    rng = np.random.default_rng(1)
+    Iref = rng.uniform(0.5, 1.5, 1000).astype(np.float32)
+    I = np.stack([Iref, 2.5 * Iref]).astype(np.float32)
+    plan = fkk.Plan(1000, 8, 2)
+    K = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    assert np.max(np.abs(K - 1.0)) < 1e-5
+
+
+def test_errors_reported(torch_cuda, fkk, cfg1):
+    I, Iref = cfg1
+    plan = fkk.Plan(512, 12, 64, in_dtype="f64")
+    bad = Iref.copy()
+    bad[7] = -1.0
+    with pytest.raises(fkk.FkkError) as e:
+        plan.transform(_dev(torch_cuda, I[:64]), _dev(torch_cuda, bad))
+    assert e.value.name == "FKK_ERR_BAD_REFERENCE"
+    In = I[:64].copy()
+    In[3, 5] = np.nan
+    with pytest.raises(fkk.FkkError) as e:
+        plan.transform(_dev(torch_cuda, In), _dev(torch_cuda, Iref))
+    assert e.value.name == "FKK_ERR_NONFINITE_INPUT"
+    # the plan stays usable after an error
+    plan.transform(_dev(torch_cuda, I[:64]), _dev(torch_cuda, Iref))
+
+
+# ------------------------------------------------------------------------- factorized path -------
+def _factorized_check(torch, fkk, I, Iref, k, *, e2e_tol=1e-3, loopback=0, in_dtype="f32"):
+    p = O.Params()
+    plan = fkk.Plan(I.shape[1], k, I.shape[0], in_dtype=in_dtype, loopback_shards=loopback)
+    Id, Rd = _dev(torch, I), _dev(torch, Iref)
+    K = plan.transform(Id, Rd).cpu().numpy()
+    G_gpu, s_gpu, V_gpu, US_gpu = plan.stage("G"), plan.stage("S"), plan.stage("V"), plan.stage("US")
+    q_gpu = plan.stage("Q")
+    A = O.log_ratio(I, Iref, p)
+    # stage-wise: Gram, singular values, projection with the GPU's V
+    G_or = O.gram(A)
+    assert np.max(np.abs(G_gpu - G_or)) / np.max(np.abs(G_or)) <= 1e-5
+    V_or, s_or, lam = O.eig_topk(G_or, k)
+    assert np.max(np.abs(s_gpu - s_or) / s_or) <= 1e-5
+    US_ref = A @ V_gpu
+    assert np.max(np.abs(US_gpu - US_ref)) / np.max(np.abs(US_ref)) <= 1e-5
+    gap = (lam[k - 1] - lam[k]) / lam[k - 1]
+    # F6..F11 from the GPU's (V, s, q): the oracle on the same inputs
+    V32 = V_gpu.astype(np.float32).astype(np.float64)
+    out_from = O.fkk_ec_from(I, Iref, V32, s_gpu, q_gpu, p)
+    K_from = plan.transform_from(Id, Rd, _dev(torch, np.ascontiguousarray(V32.T.astype(np.float32))), s_gpu,
+                                 q_gpu).cpu().numpy()
+    im_err_from = np.max(np.abs(K_from.imag - out_from["K"].imag)) / np.max(np.abs(out_from["K"].imag))
+    assert im_err_from <= 1e-4, im_err_from
+    # end to end
+    out = O.fkk_ec(I, Iref, k, p)
+    same_q = np.array_equal(out["q"], q_gpu)
+    im_err = np.max(np.abs(K.imag - out["K"].imag)) / np.max(np.abs(out["K"].imag))
+    diag = dict(gap=gap, same_q=same_q, im_err=im_err, im_err_from=im_err_from)
+    assert same_q, diag
+    assert im_err <= e2e_tol, diag
+    return plan, K, diag
+
+
+def test_factorized_cfg1(torch_cuda, fkk, cfg1):
+    I, Iref = cfg1
+    _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64")
+
+
+def test_factorized_cfg1_loopback_shards_invariant(torch_cuda, fkk, cfg1):
+    I, Iref = cfg1
+    plan1, K1, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64")
+    plan3, K3, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64", loopback=3)
+    assert np.array_equal(plan1.stage("Q"), plan3.stage("Q"))
+    assert np.max(np.abs(K1 - K3)) / np.max(np.abs(K1)) < 1e-4
+
+
+def test_factorized_ragged_small(torch_cuda, fkk, cfg1):
+    I, Iref = cfg1
+    _factorized_check(torch_cuda, fkk, I[:777], Iref, 12, in_dtype="f64")
+
+
+def test_factorized_cfg2(torch_cuda, fkk):
+    I, Iref, _ = generate(CONFIGS["cfg2"])
+    _factorized_check(torch_cuda, fkk, I, Iref, 40)
+
+
+# ------------------------------------------------------------------------- ML reuse --------------
+def test_ml_apply_matches_oracle_and_self_consistent(torch_cuda, fkk):
+    cfg = CONFIGS["cfg5_train"].with_(height=64, width=64)
+    I, Iref, _ = generate(cfg)
+    Ia, _, _ = generate(CONFIGS["cfg5_apply"].with_(height=48, width=40))
+    k = 20
+    plan = fkk.Plan(1000, k, I.shape[0])
+    K_train, basis = plan.transform(_dev(torch_cuda, I), _dev(torch_cuda, Iref), return_basis=True)
+    # oracle model from the GPU's V, s, q (stage-wise) and apply on the new cube
+    V = plan.stage("V").astype(np.float32).astype(np.float64)
+    s = plan.stage("S")
+    q = plan.stage("Q")
+    p = O.Params()
+    out = O.fkk_ec_from(I, Iref, V, s, q, p)
+    model = dict(f=out["f"], W=O.ml_projector(V, s, p), B_amp=out["B_amp"], B_ph=out["B_ph"])
+    Ka = plan.apply(basis, _dev(torch_cuda, Ia)).cpu().numpy()
+    Ka_or = O.ml_apply(Ia.astype(np.float64), Iref.astype(np.float64), model, p)
+    assert np.max(np.abs(Ka.imag - Ka_or.imag)) / np.max(np.abs(Ka_or.imag)) <= 1e-4
+    # lambda_ml = 0: applying to the training cube reproduces the training output (P14)
+    Kt = plan.apply(basis, _dev(torch_cuda, I)).cpu().numpy()
+    assert np.max(np.abs(Kt - K_train.cpu().numpy())) / np.max(np.abs(Kt)) <= 1e-4
+    assert basis.info() == dict(n_freq=1000, rank_k=k, fft_len=2048)
+    # incompatible basis
+    plan2 = fkk.Plan(512, 12, 10)
+    with pytest.raises(fkk.FkkError) as e:
+        plan2.apply(basis, _dev(torch_cuda, np.ones((4, 512), np.float32)))
+    assert e.value.name == "FKK_ERR_INCOMPATIBLE_BASIS"
+
+
+def test_host_buffer_variants(torch_cuda, fkk, cfg1):
+    I, Iref = cfg1
+    plan = fkk.Plan(512, 12, I.shape[0], in_dtype="f64")
+    K_dev = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    out = np.empty((I.shape[0], 512), np.complex64)
+    plan.direct_host(I, Iref, out)
+    assert np.array_equal(out, K_dev)
+    Kt_dev = plan.transform(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    plan.transform_host(I, Iref, out)
+    assert np.max(np.abs(out - Kt_dev)) <= 1e-6 * np.max(np.abs(Kt_dev))
