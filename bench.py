@@ -1,0 +1,322 @@
+"""bench.py -- throughput of the fKK-EC hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3]
+
+A step is one pass of the hot path over the configuration-3 image (703,026 spectra x 1,000
+channels, k = 60; BASELINE.json configs[2]): the full factorized fKK-EC transform F0..F11 through
+the C-ABI (fkk_transform) on device-resident inputs.  `value` = spectra/s of that transform, whole
+job (N GPUs shard the pixels of the same image: strong scaling).  In the same run the two other hot
+paths are timed and reported as sub-objects: the direct per-spectrum KK+PEC+SEC (kk_direct_batch)
+on the same image, and ML:fKK-EC apply (fkk_apply_trained_basis, BASELINE.json configs[4]).
+
+Multi-GPU: launched by torchrun, one rank per GPU; NCCL unique id bootstrap through
+torch.distributed; barrier + max over ranks of the device-timed step.
+The oracle (oracle/, test infrastructure) is executed only in the cpu_baseline leg (rank 0,
+N=1) and in --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spectra/s for full fKK-EC (and direct KK) at 1/2/4/8 B200; % HBM/TC roofline"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world: int):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def run_ours(args) -> dict:
+    import torch
+
+    from paper_2005_07132_b200 import fkk
+    from synth import CONFIGS, generate_rows
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [fkk.fkk_get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    cfg = CONFIGS[args.workload]
+    N, M, k = cfg.n_pixels, cfg.n_freq, cfg.rank_k
+    r0, r1 = fkk.fkk_shard_range(N, world, rank)
+    n_loc = r1 - r0
+    I_h, Iref_h, _ = generate_rows(cfg, r0, r1)
+    I = torch.from_numpy(I_h).cuda()
+    Iref = torch.from_numpy(Iref_h).cuda()
+    out = torch.empty((n_loc, M), dtype=torch.complex64, device="cuda")
+    plan = fkk.Plan(M, k, n_loc, timing=True, world_size=world, rank=rank, nccl_id=nccl_id, device=local)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- fKK-EC (the headline) ----------------
+    for _ in range(args.warmup):
+        plan.transform(I, Iref, out)
+    _barrier(world)
+    stage_acc: dict = {}
+    launches = 0
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        _barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.transform(I, Iref, out)
+            for kk, v in plan.stage_times().items():
+                stage_acc[kk] = stage_acc.get(kk, 0.0) + v
+            launches += plan.launches
+        ev1.record(stream)
+        _barrier(world)
+    t_loc = ev0.elapsed_time(ev1) / args.steps
+    t = _max_over_ranks(t_loc, world)
+    stage_ms = {kk: v / args.steps for kk, v in stage_acc.items()}
+    value = N / (t / 1e3)
+
+    # roofline of the dominant GPU kernel (the Gram): algorithmic flops N*M^2 (syrk)
+    peaks, src = _peaks()
+    gram_ms = stage_ms.get("gram", float("nan"))
+    gram_flops = float(n_loc) * M * M
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # TFLOP/s, CUDA-core FP32
+    achieved = gram_flops / (gram_ms / 1e3) / 1e12
+    roofline = {"kernel": "gram (F2, fp32 CUDA-core SIMT)", "bound": "alu", "achieved": achieved,
+                "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
+
+    # ---------------- direct KK (same image) ----------------
+    plan.direct(I, Iref, out)
+    _barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    nd = max(1, min(args.steps, 3))
+    e0.record(stream)
+    for _ in range(nd):
+        plan.direct(I, Iref, out)
+    e1.record(stream)
+    _barrier(world)
+    td = _max_over_ranks(e0.elapsed_time(e1) / nd, world)
+    direct_stage = plan.stage_times()
+
+    # ---------------- ML:fKK-EC apply (config 5) ----------------
+    ml = None
+    if not args.skip_ml:
+        tr = CONFIGS["cfg5_train"]
+        ap = CONFIGS["cfg5_apply"]
+        It_h, Rt_h, _ = generate_rows(tr, 0, tr.n_pixels)
+        ptrain = fkk.Plan(tr.n_freq, tr.rank_k, tr.n_pixels, device=local)
+        _, basis = ptrain.transform(torch.from_numpy(It_h).cuda(), torch.from_numpy(Rt_h).cuda(), return_basis=True)
+        del ptrain
+        a0, a1 = fkk.fkk_shard_range(ap.n_pixels, world, rank)
+        Ia_h, _, _ = generate_rows(ap, a0, a1)
+        Ia = torch.from_numpy(Ia_h).cuda()
+        batch = 50000
+        papply = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local)
+        oa = torch.empty((batch, ap.n_freq), dtype=torch.complex64, device="cuda")
+        for b0 in range(0, min(a1 - a0, batch), batch):
+            papply.apply(basis, Ia[b0:b0 + batch], oa[: min(batch, a1 - a0 - b0)])
+        _barrier(world)
+        e0.record(stream)
+        nb = 0
+        for b0 in range(0, a1 - a0, batch):
+            nbb = min(batch, a1 - a0 - b0)
+            papply.apply(basis, Ia[b0:b0 + nbb], oa[:nbb])
+            nb += 1
+        e1.record(stream)
+        _barrier(world)
+        tm = _max_over_ranks(e0.elapsed_time(e1), world)
+        ml = {"value": ap.n_pixels / (tm / 1e3), "unit": "spectra/s", "ms_per_pass": tm,
+              "batches": nb, "ms_per_batch": tm / max(nb, 1), "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches"}
+        del Ia, papply
+
+    # ---------------- end to end through the host-buffer C-ABI ----------------
+    e2e = None
+    if not args.skip_e2e:
+        Ih = torch.from_numpy(I_h).pin_memory()
+        Rh = torch.from_numpy(Iref_h).pin_memory()
+        Oh = torch.empty((n_loc, M), dtype=torch.complex64).pin_memory()
+        plan.transform_host(Ih, Rh, Oh)
+        ne = max(1, min(args.steps, 2))
+        _barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            plan.transform_host(Ih, Rh, Oh)
+        _barrier(world)
+        te = _max_over_ranks((time.perf_counter() - t0) / ne, world)
+        e2e = {"value": N / te, "unit": "spectra/s", "h2d_bytes_per_step": int(I_h.nbytes + Iref_h.nbytes),
+               "d2h_bytes_per_step": int(Oh.numel() * 8), "ms_per_step": te * 1e3,
+               "how": "fkk_transform_host: pinned host cube -> device, transform, complex64 cube -> pinned host"}
+
+    res = {
+        "metric": METRIC, "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator synth/, BASELINE.json configs[2])",
+        "config": {"workload": f"{args.workload}: fKK-EC transform of {N:,} x {M} (k={k}), fp32 cube, complex64 out",
+                   "n_spectra": N, "n_freq": M, "rank_k": k, "parallelism": f"pixel shards x{world}",
+                   "l2": "inputs larger than L2 (cube 2.81 GB, output 5.62 GB)"},
+        "roofline": roofline, "stage_ms": stage_ms, "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "direct_kk": {"value": N / (td / 1e3), "unit": "spectra/s", "ms_per_pass": td, "stage_ms": direct_stage},
+        "ml_apply": ml, "e2e": e2e,
+    }
+    return res
+
+
+def cpu_baseline(args, kind="oracle") -> dict:
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample of the same workload."""
+    from oracle import fkk_oracle as O
+    from synth import CONFIGS, generate_rows
+    cfg = CONFIGS[args.workload]
+    n_s = args.cpu_sample
+    I, Iref, _ = generate_rows(cfg, 0, n_s)
+    t0 = time.perf_counter()
+    O.fkk_ec(I, Iref, cfg.rank_k, O.Params())
+    dt = time.perf_counter() - t0
+    nd = args.cpu_direct_sample
+    t1 = time.perf_counter()
+    O.kk_direct(I[:nd], Iref, O.Params())
+    dd = time.perf_counter() - t1
+    cores = len(os.sched_getaffinity(0))
+    return {"value": n_s / dt, "unit": "spectra/s", "cores": cores, "kind": kind,
+            "sample": f"fKK-EC oracle (fp64 NumPy, BLAS threads = {cores}) on the first {n_s:,} spectra of {args.workload} "
+                      f"({dt:.1f} s); direct-KK oracle on {nd:,} spectra: {nd / dd:.1f} spectra/s",
+            "direct_kk_value": nd / dd}
+
+
+def run_reference(args) -> dict:
+    world, rank, local = _dist()
+    if rank != 0:
+        return {}
+    vals = []
+    cb = None
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    for _ in range(max(1, args.steps)):
+        cb = cpu_baseline(args, kind="oracle")
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "spectra/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.cpu_sample / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.workload} (bounded sample of {args.cpu_sample:,} spectra per step)"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "spectra/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--cpu-direct-sample", type=int, default=2000)
+    ap.add_argument("--skip-ml", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, _ = _dist()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if rank == 0:
+            print(json.dumps(res))
+        return
+    res = run_ours(args)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

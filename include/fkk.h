@@ -101,7 +101,9 @@ fkk_status fkk_get_nccl_unique_id(uint8_t out[128]);
 fkk_status fkk_plan_create(const fkk_plan_desc* d, fkk_plan_t* out);  /* allocates all workspace */
 fkk_status fkk_plan_destroy(fkk_plan_t p);
 const char* fkk_last_error(fkk_plan_t p);          /* valid until the next call on p; p may be NULL */
-fkk_status fkk_plan_set_stream(fkk_plan_t p, void* cuda_stream);   /* NULL -> plan-owned stream */
+/* Enqueue subsequent work on cuda_stream (a cudaStream_t; NULL = the legacy default stream).  A new
+ * plan starts on its own non-blocking stream. */
+fkk_status fkk_plan_set_stream(fkk_plan_t p, void* cuda_stream);
 fkk_status fkk_plan_sync(fkk_plan_t p);            /* synchronise; report deferred device errors */
 
 /* fkk_svd -- truncated SVD A ~ U S V^T of the log-ratio matrix through the Gram

@@ -654,9 +654,11 @@ const char* fkk_last_error(fkk_plan_t p) { return p ? p->err.c_str() : g_create_
 
 fkk_status fkk_plan_set_stream(fkk_plan_t p, void* cuda_stream) {
   return guarded(p, [&] {
+    if (p->stream == static_cast<cudaStream_t>(cuda_stream) && !p->own_stream) return;
     if (p->own_stream && p->stream) { FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream)); cudaStreamDestroy(p->stream); }
-    if (cuda_stream) { p->stream = static_cast<cudaStream_t>(cuda_stream); p->own_stream = false; }
-    else { FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)); p->own_stream = true; }
+    // NULL selects the legacy default stream (what torch's default stream handle 0 denotes)
+    p->stream = static_cast<cudaStream_t>(cuda_stream);
+    p->own_stream = false;
   });
 }
 
