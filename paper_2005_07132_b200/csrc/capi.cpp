@@ -130,6 +130,13 @@ struct fkk_plan {
          *XtPhi = nullptr, *Phi_pec = nullptr, *HPhi = nullptr, *tmp = nullptr, *Vsec = nullptr, *ridge_work = nullptr,
          *lam = nullptr, *basis_als_state = nullptr;
   float* Bi = nullptr;
+  double* eig_work = nullptr;
+  double* lam_d = nullptr;
+  // tcgen05 Gram
+  int2* gtc_tiles = nullptr;
+  int* gtc_tile_of = nullptr;
+  int gtc_ntiles = 0, gtc_nTj = 0, gtc_nsplit = 0;
+  double* gtc_part = nullptr;
   // direct path (lazy)
   int64_t direct_batch = 0;
   float *phi = nullptr, *phierr = nullptr;
@@ -156,7 +163,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, phi, phierr, als_state, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
@@ -284,8 +291,21 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     FKK_CUDA_CHECK(cudaMemcpy(p->tw64, t64.data(), t64.size() * sizeof(double2), cudaMemcpyHostToDevice));
   }
   p->A = dalloc<float>((size_t)n * M);
-  p->gram_nsplit_cap = fkk::gram_num_splits(n, M);
-  p->gram_part = dalloc<double>((size_t)p->gram_nsplit_cap * fkk::gram_num_tiles(M) * 128 * 128);
+  if (d->gemm_impl == FKK_GEMM_3XTF32) {
+    std::vector<int2> tl;
+    std::vector<int> tof;
+    fkk::gram_tc_tiles(M, tl, tof, p->gtc_nTj);
+    p->gtc_ntiles = (int)tl.size();
+    p->gtc_nsplit = fkk::gram_tc_splits(p->gtc_ntiles, n);
+    p->gtc_tiles = dalloc<int2>(tl.size());
+    p->gtc_tile_of = dalloc<int>(tof.size());
+    FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tile_of, tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
+    p->gtc_part = dalloc<double>(fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
+  } else {
+    p->gram_nsplit_cap = fkk::gram_num_splits(n, M);
+    p->gram_part = dalloc<double>((size_t)p->gram_nsplit_cap * fkk::gram_num_tiles(M) * 128 * 128);
+  }
   p->G = dalloc<double>((size_t)M * M);
   p->colsum = dalloc<double>(M);
   p->f64 = dalloc<double>(M);
@@ -315,6 +335,8 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->lam = dalloc<double>(1);
   p->basis_als_state = dalloc<double>((size_t)3 * M * (((nqc + 31) / 32) * 32));
   p->Bi = dalloc<float>((size_t)k * M * 2);
+  p->eig_work = dalloc<double>(fkk::eig_workspace_doubles(M, k));
+  p->lam_d = dalloc<double>(k);
   if (d->world_size > 1) {
     std::string e;
     if (!g_nccl.load(e)) throw Status(FKK_ERR_NCCL, e);
@@ -370,23 +392,30 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
-    const int ns = std::min(p->gram_nsplit_cap, fkk::gram_num_splits(std::max<int64_t>(r1 - r0, 1), M));
-    fkk::launch_gram_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->gram_part, ns, s);
-    fkk::launch_gram_reduce(p->gram_part, ns, M, p->G, sh > 0, s);
+    if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
+      const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, std::max<int64_t>(r1 - r0, 1)));
+      fkk::launch_gram_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+      fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+    } else {
+      const int ns = std::min(p->gram_nsplit_cap, fkk::gram_num_splits(std::max<int64_t>(r1 - r0, 1), M));
+      fkk::launch_gram_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->gram_part, ns, s);
+      fkk::launch_gram_reduce(p->gram_part, ns, M, p->G, sh > 0, s);
+    }
   }
   if (p->d.world_size > 1)
     nccl_check(g_nccl.AllReduce(p->G, p->G, (size_t)M * M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(G)");
   if (p->d.f_mode == FKK_F_EQ9) fkk::launch_scale_gram(p->G, p->f64, M, s);
   p->mark("gram");
-  // eig on the host (fp64)
-  std::vector<double> hG((size_t)M * M), hV((size_t)M * k), hl(k);
-  FKK_CUDA_CHECK(cudaMemcpyAsync(hG.data(), p->G, hG.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  // eig on the GPU (fp64): Householder tridiagonalisation, bisection, inverse iteration
+  fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, s);
+  std::vector<double> hl(k);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(hl.data(), p->lam_d, k * sizeof(double), cudaMemcpyDeviceToHost, s));
   p->check_flags_sync();
-  if (fkk::host_eig_topk(hG.data(), M, k, hV.data(), hl.data()) != 0) throw Status(FKK_ERR_NUMERICAL, "eigensolver failed");
   p->h_s.assign(k, 0.0);
-  for (int i = 0; i < k; ++i) p->h_s[i] = std::sqrt(std::max(hl[i], 0.0));
-  FKK_CUDA_CHECK(cudaMemcpyAsync(p->V64, hV.data(), hV.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // hV is a stack buffer
+  for (int i = 0; i < k; ++i) {
+    if (!std::isfinite(hl[i])) throw Status(FKK_ERR_NUMERICAL, "eigensolver produced a non-finite eigenvalue");
+    p->h_s[i] = std::sqrt(std::max(hl[i], 0.0));
+  }
   p->mark("eig");
 }
 

@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace fkk {
 
@@ -67,6 +68,14 @@ int gram_num_tiles(int M);
 int gram_num_splits(int64_t n, int M);
 void launch_gram_simt(const float* A, int64_t n, int M, double* partials, int nsplit, cudaStream_t s);
 void launch_gram_reduce(const double* partials, int nsplit, int M, double* G, int accumulate, cudaStream_t s);
+// tcgen05 3xTF32 Gram (k_gram_tc.cu): 128 x 256 tiles of the upper triangle x row splits.
+void gram_tc_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nTj);
+int gram_tc_splits(int ntiles, int64_t n);
+size_t gram_tc_partial_doubles(int ntiles, int nsplit);
+void launch_gram_tc(const float* A, int64_t n, int M, const int2* d_tiles, int ntiles, int nsplit, double* partials,
+                    cudaStream_t s);
+void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nTj,
+                           double* G, int accumulate, cudaStream_t s);
 // Projection US = A0 W (k_project.cu) with per-block column extremes [blk][c][2].
 int project_num_blocks(int64_t n);
 void launch_project_simt(const float* A, int64_t n, int M, const float* W, int k, int kp, float* US, float* ext_val,
@@ -88,6 +97,11 @@ void launch_ridge(const double* C, int k, const double* R, int ncol, double ridg
                   double* work, int* flags, cudaStream_t s);
 void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vsec, const double* Hv,
                        const double* Phi_pec, int k, int M, float* Bi, cudaStream_t s);
+
+// ---- GPU eigensolver (k_eig.cu): top-k eigenpairs of the symmetric M x M fp64 G (device);
+// V: k vectors of length M (= M x k column-major), lam_out: k descending.
+size_t eig_workspace_doubles(int M, int k);
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, cudaStream_t s);
 
 // ---- host eigensolver (host_eig.cpp): returns 0 on success
 int host_eig_topk(const double* G, int M, int k, double* V /* k vectors of length M */, double* lam);

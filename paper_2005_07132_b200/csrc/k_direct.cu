@@ -82,7 +82,7 @@ direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __
 // system has the same band values by position).  Factors (L1, L2, g/D) live in a [row][spectrum]
 // fp64 state so that a warp's accesses are coalesced; y and z move through a 32x33 smem tile.
 template <typename TY, typename TZ>
-__global__ void __launch_bounds__(128, 8)
+__global__ void __launch_bounds__(128, 4)
 als_rows_kernel(const TY* __restrict__ y, int64_t n, int M, double lam, double p, int iters,
                 double* __restrict__ st, int64_t nb, TZ* __restrict__ z) {
   __shared__ double tile[4][32][33];   // y tile in; in the last sweep overwritten by z (same slot)
@@ -101,6 +101,21 @@ als_rows_kernel(const TY* __restrict__ y, int64_t n, int M, double lam, double p
     const bool do_bsub = sw > 0, do_fact = sw < iters;
     double zp1 = 0.0, zp2 = 0.0;
     double Dm1 = 0.0, Dm2 = 0.0, L1m1 = 0.0, L2m1 = 0.0, L2m2 = 0.0, gm1 = 0.0, gm2 = 0.0;
+    // software pipeline: the (L1, L2, g/D) of the next PF rows are loaded PF rows ahead so the
+    // dependent fp64 recurrence does not wait on L2/HBM latency every row
+    constexpr int PF = 4;
+    double nl1[PF], nl2[PF], ngd[PF];
+    auto row_of = [&](int t) { return asc ? t : (M - 1 - t); };
+    if (do_bsub) {
+#pragma unroll
+      for (int q2 = 0; q2 < PF; ++q2) {
+        const int t = q2;
+        if (t < M) {
+          const int64_t ix = (int64_t)row_of(t) * nb + s;
+          nl1[q2] = L1[ix]; nl2[q2] = L2[ix]; ngd[q2] = GD[ix];
+        }
+      }
+    }
     for (int tt = 0; tt < ntile; ++tt) {
       const int tile_i = asc ? tt : (ntile - 1 - tt);
       const int r0 = tile_i * 32;
@@ -113,42 +128,50 @@ als_rows_kernel(const TY* __restrict__ y, int64_t n, int M, double lam, double p
       }
       __syncwarp();
 #pragma unroll 1
-      for (int u = 0; u < 32; ++u) {
-        const int jloc = asc ? u : 31 - u;
-        const int i = r0 + jloc;
-        if (i >= M) continue;
-        const int t = asc ? i : (M - 1 - i);  // position in the new system's elimination order
-        const double yv = tile[warp][lane][jloc];
-        const int64_t idx = (int64_t)i * nb + s;
-        double w = 1.0;
-        double zval = 0.0;
-        if (do_bsub) {
-          const double l1 = L1[idx], l2 = L2[idx], gd = GD[idx];
-          zval = gd - l1 * zp1 - l2 * zp2;
-          zp2 = zp1;
-          zp1 = zval;
-          w = (yv > zval) ? p : q;
-        }
-        if (do_fact) {
-          // band values of W + lam D^T D at position t (D^T D: diag 1,5,6..6,5,1; first
-          // off-diagonal -2,-4..-4,-2; second off-diagonal 1)
-          const double d0 = (t == 0 || t == M - 1) ? 1.0 : ((t == 1 || t == M - 2) ? 5.0 : 6.0);
-          const double d1 = (t >= M - 1) ? 0.0 : ((t == 0 || t == M - 2) ? -2.0 : -4.0);
-          const double a0 = w + lam * d0;
-          const double a1 = lam * d1;
-          const double a2 = (t <= M - 3) ? lam : 0.0;
-          const double D = a0 - L1m1 * L1m1 * Dm1 - L2m2 * L2m2 * Dm2;
-          const double rD = 1.0 / D;
-          const double l1n = (a1 - L2m1 * L1m1 * Dm1) * rD;
-          const double l2n = a2 * rD;
-          const double g = w * yv - L1m1 * gm1 - L2m2 * gm2;
-          if (valid) { L1[idx] = l1n; L2[idx] = l2n; GD[idx] = g * rD; }
-          Dm2 = Dm1; Dm1 = D;
-          L2m2 = L2m1; L2m1 = l2n;
-          L1m1 = l1n;
-          gm2 = gm1; gm1 = g;
-        } else {
-          tile[warp][lane][jloc] = zval;
+      for (int u0 = 0; u0 < 32; u0 += PF) {
+#pragma unroll
+        for (int q2 = 0; q2 < PF; ++q2) {
+          const int u = u0 + q2;
+          const int jloc = asc ? u : 31 - u;
+          const int i = r0 + jloc;
+          if (i >= M) continue;
+          const int t = asc ? i : (M - 1 - i);  // position in the new system's elimination order
+          const double yv = tile[warp][lane][jloc];
+          const int64_t idx = (int64_t)i * nb + s;
+          double w = 1.0;
+          double zval = 0.0;
+          if (do_bsub) {
+            const double l1 = nl1[q2], l2 = nl2[q2], gd = ngd[q2];
+            if (t + PF < M) {   // prefetch PF rows ahead (same ring slot)
+              const int64_t ix = (int64_t)row_of(t + PF) * nb + s;
+              nl1[q2] = L1[ix]; nl2[q2] = L2[ix]; ngd[q2] = GD[ix];
+            }
+            zval = gd - l1 * zp1 - l2 * zp2;
+            zp2 = zp1;
+            zp1 = zval;
+            w = (yv > zval) ? p : q;
+          }
+          if (do_fact) {
+            // band values of W + lam D^T D at position t (D^T D: diag 1,5,6..6,5,1; first
+            // off-diagonal -2,-4..-4,-2; second off-diagonal 1)
+            const double d0 = (t == 0 || t == M - 1) ? 1.0 : ((t == 1 || t == M - 2) ? 5.0 : 6.0);
+            const double d1 = (t >= M - 1) ? 0.0 : ((t == 0 || t == M - 2) ? -2.0 : -4.0);
+            const double a0 = w + lam * d0;
+            const double a1 = lam * d1;
+            const double a2 = (t <= M - 3) ? lam : 0.0;
+            const double D = a0 - L1m1 * L1m1 * Dm1 - L2m2 * L2m2 * Dm2;
+            const double rD = 1.0 / D;
+            const double l1n = (a1 - L2m1 * L1m1 * Dm1) * rD;
+            const double l2n = a2 * rD;
+            const double g = w * yv - L1m1 * gm1 - L2m2 * gm2;
+            if (valid) { L1[idx] = l1n; L2[idx] = l2n; GD[idx] = g * rD; }
+            Dm2 = Dm1; Dm1 = D;
+            L2m2 = L2m1; L2m1 = l2n;
+            L1m1 = l1n;
+            gm2 = gm1; gm1 = g;
+          } else {
+            tile[warp][lane][jloc] = zval;
+          }
         }
       }
       if (!do_fact) {
@@ -161,6 +184,61 @@ als_rows_kernel(const TY* __restrict__ y, int64_t n, int M, double lam, double p
       }
     }
   }
+}
+
+// Few-row variant (the |q| <= 2k rows of fPEC, Eq. 16): one warp per row, the factor state in shared
+// memory (4M doubles) so the serial fp64 recurrence sees smem instead of L2 latency.  Same sweep
+// order and arithmetic as als_rows_kernel.
+template <typename TY, typename TZ>
+__global__ void __launch_bounds__(32) als_rows_smem_kernel(const TY* __restrict__ y, int M, double lam, double p,
+                                                           int iters, TZ* __restrict__ z) {
+  extern __shared__ __align__(16) double sh[];
+  double* yv = sh;
+  double* L1 = yv + M;
+  double* L2 = L1 + M;
+  double* GD = L2 + M;
+  const int row = blockIdx.x, lane = threadIdx.x;
+  for (int i = lane; i < M; i += 32) yv[i] = (double)y[(int64_t)row * M + i];
+  __syncwarp();
+  if (lane == 0) {
+    const double q = 1.0 - p;
+    for (int sw = 0; sw <= iters; ++sw) {
+      const bool asc = (sw & 1) == 0;
+      const bool do_bsub = sw > 0, do_fact = sw < iters;
+      double zp1 = 0.0, zp2 = 0.0;
+      double Dm1 = 0.0, Dm2 = 0.0, L1m1 = 0.0, L2m1 = 0.0, L2m2 = 0.0, gm1 = 0.0, gm2 = 0.0;
+      for (int t = 0; t < M; ++t) {
+        const int i = asc ? t : (M - 1 - t);
+        const double yy = yv[i];
+        double w = 1.0, zval = 0.0;
+        if (do_bsub) {
+          zval = GD[i] - L1[i] * zp1 - L2[i] * zp2;
+          zp2 = zp1;
+          zp1 = zval;
+          w = (yy > zval) ? p : q;
+        }
+        if (do_fact) {
+          const double d0 = (t == 0 || t == M - 1) ? 1.0 : ((t == 1 || t == M - 2) ? 5.0 : 6.0);
+          const double d1 = (t >= M - 1) ? 0.0 : ((t == 0 || t == M - 2) ? -2.0 : -4.0);
+          const double a2 = (t <= M - 3) ? lam : 0.0;
+          const double D = w + lam * d0 - L1m1 * L1m1 * Dm1 - L2m2 * L2m2 * Dm2;
+          const double rD = 1.0 / D;
+          const double l1n = (lam * d1 - L2m1 * L1m1 * Dm1) * rD;
+          const double l2n = a2 * rD;
+          const double g = w * yy - L1m1 * gm1 - L2m2 * gm2;
+          L1[i] = l1n; L2[i] = l2n; GD[i] = g * rD;
+          Dm2 = Dm1; Dm1 = D;
+          L2m2 = L2m1; L2m1 = l2n;
+          L1m1 = l1n;
+          gm2 = gm1; gm1 = g;
+        } else {
+          yv[i] = zval;    // y is dead after the last factorisation: reuse it for z
+        }
+      }
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < M; i += 32) z[(int64_t)row * M + i] = (TZ)yv[i];
 }
 
 template <typename TIn>
@@ -277,6 +355,23 @@ void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const floa
 void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, double* state,
                      void* z, int z_f64, cudaStream_t s) {
   if (n <= 0) return;
+  const size_t sm = (size_t)4 * M * sizeof(double);
+  if (n <= 4096 && sm <= 200 * 1024) {
+    // few rows: smem-resident state, one warp per row
+#define FKK_ALS_SMEM(TY, TZ)                                                                          \
+    {                                                                                                 \
+      auto kf = als_rows_smem_kernel<TY, TZ>;                                                         \
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                 \
+      kf<<<(unsigned)n, 32, sm, s>>>((const TY*)y, M, lam, p, iters, (TZ*)z);                         \
+    }
+    if (y_f64 && z_f64) FKK_ALS_SMEM(double, double)
+    else if (!y_f64 && !z_f64) FKK_ALS_SMEM(float, float)
+    else if (!y_f64 && z_f64) FKK_ALS_SMEM(float, double)
+    else FKK_ALS_SMEM(double, float)
+#undef FKK_ALS_SMEM
+    check_launch("als_rows_smem");
+    return;
+  }
   const int64_t nb = ((n + 31) / 32) * 32;
   const int64_t warps = nb / 32;
   const int grid = (int)((warps + 3) / 4);

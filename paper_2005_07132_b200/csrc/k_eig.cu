@@ -1,0 +1,426 @@
+// GPU fp64 top-k symmetric eigensolver for the Gram matrix (F4: the truncated SVD of A through
+// G = A^T A; s_i = sqrt(lambda_i), V_k = top-k eigenvectors).  Same algorithm as the
+// host reference solver (host_eig.cpp), laid out for the GPU:
+//   tridiag   : Householder tridiagonalisation Q^T G Q = T in ONE cooperative kernel; per column
+//               every CTA forms the reflector redundantly in smem, the grid computes p = tau A v
+//               (warp per row), grid.sync, every CTA forms w = p - (tau/2)(p.v) v, the grid applies
+//               the rank-2 update A -= v w^T + w v^T, grid.sync.  G stays L2-resident (8 MB @ M=1000).
+//   bisect    : warp per eigenvalue, 32-point Sturm multisection (33x narrowing per round)
+//   inviter   : thread per eigenvector, partial-pivoting tridiagonal LU of T - lambda I, 3 solves
+//   reorth    : classical Gram-Schmidt, twice, in descending-eigenvalue order (one CTA)
+//   backxform : CTA per eigenvector, u = H_0 ... H_{M-3} z, then the sign rule (largest |.| > 0)
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "fkk_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace fkk {
+
+namespace {
+
+constexpr int kEigThreads = 256;
+constexpr int kTriThreads = 512;
+constexpr int kSeg = 256;
+
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+// One grid-wide pass and one grid.sync per column j: the rank-2 update of column j-1 is applied
+// lazily while p_j = tau_j A^(j) v_j is formed, row by row (each row read and written once):
+//   row_r(A^(j)) = row_r(A^(j-1)) - v_{j-1}[r] w_{j-1} - w_{j-1}[r] v_{j-1}
+// Every CTA builds v_j from row j of A^(j-1) plus the pending update (symmetry: row j = column j).
+__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict__ A, int M, double* __restrict__ d,
+                                                              double* __restrict__ e, double* __restrict__ tau,
+                                                              double* __restrict__ pg) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  double* v = sm;            // v_j   (index i <-> row j+1+i)
+  double* vp = sm + M;       // v_{j-1} (index i <-> row j+i)
+  double* wp = sm + 2 * M;   // w_{j-1} (index i <-> row j+i)
+  double* red = sm + 3 * M;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31;
+  const int gwarp = (blockIdx.x * nt + tid) >> 5;
+  const int nwarps = (gridDim.x * nt) >> 5;
+  bool pending = false;      // (vp, wp) hold the update of column j-1
+  double tprev = 0.0;
+  for (int j = 0; j + 2 < M; ++j) {
+    const int m = M - j - 1, base = j + 1;
+    // reflector of the previous column goes to its (dead) row j-1, after everybody read that row
+    if (j > 0 && blockIdx.x == 0) {
+      double* rj = A + (int64_t)(j - 1) * M + j;
+      for (int i = tid; i < m + 1; i += nt) rj[i] = tprev != 0.0 ? vp[i] : 0.0;
+    }
+    // x = column j of A^(j) below the diagonal (row j of A^(j-1) + pending update)
+    const double* rowj = A + (int64_t)j * M;
+    double s = 0.0;
+    const double vpj = pending ? vp[0] : 0.0, wpj = pending ? wp[0] : 0.0;
+    for (int i = tid; i < m; i += nt) {
+      double x = rowj[base + i];
+      if (pending) x -= vpj * wp[1 + i] + wpj * vp[1 + i];
+      v[i] = x;
+      s += x * x;
+    }
+    double djj = 0.0;
+    if (tid == 0) { djj = rowj[j]; if (pending) djj -= 2.0 * vpj * wpj; }
+    const double nrm2 = block_sum_d(s, red);
+    const double x0 = v[0];
+    const double nrm = sqrt(nrm2);
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    const double v0 = x0 - alpha;
+    const double vtv = nrm2 - x0 * x0 + v0 * v0;
+    const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
+    __syncthreads();
+    if (tid == 0) v[0] = v0;
+    if (blockIdx.x == 0 && tid == 0) {
+      d[j] = djj;
+      e[j] = t == 0.0 ? x0 : alpha;
+      tau[j] = t;
+    }
+    __syncthreads();
+    // pass over the trailing rows: apply the pending update, write back, p = t A^(j) v.  A warp
+    // task is (row, 256-column segment): 8 independent loads per lane in flight; the per-segment
+    // partial dots are summed in a fixed order after the grid barrier (deterministic).
+    const int nseg = (m + kSeg - 1) / kSeg;
+    for (int task = gwarp; task < m * nseg; task += nwarps) {
+      const int r = task / nseg, sg = task - r * nseg;
+      double* row = A + (int64_t)(base + r) * M + base;
+      const int c0 = sg * kSeg, c1 = min(m, c0 + kSeg);
+      double acc = 0.0;
+      if (pending) {
+        const double vr = vp[1 + r], wr = wp[1 + r];
+#pragma unroll 8
+        for (int c = c0 + lane; c < c1; c += 32) {
+          const double a = row[c] - (vr * wp[1 + c] + wr * vp[1 + c]);
+          row[c] = a;
+          acc = fma(a, v[c], acc);
+        }
+      } else {
+#pragma unroll 8
+        for (int c = c0 + lane; c < c1; c += 32) acc = fma(row[c], v[c], acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) pg[(int64_t)sg * M + r] = t * acc;
+    }
+    grid.sync();
+    // w_j = p - (t/2)(p.v) v  -> becomes the pending update (index shift: row j+1+i -> i)
+    double ps = 0.0;
+    for (int i = tid; i < m; i += nt) {
+      double pv = 0.0;
+      for (int sg = 0; sg < nseg; ++sg) pv += pg[(int64_t)sg * M + i];
+      wp[i] = pv;
+      ps += pv * v[i];
+    }
+    const double K = 0.5 * t * block_sum_d(ps, red);
+    for (int i = tid; i < m; i += nt) { wp[i] -= K * v[i]; vp[i] = v[i]; }
+    if (t == 0.0) for (int i = tid; i < m; i += nt) { wp[i] = 0.0; vp[i] = 0.0; }
+    __syncthreads();
+    pending = true;
+    tprev = t;
+  }
+  // flush: reflector of the last column and the trailing 2 x 2 block with the pending update
+  if (blockIdx.x == 0) {
+    const int j = M - 2;
+    if (j > 0) {
+      double* rj = A + (int64_t)(j - 1) * M + j;
+      for (int i = tid; i < 2; i += nt) rj[i] = tprev != 0.0 ? vp[i] : 0.0;
+    }
+    if (tid == 0) {
+      double a00 = A[(int64_t)(M - 2) * M + (M - 2)], a10 = A[(int64_t)(M - 1) * M + (M - 2)];
+      double a11 = A[(int64_t)(M - 1) * M + (M - 1)];
+      if (pending && M >= 3) {
+        a00 -= 2.0 * vp[0] * wp[0];
+        a10 -= vp[1] * wp[0] + wp[1] * vp[0];
+        a11 -= 2.0 * vp[1] * wp[1];
+      }
+      d[M - 2] = a00;
+      e[M - 2] = a10;
+      d[M - 1] = a11;
+    }
+  }
+}
+
+__device__ __forceinline__ int sturm_count_dev(const double* d, const double* e, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0) cnt++;
+  for (int i = 1; i < n; ++i) {
+    const double ee = e[i - 1];
+    q = d[i] - x - ee * ee / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) cnt++;
+  }
+  return cnt;
+}
+
+// warp per eigenvalue index jj (jj-th largest); also computes ||T|| bounds
+__global__ void bisect_kernel(const double* __restrict__ d, const double* __restrict__ e, int M, int k,
+                              double* __restrict__ lam, double* __restrict__ tnorm_out) {
+  const int lane = threadIdx.x & 31;
+  const int jj = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (jj >= k) return;
+  double gl = 1e300, gu = -1e300, tn = 0.0;
+  for (int i = lane; i < M; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < M - 1 ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - r);
+    gu = fmax(gu, d[i] + r);
+    tn = fmax(tn, fabs(d[i]) + r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+  }
+  const double eps = 2.220446049250313e-16;
+  const double pivmin = fmax(1e-300, tn * 1e-300);
+  double lo = gl - 2.0 * eps * tn * M - 1e-300, hi = gu + 2.0 * eps * tn * M + 1e-300;
+  const int idx = M - 1 - jj;   // ascending index
+  for (int round = 0; round < 64; ++round) {
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const int c = sturm_count_dev(d, e, M, x, pivmin);
+    const unsigned ball = __ballot_sync(0xffffffffu, c > idx);
+    double xlo = __shfl_sync(0xffffffffu, x, ball ? (__ffs(ball) - 2 < 0 ? 0 : __ffs(ball) - 2) : 31);
+    double xhi = __shfl_sync(0xffffffffu, x, ball ? __ffs(ball) - 1 : 31);
+    if (ball == 0) { lo = xhi; }                       // eigenvalue above the last point
+    else if (__ffs(ball) == 1) { hi = xhi; }           // below the first point
+    else { lo = xlo; hi = xhi; }
+  }
+  if (lane == 0) {
+    lam[jj] = 0.5 * (lo + hi);
+    if (jj == 0) tnorm_out[0] = tn;
+  }
+}
+
+// CTA (one warp) per eigenvector: inverse iteration on T - lambda I (LAPACK dgttrf/dgttrs logic),
+// the LU factors in shared memory (lane 0 runs the recurrences; the warp fills and normalises).
+__global__ void __launch_bounds__(32) inviter_kernel(const double* __restrict__ d, const double* __restrict__ e, int M,
+                                                     int k, const double* __restrict__ lam,
+                                                     const double* __restrict__ tnorm, double* __restrict__ Z) {
+  extern __shared__ __align__(16) double sh[];
+  const int jj = blockIdx.x;
+  const int lane = threadIdx.x;
+  double* dl = sh;
+  double* dd = dl + M;
+  double* du = dd + M;
+  double* du2 = du + M;
+  double* z = du2 + M;
+  unsigned char* piv = reinterpret_cast<unsigned char*>(z + M);
+  const double eps = 2.220446049250313e-16;
+  const double tn = tnorm[0];
+  const double tiny = eps * tn + 1e-300;
+  double l = lam[jj];
+  if (jj > 0 && fabs(lam[jj - 1] - l) < 10.0 * eps * tn) l -= 10.0 * eps * tn * jj;   // split exact ties
+  for (int i = lane; i < M; i += 32) {
+    dd[i] = d[i] - l;
+    piv[i] = 0;
+    if (i < M - 1) { dl[i] = e[i]; du[i] = e[i]; }
+    if (i < M - 2) du2[i] = 0.0;
+    uint64_t s = 0x9E3779B97F4A7C15ull * (uint64_t)(jj + 1) + 0xD1B54A32D192ED03ull * (uint64_t)(i + 1);
+    s ^= s >> 31; s *= 0x7FB5D329728EA185ull; s ^= s >> 27; s *= 0x81DADEF4BC2DD44Dull; s ^= s >> 33;
+    z[i] = ((double)(s >> 11) / 9007199254740992.0) - 0.5;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 0; i < M - 1; ++i) {
+      if (fabs(dd[i]) >= fabs(dl[i])) {
+        if (dd[i] == 0.0) dd[i] = tiny;
+        const double f = dl[i] / dd[i];
+        dl[i] = f;
+        dd[i + 1] -= f * du[i];
+      } else {
+        const double f = dd[i] / dl[i];
+        dd[i] = dl[i];
+        dl[i] = f;
+        const double tmp = du[i];
+        du[i] = dd[i + 1];
+        dd[i + 1] = tmp - f * dd[i + 1];
+        if (i < M - 2) { du2[i] = du[i + 1]; du[i + 1] = -f * du[i + 1]; }
+        piv[i] = 1;
+      }
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < M; i += 32) {
+    double v = dd[i];
+    if (fabs(v) < tiny) v = v < 0 ? -tiny : tiny;
+    dd[i] = 1.0 / v;     // keep reciprocals: the solves multiply
+  }
+  __syncwarp();
+  for (int it = 0; it < 3; ++it) {
+    if (lane == 0) {
+      for (int i = 0; i < M - 1; ++i) {
+        const double bi = z[i], bi1 = z[i + 1];
+        if (piv[i]) { z[i] = bi1; z[i + 1] = bi - dl[i] * bi1; }
+        else { z[i + 1] = bi1 - dl[i] * bi; }
+      }
+      z[M - 1] *= dd[M - 1];
+      if (M > 1) z[M - 2] = (z[M - 2] - du[M - 2] * z[M - 1]) * dd[M - 2];
+      for (int i = M - 3; i >= 0; --i) z[i] = (z[i] - du[i] * z[i + 1] - du2[i] * z[i + 2]) * dd[i];
+    }
+    __syncwarp();
+    double nz = 0.0;
+    for (int i = lane; i < M; i += 32) nz += z[i] * z[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    const double inv = 1.0 / sqrt(nz);
+    for (int i = lane; i < M; i += 32) z[i] *= inv;
+    __syncwarp();
+  }
+  for (int i = lane; i < M; i += 32) Z[(int64_t)jj * M + i] = z[i];
+}
+
+// classical Gram-Schmidt applied twice, vectors in descending-eigenvalue order (one CTA)
+__global__ void __launch_bounds__(1024) reorth_kernel(double* __restrict__ Z, int M, int k) {
+  __shared__ double dots[128];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int j = 0; j < k; ++j) {
+    double* zj = Z + (int64_t)j * M;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int c = wid; c < j; c += nw) {
+        const double* zc = Z + (int64_t)c * M;
+        double acc = 0.0;
+        for (int i = lane; i < M; i += 32) acc = fma(zc[i], zj[i], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) dots[c] = acc;
+      }
+      __syncthreads();
+      for (int i = tid; i < M; i += nt) {
+        double x = zj[i];
+        for (int c = 0; c < j; ++c) x -= dots[c] * Z[(int64_t)c * M + i];
+        zj[i] = x;
+      }
+      __syncthreads();
+    }
+    double s = 0.0;
+    for (int i = tid; i < M; i += nt) s += zj[i] * zj[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) tot += red[w2];
+    const double inv = 1.0 / sqrt(tot);
+    for (int i = tid; i < M; i += nt) zj[i] *= inv;
+    __syncthreads();
+  }
+}
+
+// CTA per eigenvector: u = H_0 H_1 ... H_{M-3} z, reflector v_j stored in row j of A at j+1..M-1
+__global__ void __launch_bounds__(kEigThreads) backxform_kernel(const double* __restrict__ A, const double* __restrict__ tau,
+                                                                int M, const double* __restrict__ Z,
+                                                                const double* __restrict__ lam, double* __restrict__ V,
+                                                                double* __restrict__ lam_out) {
+  extern __shared__ __align__(16) double zs[];   // M
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const int jj = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int i = tid; i < M; i += nt) zs[i] = Z[(int64_t)jj * M + i];
+  __syncthreads();
+  for (int j = M - 3; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    const double* vj = A + (int64_t)j * M;
+    double acc = 0.0;
+    for (int i = j + 1 + tid; i < M; i += nt) acc = fma(vj[i], zs[i], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[wid] = acc;
+    __syncthreads();
+    double dot = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) dot += red[w2];
+    dot *= t;
+    for (int i = j + 1 + tid; i < M; i += nt) zs[i] -= dot * vj[i];
+    __syncthreads();
+  }
+  // sign rule: entry of largest |.| positive, ties -> lowest index
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = tid; i < M; i += nt) {
+    const double a = fabs(zs[i]);
+    if (a > best) { best = a; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if (lane == 0) { red[wid] = best; redi[wid] = bi; }
+  __syncthreads();
+  double gb = red[0];
+  int gi = redi[0];
+  for (int w2 = 1; w2 < nw; ++w2)
+    if (red[w2] > gb || (red[w2] == gb && redi[w2] < gi)) { gb = red[w2]; gi = redi[w2]; }
+  const double sg = zs[gi] < 0.0 ? -1.0 : 1.0;
+  for (int i = tid; i < M; i += nt) V[(int64_t)jj * M + i] = sg * zs[i];
+  if (tid == 0) lam_out[jj] = lam[jj];
+}
+
+}  // namespace
+
+size_t eig_workspace_doubles(int M, int k) {
+  // A copy (M*M) + d, e, tau, p (4M) + lam, tnorm (k+1) + Z (k*M) + inviter scratch (4kM + kM/8 + 1)
+  return (size_t)M * M + 3 * (size_t)M + 16 * (size_t)M + (size_t)k + 1 + (size_t)k * M + 16;
+}
+
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, cudaStream_t s) {
+  double* A = work;
+  double* d = A + (size_t)M * M;
+  double* e = d + M;
+  double* tau = e + M;
+  double* pg = tau + M;
+  double* lam = pg + 16 * (size_t)M;
+  double* tnorm = lam + k;
+  double* Z = tnorm + 1;
+  FKK_CUDA_CHECK(cudaMemcpyAsync(A, G, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // cooperative tridiagonalisation
+  static int coop_grid = 0;
+  const size_t smem = (3 * (size_t)M + 32) * sizeof(double);
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, kTriThreads, smem));
+  if (per < 1) throw Status(10, "tridiag kernel cannot be co-resident");
+  coop_grid = sms;
+  int Mi = M;
+  void* args[] = {&A, &Mi, &d, &e, &tau, &pg};
+  FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_kernel, dim3(coop_grid), dim3(kTriThreads), args, smem, s));
+  count_launch();
+  if (M == 1) return;
+  bisect_kernel<<<(k * 32 + 127) / 128, 128, 0, s>>>(d, e, M, k, lam, tnorm);
+  check_launch("eig_bisect");
+  const size_t ism = (size_t)5 * M * sizeof(double) + (size_t)M + 16;
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
+  inviter_kernel<<<k, 32, ism, s>>>(d, e, M, k, lam, tnorm, Z);
+  check_launch("eig_inviter");
+  reorth_kernel<<<1, 1024, 0, s>>>(Z, M, k);
+  check_launch("eig_reorth");
+  const size_t bsm = (size_t)M * sizeof(double);
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+  backxform_kernel<<<k, kEigThreads, bsm, s>>>(A, tau, M, Z, lam, V, lam_out);
+  check_launch("eig_backxform");
+}
+
+}  // namespace fkk

@@ -124,9 +124,9 @@ class Basis:
         return dict(n_freq=m.value, rank_k=k.value, fft_len=L.value)
 
     def close(self):
-        if self._h:
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.fkk_basis_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 
@@ -176,9 +176,9 @@ class Plan:
         return self._h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.fkk_plan_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 

@@ -95,9 +95,12 @@ def test_errors_reported(torch_cuda, fkk, cfg1):
 
 
 # ------------------------------------------------------------------------- factorized path -------
-def _factorized_check(torch, fkk, I, Iref, k, *, e2e_tol=1e-3, loopback=0, in_dtype="f32"):
+GEMMS = ["3xtf32", "fp32_simt"]
+
+
+def _factorized_check(torch, fkk, I, Iref, k, *, e2e_tol=1e-3, loopback=0, in_dtype="f32", gemm=None):
     p = O.Params()
-    plan = fkk.Plan(I.shape[1], k, I.shape[0], in_dtype=in_dtype, loopback_shards=loopback)
+    plan = fkk.Plan(I.shape[1], k, I.shape[0], in_dtype=in_dtype, loopback_shards=loopback, gemm=gemm)
     Id, Rd = _dev(torch, I), _dev(torch, Iref)
     K = plan.transform(Id, Rd).cpu().numpy()
     G_gpu, s_gpu, V_gpu, US_gpu = plan.stage("G"), plan.stage("S"), plan.stage("V"), plan.stage("US")
@@ -109,6 +112,10 @@ def _factorized_check(torch, fkk, I, Iref, k, *, e2e_tol=1e-3, loopback=0, in_dt
     V_or, s_or, lam = O.eig_topk(G_or, k)
     # Weyl: |d sigma_i| <= ||dA||_2, a normwise bound -> relative to sigma_1 (DESIGN.md parity contract)
     assert np.max(np.abs(s_gpu - s_or)) / s_or[0] <= 1e-5
+    # the GPU eigensolver on the GPU's own G: residual and orthonormality (property at any size)
+    lam_gpu = s_gpu ** 2
+    assert np.max(np.abs(G_gpu @ V_gpu - V_gpu * lam_gpu[None, :])) / lam_gpu[0] <= 1e-10
+    assert np.max(np.abs(V_gpu.T @ V_gpu - np.eye(k))) <= 1e-10
     US_ref = A @ V_gpu
     assert np.max(np.abs(US_gpu - US_ref)) / np.max(np.abs(US_ref)) <= 1e-5
     gap = (lam[k - 1] - lam[k]) / lam[k - 1]
@@ -129,27 +136,51 @@ def _factorized_check(torch, fkk, I, Iref, k, *, e2e_tol=1e-3, loopback=0, in_dt
     return plan, K, diag
 
 
-def test_factorized_cfg1(torch_cuda, fkk, cfg1):
+@pytest.mark.parametrize("gemm", GEMMS)
+def test_factorized_cfg1(torch_cuda, fkk, cfg1, gemm):
     I, Iref = cfg1
-    _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64")
+    _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64", gemm=gemm)
 
 
-def test_factorized_cfg1_loopback_shards_invariant(torch_cuda, fkk, cfg1):
+@pytest.mark.parametrize("gemm", GEMMS)
+def test_factorized_cfg1_loopback_shards_invariant(torch_cuda, fkk, cfg1, gemm):
     I, Iref = cfg1
-    plan1, K1, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64")
-    plan3, K3, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64", loopback=3)
+    plan1, K1, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64", gemm=gemm)
+    plan3, K3, _ = _factorized_check(torch_cuda, fkk, I, Iref, 12, in_dtype="f64", loopback=3, gemm=gemm)
     assert np.array_equal(plan1.stage("Q"), plan3.stage("Q"))
     assert np.max(np.abs(K1 - K3)) / np.max(np.abs(K1)) < 1e-4
 
 
-def test_factorized_ragged_small(torch_cuda, fkk, cfg1):
+@pytest.mark.parametrize("gemm", GEMMS)
+def test_factorized_ragged_small(torch_cuda, fkk, cfg1, gemm):
     I, Iref = cfg1
-    _factorized_check(torch_cuda, fkk, I[:777], Iref, 12, in_dtype="f64")
+    _factorized_check(torch_cuda, fkk, I[:777], Iref, 12, in_dtype="f64", gemm=gemm)
 
 
-def test_factorized_cfg2(torch_cuda, fkk):
+@pytest.fixture(scope="module")
+def cfg2():
     I, Iref, _ = generate(CONFIGS["cfg2"])
-    _factorized_check(torch_cuda, fkk, I, Iref, 40)
+    return I, Iref
+
+
+@pytest.mark.parametrize("gemm", GEMMS)
+def test_factorized_cfg2(torch_cuda, fkk, cfg2, gemm):
+    I, Iref = cfg2
+    _factorized_check(torch_cuda, fkk, I, Iref, 40, gemm=gemm)
+
+
+def test_gram_tc_equals_simt_in_fp32_accuracy(torch_cuda, fkk, cfg2):
+    """3xTF32 tcgen05 Gram vs the exact-fp32 CUDA-core Gram vs fp64 (max-norm relative)."""
+    I, Iref = cfg2
+    I = I[:20000]
+    G = {}
+    for g in GEMMS:
+        plan = fkk.Plan(1000, 40, I.shape[0], gemm=g)
+        plan.svd(_dev(torch_cuda, I), _dev(torch_cuda, Iref))
+        G[g] = plan.stage("G")
+    G_or = O.gram(O.log_ratio(I, Iref, O.Params()))
+    for g in GEMMS:
+        assert np.max(np.abs(G[g] - G_or)) / np.max(np.abs(G_or)) <= 2e-6, g
 
 
 # ------------------------------------------------------------------------- ML reuse --------------
