@@ -171,6 +171,12 @@ int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap
 /* Number of kernel launches issued by the last call (the bench reports it). */
 int64_t fkk_last_launch_count(fkk_plan_t p);
 
+/* Test hook (tensor-core plumbing self-test): one tcgen05.mma kind::tf32 of A (128 x 8, row-major
+ * fp32, device) times B^T (B: N x 8, N in {16, 32, ..., 256}) into D (128 x N fp32, device) with the
+ * UMMA smem layout selected by mode (bit 0: A MN-major, bit 1: B MN-major, bit 2: 16-B padding).
+ * Synchronises the device. */
+fkk_status fkk_debug_tc_mma(int32_t mode, const float* d_A, const float* d_B, float* d_D, int32_t N);
+
 /* ---------------- host-only helpers (no GPU needed; exercised by the CPU tests) ---------------- */
 /* Top-k eigenpairs of a symmetric M x M fp64 matrix (row-major; only the lower triangle is read):
  * Householder tridiagonalisation, Sturm bisection, inverse iteration, back-transformation.

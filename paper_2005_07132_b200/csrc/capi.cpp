@@ -635,7 +635,7 @@ void fkk_plan_desc_init(fkk_plan_desc* d, int32_t n_freq, int32_t rank_k, int64_
   d->sg_order = 2;
   d->ridge_rel = 1e-3;
   d->ml_ridge_rel = 0.0;
-  d->gemm_impl = FKK_GEMM_FP32_SIMT;
+  d->gemm_impl = FKK_GEMM_3XTF32;
   d->out_layout = FKK_OUT_COMPLEX64;
   d->in_dtype = FKK_IN_F32;
   d->device = 0;
@@ -917,6 +917,18 @@ int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap
 }
 
 int64_t fkk_last_launch_count(fkk_plan_t p) { return p ? p->launches : 0; }
+
+fkk_status fkk_debug_tc_mma(int32_t mode, const float* d_A, const float* d_B, float* d_D, int32_t N) {
+  if (!d_A || !d_B || !d_D || N < 16 || N > 256 || N % 16) return FKK_ERR_INVALID_ARG;
+  try {
+    fkk::launch_tc_selftest(mode, d_A, d_B, d_D, N, nullptr);
+    FKK_CUDA_CHECK(cudaDeviceSynchronize());
+    return FKK_OK;
+  } catch (const Status& e) {
+    g_create_err = e.what();
+    return (fkk_status)e.code;
+  }
+}
 
 fkk_status fkk_host_eig_topk(const double* G, int32_t M, int32_t k, double* V, double* lam) {
   if (!G || !V || !lam || M < 1 || k < 1 || k > M) return FKK_ERR_INVALID_ARG;

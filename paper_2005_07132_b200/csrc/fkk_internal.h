@@ -103,6 +103,8 @@ void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vse
 size_t eig_workspace_doubles(int M, int k);
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, cudaStream_t s);
 
+void launch_tc_selftest(int mode, const float* A, const float* B, float* D, int N, cudaStream_t s);
+
 // ---- host eigensolver (host_eig.cpp): returns 0 on success
 int host_eig_topk(const double* G, int M, int k, double* V /* k vectors of length M */, double* lam);
 

@@ -1,15 +1,26 @@
 // Gram matrix G0 = A0^T A0 (F2, the normal matrix of the truncated SVD) on the
-// 5th-generation tensor cores: tcgen05.mma kind::tf32, 3xTF32 (hi*hi + hi*lo + lo*hi, reading A22),
-// fp32 accumulation in TMEM over <= 8192 pixels, then an fp64 flush into this CTA's own partial tile
-// (deterministic; summed over the row splits by gram_tc_reduce).
+// 5th-generation tensor cores: tcgen05.mma kind::tf32 with the 3xTF32 split (reading A22):
+//   G ~ hi_i hi_j + (hi_i lo_j + lo_i hi_j),  hi = rna_tf32(x), lo = rna_tf32(x - hi).
 //
-// Tiles of G: 128 (i) x 256 (j) covering the upper triangle; the CTA for (tile, split) streams the
-// pixels of its split.  Both operands are MN-major in smem (the channel index is contiguous in A0):
-// a core matrix is 8 pixels (K) x 16 B (4 channels); a 4-channel column strip holds the KC pixels of
-// a stage contiguously and strips are SBO = 16*KC + 16 bytes apart (the 16-B pad makes the producer's
-// 128-bit smem stores bank-conflict free).
-//   warps 0-3 : producers (global fp32 loads, tf32 hi/lo split, st.shared) and the TMEM epilogue
-//   warp 4    : TMEM allocation and the single-thread MMA issue
+// Accuracy design (measured on B200): the tensor-core fp32 accumulator
+// truncates on every add (~0.4 half-ulp bias per tcgen05.mma), so a long TMEM accumulation drifts
+// (-3e-5 relative after 8192 pixels).  Hence
+//   * hi*hi and the two cross terms accumulate in separate TMEM accumulators (the cross-term sum is
+//     2^-11 smaller, its bias negligible);
+//   * every GPERIOD = 128 pixels the accumulators are drained by 4 epilogue warps into an fp32
+//     running sum held in registers (IEEE round-to-nearest adds), double-buffered so the MMAs on
+//     the other accumulator pair continue; every 8192 pixels the running sum is added into this
+//     CTA's fp64 partial tile (deterministic; summed over the row splits by gram_tc_reduce).
+//
+// Tiles: 128 x 128 blocks (ti <= tj) of G; CTA = (tile, row split).  Operands K-major in smem
+// (K = pixel): core matrix = 8 channels x 16 B (4 pixels); the KC/4 core matrices of an
+// 8-channel group are contiguous (LBO = 128 B), groups SBO = 32*KC + 16 B apart (pad: conflict-free
+// 128-bit stores).  A0 is channel-contiguous, so a producer thread loads 4 pixels x 4 channels
+// (four float4) and transposes them in registers into four 16-B core-matrix rows.
+//   warps 0-7  : producers (fp32 loads one stage ahead in registers, tf32 hi/lo split, st.shared)
+//   warps 8-15 : epilogue (tcgen05.ld of TMEM lanes 32*(w%4)..; two warps per lane group, 64 columns
+//                each; fp32 running sum in registers, fp64 flush)
+//   warp 16    : TMEM allocation and the single-thread tcgen05.mma issue
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,188 +33,218 @@ namespace fkk {
 
 namespace {
 
-constexpr int GB_M = 128;                 // tile rows (i)
-constexpr int GB_N = 256;                 // tile cols (j)
-constexpr int GKC = 32;                   // pixels per stage
-constexpr int GSTAGES = 2;
-constexpr int GFLUSH = 8192;              // fp32 accumulation span in pixels
-constexpr int GSTRIP = GKC * 16 + 16;     // bytes per 4-channel strip (SBO)
-constexpr int GA_BYTES = (GB_M / 4) * GSTRIP;   // 16896
-constexpr int GB_BYTES = (GB_N / 4) * GSTRIP;   // 33792
-constexpr int GSTAGE_BYTES = 2 * GA_BYTES + 2 * GB_BYTES;
+constexpr int GT = 128;                    // tile edge (i and j)
+constexpr int GKC = 32;                    // pixels per stage
+constexpr int GSTAGES = 3;
+constexpr int GPERIOD = 128;               // pixels per TMEM accumulation period
+constexpr int GFLUSH = 8192;               // pixels per fp64 flush of the register sum
+constexpr int GLBO = 128;                  // K-adjacent core matrices
+constexpr int GSBO = (GKC / 4) * GLBO + 16;   // 8-channel groups: 1040 B
+constexpr int GOP_BYTES = (GT / 8) * GSBO;    // one 128-channel operand, hi or lo: 16640 B
+constexpr int GSTAGE_BYTES = 4 * GOP_BYTES;   // A hi, A lo, B hi, B lo
 constexpr int GSMEM = GSTAGES * GSTAGE_BYTES + 256;
-constexpr int GTHREADS = 160;
+constexpr int GPROD = 256;                 // producer threads
+constexpr int GTHREADS = 544;
+constexpr uint32_t GTMEM_COLS = 512;       // 2 buffers x (hi 128 + mid 128)
+
+static_assert(GFLUSH % GPERIOD == 0 && GPERIOD % GKC == 0, "period layout");
+
+// 4 pixels x 4 channels of A0 (four float4, channel-contiguous rows)
+__device__ __forceinline__ void load_block(const float* __restrict__ A, int M, int64_t px0, int64_t pend, int col,
+                                           float4 (&x)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    x[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (px0 + q < pend && col < M) x[q] = __ldg(reinterpret_cast<const float4*>(A + (px0 + q) * (int64_t)M + col));
+  }
+}
+// -> tf32 hi/lo -> four 16-B K-major core-matrix rows (channel c4*4+e, pixels 4*p4..4*p4+3)
+__device__ __forceinline__ void store_block(const float4 (&x)[4], unsigned char* hi_base, unsigned char* lo_base,
+                                            int c4, int p4) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int r = c4 * 4 + e;
+    const int off = (r >> 3) * GSBO + p4 * GLBO + (r & 7) * 16;
+    const float v0 = e == 0 ? x[0].x : e == 1 ? x[0].y : e == 2 ? x[0].z : x[0].w;
+    const float v1 = e == 0 ? x[1].x : e == 1 ? x[1].y : e == 2 ? x[1].z : x[1].w;
+    const float v2 = e == 0 ? x[2].x : e == 1 ? x[2].y : e == 2 ? x[2].z : x[2].w;
+    const float v3 = e == 0 ? x[3].x : e == 1 ? x[3].y : e == 2 ? x[3].z : x[3].w;
+    float4 h, l;
+    tc::split_tf32(v0, h.x, l.x);
+    tc::split_tf32(v1, h.y, l.y);
+    tc::split_tf32(v2, h.z, l.z);
+    tc::split_tf32(v3, h.w, l.w);
+    *reinterpret_cast<float4*>(hi_base + off) = h;
+    *reinterpret_cast<float4*>(lo_base + off) = l;
+  }
+}
 
 __global__ void __launch_bounds__(GTHREADS, 1)
 gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __restrict__ tiles, int ntiles,
                double* __restrict__ partials) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GSTAGES * GSTAGE_BYTES);
-  uint64_t* full = bars;                  // [GSTAGES]
-  uint64_t* empty = bars + GSTAGES;       // [GSTAGES]
-  uint64_t* acc_full = bars + 2 * GSTAGES;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* full = bars;                  // [GSTAGES]  producers -> MMA
+  uint64_t* empty = bars + GSTAGES;       // [GSTAGES]  MMA commit -> producers
+  uint64_t* acc_full = bars + 2 * GSTAGES;    // [2] MMA commit -> epilogue
+  uint64_t* acc_empty = acc_full + 2;         // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = blockIdx.x % ntiles, split = blockIdx.x / ntiles, nsplit = gridDim.x / ntiles;
   const int ti = tiles[t].x, tj = tiles[t].y;
+  const bool diag = ti == tj;
   const int64_t rb = n * split / nsplit, re = n * (split + 1) / nsplit;
-  double* part = partials + (int64_t)blockIdx.x * (GB_M * GB_N);   // [j][i] layout
+  const int64_t nper = re > rb ? (re - rb + GPERIOD - 1) / GPERIOD : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < GSTAGES; ++s) { tc::mbar_init(&full[s], 128); tc::mbar_init(&empty[s], 1); }
-    tc::mbar_init(acc_full, 1);
-    tc::mbar_init(acc_empty, 128);
+    for (int s = 0; s < GSTAGES; ++s) { tc::mbar_init(&full[s], GPROD); tc::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 256); }
     tc::fence_mbar_init();
   }
-  if (warp == 4) tc::tmem_alloc(tmem_slot, GB_N);
+  if (warp == 16) tc::tmem_alloc(tmem_slot, GTMEM_COLS);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t nchunks = re > rb ? (re - rb + GFLUSH - 1) / GFLUSH : 0;
-  if (warp < 4) {
-    // ------------------------------------------------------------ producers + epilogue
+  if (warp < 8) {
+    // ------------------------------------------------------------ producers (one item per operand)
+    const int c4 = tid & 31, p4 = tid >> 5;     // channel quad, pixel quad
+    float4 xa[4], xb[4];
+    int64_t k0 = rb;
+    if (k0 < re) {
+      load_block(A, M, k0 + 4 * p4, re, ti * GT + 4 * c4, xa);
+      if (!diag) load_block(A, M, k0 + 4 * p4, re, tj * GT + 4 * c4, xb);
+    }
     int stage = 0;
-    uint32_t phase = 0, acc_phase = 0;
-    for (int64_t ch = 0; ch < nchunks; ++ch) {
-      const int64_t c0 = rb + ch * GFLUSH, c1 = (re < c0 + GFLUSH) ? re : (c0 + GFLUSH);
-      for (int64_t k0 = c0; k0 < c1; k0 += GKC) {
-        tc::mbar_wait(&empty[stage], phase ^ 1);
-        unsigned char* st = smem + stage * GSTAGE_BYTES;
-        unsigned char* ahi = st;
-        unsigned char* alo = st + GA_BYTES;
-        unsigned char* bhi = st + 2 * GA_BYTES;
-        unsigned char* blo = bhi + GB_BYTES;
-        // A block: 32 pixels x 128 channels (i = ti*128 ..), 8 float4 per thread
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const int idx = tid + h * 128;
-          const int row = idx >> 5, c4 = idx & 31;
-          const int64_t px = k0 + row;
-          const int col = ti * GB_M + c4 * 4;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (px < c1 && col < M) v = __ldg(reinterpret_cast<const float4*>(A + px * (int64_t)M + col));
-          float4 hi, lo;
-          tc::split4(v, hi, lo);
-          const int off = c4 * GSTRIP + row * 16;
-          *reinterpret_cast<float4*>(ahi + off) = hi;
-          *reinterpret_cast<float4*>(alo + off) = lo;
-        }
-        // B block: 32 pixels x 256 channels (j = tj*256 ..), 16 float4 per thread
-#pragma unroll
-        for (int h = 0; h < 16; ++h) {
-          const int idx = tid + h * 128;
-          const int row = idx >> 6, c4 = idx & 63;
-          const int64_t px = k0 + row;
-          const int col = tj * GB_N + c4 * 4;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (px < c1 && col < M) v = __ldg(reinterpret_cast<const float4*>(A + px * (int64_t)M + col));
-          float4 hi, lo;
-          tc::split4(v, hi, lo);
-          const int off = c4 * GSTRIP + row * 16;
-          *reinterpret_cast<float4*>(bhi + off) = hi;
-          *reinterpret_cast<float4*>(blo + off) = lo;
-        }
-        tc::fence_proxy_async_smem();
-        tc::mbar_arrive(&full[stage]);
-        stage ^= 1;
-        if (stage == 0) phase ^= 1;
+    uint32_t phase = 0;
+    for (; k0 < re; k0 += GKC) {
+      tc::mbar_wait(&empty[stage], phase ^ 1);
+      unsigned char* st = smem + stage * GSTAGE_BYTES;
+      store_block(xa, st, st + GOP_BYTES, c4, p4);
+      if (!diag) store_block(xb, st + 2 * GOP_BYTES, st + 3 * GOP_BYTES, c4, p4);
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full[stage]);
+      if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
+      const int64_t kn = k0 + GKC;           // prefetch the next stage into registers
+      if (kn < re) {
+        load_block(A, M, kn + 4 * p4, re, ti * GT + 4 * c4, xa);
+        if (!diag) load_block(A, M, kn + 4 * p4, re, tj * GT + 4 * c4, xb);
       }
-      // flush the fp32 accumulator: TMEM lane = i (row), column = j; partial layout [j][i]
-      tc::mbar_wait(acc_full, acc_phase);
-      acc_phase ^= 1;
-      tc::tc_fence_after();
-      const int i = warp * 32 + lane;
-#pragma unroll 1
-      for (int cb = 0; cb < GB_N / 16; ++cb) {
-        float v[16];
-        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cb * 16), v);
+    }
+  } else if (warp < 16) {
+    // ------------------------------------------------------------ epilogue
+    const int lg = warp & 3;                       // TMEM lane group (warp % 4)
+    const int chalf = (warp - 8) >> 2;             // column half: 0 -> 0..63, 1 -> 64..127
+    const int i = lg * 32 + lane;                  // tile row
+    double* part = partials + (int64_t)blockIdx.x * (GT * GT);   // [j][i]
+    float S[64];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          double* p = part + (int64_t)(cb * 16 + q) * GB_M + i;
-          *p = (ch == 0 ? 0.0 : *p) + (double)v[q];
-        }
+    for (int q = 0; q < 64; ++q) S[q] = 0.f;
+    uint32_t ph[2] = {0, 0};
+    bool first = true;
+    for (int64_t pidx = 0; pidx < nper; ++pidx) {
+      const int b = (int)(pidx & 1);
+      tc::mbar_wait(&acc_full[b], ph[b]);
+      ph[b] ^= 1;
+      tc::tc_fence_after();
+      const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 64 * chalf);
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        float h[16], m[16];
+        tc::tmem_ld16(tb + cb * 16, h);
+        tc::tmem_ld16(tb + 128 + cb * 16, m);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) S[cb * 16 + q] += h[q] + m[q];
       }
       tc::tc_fence_before();
-      tc::mbar_arrive(acc_empty);
+      tc::mbar_arrive(&acc_empty[b]);
+      const bool last = pidx == nper - 1;
+      if (last || ((pidx + 1) * GPERIOD) % GFLUSH == 0) {
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          double* p = part + (int64_t)(64 * chalf + q) * GT + i;
+          *p = (first ? 0.0 : *p) + (double)S[q];
+          S[q] = 0.f;
+        }
+        first = false;
+      }
     }
-    if (nchunks == 0) {
-      for (int e = tid; e < GB_M * GB_N; e += 128) part[e] = 0.0;
-    }
+    if (nper == 0)
+      for (int q = 0; q < 64; ++q) part[(int64_t)(64 * chalf + q) * GT + i] = 0.0;
   } else if (lane == 0) {
     // ------------------------------------------------------------ single-thread MMA issue
-    constexpr uint32_t idesc = tc::make_idesc_tf32(GB_M, GB_N, true, true);
+    constexpr uint32_t idesc = tc::make_idesc_tf32(GT, GT, false, false);
     int stage = 0;
-    uint32_t phase = 0, acc_empty_phase = 0;
+    uint32_t phase = 0;
+    uint32_t eph[2] = {0, 0};
     const uint32_t sbase = tc::smem_u32(smem);
-    for (int64_t ch = 0; ch < nchunks; ++ch) {
-      const int64_t c0 = rb + ch * GFLUSH, c1 = (re < c0 + GFLUSH) ? re : (c0 + GFLUSH);
-      if (ch > 0) {
-        tc::mbar_wait(acc_empty, acc_empty_phase);
-        acc_empty_phase ^= 1;
+    for (int64_t pidx = 0; pidx < nper; ++pidx) {
+      const int b = (int)(pidx & 1);
+      if (pidx >= 2) {
+        tc::mbar_wait(&acc_empty[b], eph[b]);
+        eph[b] ^= 1;
         tc::tc_fence_after();
       }
+      const uint32_t d_hi = tmem + 256 * b, d_mid = d_hi + 128;
+      const int64_t p0 = rb + pidx * GPERIOD, p1 = (re < p0 + GPERIOD) ? re : (p0 + GPERIOD);
       uint32_t acc = 0;
-      for (int64_t k0 = c0; k0 < c1; k0 += GKC) {
+      for (int64_t k0 = p0; k0 < p1; k0 += GKC) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
         const uint32_t st = sbase + stage * GSTAGE_BYTES;
-        const uint32_t ahi = st, alo = st + GA_BYTES, bhi = st + 2 * GA_BYTES, blo = bhi + GB_BYTES;
+        const uint32_t ahi = st, alo = st + GOP_BYTES;
+        const uint32_t bhi = diag ? ahi : st + 2 * GOP_BYTES, blo = diag ? alo : st + 3 * GOP_BYTES;
 #pragma unroll
         for (int ks = 0; ks < GKC / 8; ++ks) {
-          const uint32_t ko = ks * 128;   // 8 pixels x 16 B
-          const uint64_t dah = tc::make_sdesc(ahi + ko, 128, GSTRIP), dal = tc::make_sdesc(alo + ko, 128, GSTRIP);
-          const uint64_t dbh = tc::make_sdesc(bhi + ko, 128, GSTRIP), dbl = tc::make_sdesc(blo + ko, 128, GSTRIP);
-          tc::mma_tf32(tmem, dal, dbh, idesc, acc);   // lo * hi
+          const uint32_t ko = ks * 2 * GLBO;   // 8 pixels = 2 K-core matrices
+          const uint64_t dah = tc::make_sdesc(ahi + ko, GLBO, GSBO), dal = tc::make_sdesc(alo + ko, GLBO, GSBO);
+          const uint64_t dbh = tc::make_sdesc(bhi + ko, GLBO, GSBO), dbl = tc::make_sdesc(blo + ko, GLBO, GSBO);
+          tc::mma_tf32(d_mid, dal, dbh, idesc, acc);   // lo_i * hi_j
+          tc::mma_tf32(d_mid, dah, dbl, idesc, 1);     // hi_i * lo_j
+          tc::mma_tf32(d_hi, dah, dbh, idesc, acc);    // hi_i * hi_j
           acc = 1;
-          tc::mma_tf32(tmem, dah, dbl, idesc, 1);     // hi * lo
-          tc::mma_tf32(tmem, dah, dbh, idesc, 1);     // hi * hi
         }
         tc::mma_commit(&empty[stage]);
-        stage ^= 1;
-        if (stage == 0) phase ^= 1;
+        if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
       }
-      tc::mma_commit(acc_full);
+      tc::mma_commit(&acc_full[b]);
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 4) tc::tmem_dealloc(tmem, GB_N);
+  if (warp == 16) tc::tmem_dealloc(tmem, GTMEM_COLS);
 }
 
 __global__ void gram_tc_reduce_kernel(const double* __restrict__ partials, int ntiles, int nsplit, int M,
-                                      const int* __restrict__ tile_of, int nTj, double* __restrict__ G, int accumulate) {
+                                      const int* __restrict__ tile_of, int nT, double* __restrict__ G, int accumulate) {
   const int64_t total = (int64_t)M * M;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e / M), c = (int)(e % M);
     const int i = min(r, c), j = max(r, c);
-    const int ti = i / GB_M, tj = j / GB_N;
-    const int t = tile_of[ti * nTj + tj];
-    const int64_t off = (int64_t)(j - tj * GB_N) * GB_M + (i - ti * GB_M);
+    const int ti = i / GT, tj = j / GT;
+    const int t = tile_of[ti * nT + tj];
+    const int64_t off = (int64_t)(j - tj * GT) * GT + (i - ti * GT);
     double s = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) s += partials[((int64_t)sp * ntiles + t) * (GB_M * GB_N) + off];
+    for (int sp = 0; sp < nsplit; ++sp) s += partials[((int64_t)sp * ntiles + t) * (GT * GT) + off];
     G[e] = accumulate ? G[e] + s : s;
   }
 }
 
 }  // namespace
 
-// Tile list of the upper triangle: (ti, tj) with tj*256 + 255 >= ti*128.
-void gram_tc_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nTj) {
-  const int nTi = (M + GB_M - 1) / GB_M;
-  nTj = (M + GB_N - 1) / GB_N;
+// Tile list of the upper triangle of 128 x 128 blocks (ti <= tj).
+void gram_tc_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nT) {
+  nT = (M + GT - 1) / GT;
   tiles.clear();
-  tile_of.assign((size_t)nTi * nTj, -1);
-  for (int ti = 0; ti < nTi; ++ti)
-    for (int tj = 0; tj < nTj; ++tj)
-      if (tj * GB_N + GB_N - 1 >= ti * GB_M) {
-        tile_of[ti * nTj + tj] = (int)tiles.size();
-        tiles.push_back(make_int2(ti, tj));
-      }
+  tile_of.assign((size_t)nT * nT, -1);
+  for (int ti = 0; ti < nT; ++ti)
+    for (int tj = ti; tj < nT; ++tj) {
+      tile_of[ti * nT + tj] = (int)tiles.size();
+      tiles.push_back(make_int2(ti, tj));
+    }
 }
 
 int gram_tc_splits(int ntiles, int64_t n) {
@@ -215,7 +256,7 @@ int gram_tc_splits(int ntiles, int64_t n) {
   return (int)std::min<int64_t>(ns, by_rows);
 }
 
-size_t gram_tc_partial_doubles(int ntiles, int nsplit) { return (size_t)ntiles * nsplit * GB_M * GB_N; }
+size_t gram_tc_partial_doubles(int ntiles, int nsplit) { return (size_t)ntiles * nsplit * GT * GT; }
 
 void launch_gram_tc(const float* A, int64_t n, int M, const int2* d_tiles, int ntiles, int nsplit, double* partials,
                     cudaStream_t s) {
@@ -224,9 +265,9 @@ void launch_gram_tc(const float* A, int64_t n, int M, const int2* d_tiles, int n
   check_launch("gram_tc");
 }
 
-void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nTj,
+void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nT,
                            double* G, int accumulate, cudaStream_t s) {
-  gram_tc_reduce_kernel<<<1024, 256, 0, s>>>(partials, ntiles, nsplit, M, d_tile_of, nTj, G, accumulate);
+  gram_tc_reduce_kernel<<<1024, 256, 0, s>>>(partials, ntiles, nsplit, M, d_tile_of, nT, G, accumulate);
   check_launch("gram_tc_reduce");
 }
 

@@ -77,6 +77,7 @@ _SIGS = {
     "fkk_stage_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _i32]),
     "fkk_last_launch_count": (_i64, [_vp]),
     "fkk_host_eig_topk": (_i32, [_dp, _i32, _i32, _dp, _dp]),
+    "fkk_debug_tc_mma": (_i32, [_i32, _vp, _vp, _vp, _i32]),
     "fkk_shard_range": (None, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fkk_merge_extremes": (_i32, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_i64), _i32, _i32,
                                   ctypes.POINTER(_i64)]),
@@ -337,6 +338,14 @@ def fkk_apply_trained_basis(plan: Plan, basis: Basis, I, out=None):
 
 def kk_direct_batch(plan: Plan, I, Iref, out=None):
     return plan.direct(I, Iref, out)
+
+
+def fkk_debug_tc_mma(mode: int, A, B):
+    """Tensor-core self-test: D = tf32(A) tf32(B)^T through one tcgen05.mma (A 128x8, B Nx8 CUDA fp32)."""
+    torch = _torch()
+    D = torch.zeros((128, B.shape[0]), dtype=torch.float32, device=A.device)
+    _check(None, _lib.fkk_debug_tc_mma(mode, _dev_ptr(A, "A"), _dev_ptr(B, "B"), _dev_ptr(D, "D"), B.shape[0]))
+    return D
 
 
 def fkk_get_nccl_unique_id() -> bytes:
