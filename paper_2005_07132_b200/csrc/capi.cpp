@@ -85,10 +85,12 @@ struct fkk_basis {
   double* f64 = nullptr;
   float* W = nullptr;    // M x kp, D_f V diag(s^2/(s^2+lam_ml))
   float* Bi = nullptr;   // k x M x 2
+  float* bimg = nullptr; // tensor-core B image (reconstruct_tc)
+  bool bimg_valid = false;
   double* V64 = nullptr;
   std::vector<double> s;
   ~fkk_basis() {
-    cudaFree(inv_ref); cudaFree(ref64); cudaFree(f64); cudaFree(W); cudaFree(Bi); cudaFree(V64);
+    cudaFree(inv_ref); cudaFree(ref64); cudaFree(f64); cudaFree(W); cudaFree(Bi); cudaFree(V64); cudaFree(bimg);
   }
 };
 
@@ -130,6 +132,7 @@ struct fkk_plan {
          *XtPhi = nullptr, *Phi_pec = nullptr, *HPhi = nullptr, *tmp = nullptr, *Vsec = nullptr, *ridge_work = nullptr,
          *lam = nullptr, *basis_als_state = nullptr;
   float* Bi = nullptr;
+  float* bimg = nullptr;
   double* eig_work = nullptr;
   double* lam_d = nullptr;
   // tcgen05 Gram
@@ -163,7 +166,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
@@ -312,7 +315,7 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->f32 = dalloc<float>(M);
   p->V64 = dalloc<double>((size_t)M * k);
   p->W = dalloc<float>((size_t)M * kp);
-  p->US = dalloc<float>((size_t)n * k);
+  p->US = dalloc<float>((size_t)n * kp);   // row stride kp, zero-padded columns
   const int nblk = fkk::project_num_blocks(n);
   p->ext_val = dalloc<float>((size_t)nblk * k * 2);
   p->ext_idx = dalloc<int64_t>((size_t)nblk * k * 2);
@@ -335,6 +338,7 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->lam = dalloc<double>(1);
   p->basis_als_state = dalloc<double>((size_t)3 * M * (((nqc + 31) / 32) * 32));
   p->Bi = dalloc<float>((size_t)k * M * 2);
+  p->bimg = dalloc<float>(fkk::reconstruct_tc_bimg_floats(k, M));
   p->eig_work = dalloc<double>(fkk::eig_workspace_doubles(M, k));
   p->lam_d = dalloc<double>(k);
   if (d->world_size > 1) {
@@ -432,7 +436,7 @@ void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
-    fkk::launch_project_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->W, k, kp, p->US + r0 * (int64_t)k, p->ext_val,
+    fkk::launch_project_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->W, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
                              p->ext_idx, row0 + r0, s);
     if (r1 > r0)
       fkk::launch_extremes_reduce(p->ext_val, p->ext_idx, fkk::project_num_blocks(r1 - r0), k,
@@ -486,7 +490,7 @@ void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_
   std::vector<int64_t> ql(nq);
   for (int i = 0; i < nq; ++i) ql[i] = (q[i] >= row0 && q[i] < row0 + n_rows) ? q[i] - row0 : -1;
   FKK_CUDA_CHECK(cudaMemcpyAsync(p->q_dev, ql.data(), nq * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  fkk::launch_gather_rows(p->US, k, p->q_dev, nq, p->X, s);
+  fkk::launch_gather_rows(p->US, k, kp, p->q_dev, nq, p->X, s);
   FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // ql is a stack buffer
   if (p->d.world_size > 1)
     nccl_check(g_nccl.AllReduce(p->X, p->X, (size_t)nq * k, ncclFloat64, ncclSum, p->comm, s), "AllReduce(X)");
@@ -504,9 +508,13 @@ void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_
   fkk::launch_add_f64(p->Vt_f, p->HPhi, p->tmp, (int64_t)k * M, s);
   fkk::launch_sg_rows_f64(p->tmp, k, M, p->sg_half, p->Vsec, s);                                  // Eq. 22
   fkk::launch_assemble_B(p->Vt_f, p->HPhi, p->Vsec, p->Hv, p->Phi_pec, k, M, p->Bi, s);           // Eq. 23
+  if (p->d.gemm_impl == FKK_GEMM_3XTF32) fkk::launch_build_bimg(p->Bi, k, M, p->bimg, s);
   p->mark("basis");
   // ---- reconstruction (F11)
-  fkk::launch_reconstruct_simt(p->US, n_rows, k, p->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  if (p->d.gemm_impl == FKK_GEMM_3XTF32)
+    fkk::launch_reconstruct_tc(p->US, n_rows, k, kp, p->bimg, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  else
+    fkk::launch_reconstruct_simt(p->US, n_rows, k, kp, p->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
   p->mark("reconstruct");
   p->last_rows = n_rows;
   p->last_row0 = row0;
@@ -526,6 +534,12 @@ fkk_basis* export_basis(fkk_plan* p) {
   b->W = dalloc<float>((size_t)M * kp);
   b->Bi = dalloc<float>((size_t)k * M * 2);
   b->V64 = dalloc<double>((size_t)M * k);
+  b->bimg = dalloc<float>(fkk::reconstruct_tc_bimg_floats(k, M));
+  if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
+    FKK_CUDA_CHECK(cudaMemcpyAsync(b->bimg, p->bimg, fkk::reconstruct_tc_bimg_floats(k, M) * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, s));
+    b->bimg_valid = true;
+  }
   FKK_CUDA_CHECK(cudaMemcpyAsync(b->inv_ref, p->inv_ref, M * sizeof(float), cudaMemcpyDeviceToDevice, s));
   FKK_CUDA_CHECK(cudaMemcpyAsync(b->ref64, p->ref64, M * sizeof(double), cudaMemcpyDeviceToDevice, s));
   FKK_CUDA_CHECK(cudaMemcpyAsync(b->f64, p->f64, M * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -596,7 +610,12 @@ void apply_run(fkk_plan* p, fkk_basis* b, const void* d_icars, int64_t n_rows, v
   p->mark("logratio");
   fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
   p->mark("project");
-  fkk::launch_reconstruct_simt(p->US, n_rows, b->k, b->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
+    if (!b->bimg_valid) { fkk::launch_build_bimg(b->Bi, b->k, M, b->bimg, s); b->bimg_valid = true; }
+    fkk::launch_reconstruct_tc(p->US, n_rows, b->k, b->kp, b->bimg, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  } else {
+    fkk::launch_reconstruct_simt(p->US, n_rows, b->k, b->kp, b->Bi, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+  }
   p->mark("reconstruct");
 }
 
@@ -895,7 +914,12 @@ fkk_status fkk_get_stage(fkk_plan_t p, int32_t stage, void* dst, size_t bytes, i
     }
     cudaMemcpyKind kind = host_src ? (dst_is_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost)
                                    : (dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
-    FKK_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, kind, p->stream));
+    if (stage == FKK_STAGE_US) {   // stored with row stride kp
+      const size_t rows = n / ((size_t)p->k * 4);
+      if (rows) FKK_CUDA_CHECK(cudaMemcpy2DAsync(dst, (size_t)p->k * 4, src, (size_t)p->kp * 4, (size_t)p->k * 4, rows, kind, p->stream));
+    } else {
+      FKK_CUDA_CHECK(cudaMemcpyAsync(dst, src, n, kind, p->stream));
+    }
     FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
   });
 }

@@ -46,7 +46,7 @@ void launch_fill_f(float* p, float v, int64_t n, cudaStream_t s);
 void launch_scale_gram(double* G, const double* f, int M, cudaStream_t s);
 void launch_cast_w(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* W,
                    cudaStream_t s);
-void launch_gather_rows(const float* US, int k, const int64_t* q_local, int nq, double* X, cudaStream_t s);
+void launch_gather_rows(const float* US, int k, int ldus, const int64_t* q_local, int nq, double* X, cudaStream_t s);
 void launch_extremes_reduce(const float* ext_val, const int64_t* ext_idx, int nblk, int k, float* out_val,
                             int64_t* out_idx, cudaStream_t s);
 void launch_add_f64(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
@@ -80,9 +80,16 @@ void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M
 int project_num_blocks(int64_t n);
 void launch_project_simt(const float* A, int64_t n, int M, const float* W, int k, int kp, float* US, float* ext_val,
                          int64_t* ext_idx, int64_t row_offset, cudaStream_t s);
-// Reconstruction K = exp(US B_amp) e^{i US B_ph} (k_reconstruct.cu); Bi: k x M x 2 (amp, ph).
-void launch_reconstruct_simt(const float* US, int64_t n, int k, const float* Bi, int M, void* out, int out_imag_only,
-                             cudaStream_t s);
+// Reconstruction K = exp(US B_amp) e^{i US B_ph} (k_reconstruct.cu); Bi: k x M x 2 (amp, ph);
+// US: n x ldus fp32 (ldus >= k, columns >= k zero).
+void launch_reconstruct_simt(const float* US, int64_t n, int k, int ldus, const float* Bi, int M, void* out,
+                             int out_imag_only, cudaStream_t s);
+// tcgen05 3xTF32 reconstruction (k_reconstruct_tc.cu): B image (K-major core matrices, hi/lo) built
+// once per basis; bimg_floats() gives its size.
+size_t reconstruct_tc_bimg_floats(int k, int M);
+void launch_build_bimg(const float* Bi, int k, int M, float* bimg, cudaStream_t s);
+void launch_reconstruct_tc(const float* US, int64_t n, int k, int ldus, const float* bimg, int M, void* out,
+                           int out_imag_only, cudaStream_t s);
 // Basis (k_basis.cu): all fp64, tiny.
 void launch_hilbert_rows_f64(const double* X, int rows, int M, int ldx, double* out, int L, int pad_zero,
                              const double2* tw, cudaStream_t s);

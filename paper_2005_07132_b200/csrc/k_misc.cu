@@ -114,11 +114,11 @@ __global__ void cast_w_kernel(const double* V, const double* fscale, const doubl
   }
 }
 
-__global__ void gather_kernel(const float* US, int k, const int64_t* q, int nq, double* X) {
+__global__ void gather_kernel(const float* US, int k, int ldus, const int64_t* q, int nq, double* X) {
   const int r = blockIdx.x;
   if (r >= nq) return;
   const int64_t row = q[r];
-  for (int c = threadIdx.x; c < k; c += blockDim.x) X[(int64_t)r * k + c] = row >= 0 ? (double)US[row * k + c] : 0.0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) X[(int64_t)r * k + c] = row >= 0 ? (double)US[row * ldus + c] : 0.0;
 }
 
 __global__ void extremes_reduce_kernel(const float* val, const int64_t* idx, int nblk, int k, float* oval,
@@ -221,9 +221,9 @@ void launch_cast_w(const double* V, const double* fscale, const double* cscale, 
   check_launch("cast_w");
 }
 
-void launch_gather_rows(const float* US, int k, const int64_t* q_local, int nq, double* X, cudaStream_t s) {
+void launch_gather_rows(const float* US, int k, int ldus, const int64_t* q_local, int nq, double* X, cudaStream_t s) {
   if (nq <= 0) return;
-  gather_kernel<<<nq, 128, 0, s>>>(US, k, q_local, nq, X);
+  gather_kernel<<<nq, 128, 0, s>>>(US, k, ldus, q_local, nq, X);
   check_launch("gather");
 }
 

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) project_simt_kernel(const float* __restri
       const int64_t p = p0 + pl;
       if (p < n) {
         const float v = acc[x][y];
-        if (c < k) US[p * k + c] = v;
+        US[p * KP + c] = v;   // stride kp; columns >= k are exact zeros (W padded with zeros)
         if (v > vmax) { vmax = v; imax = pl; }   // ascending pl: strict > keeps the lowest index
         if (v < vmin) { vmin = v; imin = pl; }
       }

@@ -27,7 +27,7 @@ __device__ __forceinline__ float2 cis_exp(float amp, float ph) {
   return make_float2(m * cs, m * sn);
 }
 
-__global__ void __launch_bounds__(256) reconstruct_simt_kernel(const float* __restrict__ US, int64_t n, int k,
+__global__ void __launch_bounds__(256) reconstruct_simt_kernel(const float* __restrict__ US, int64_t n, int k, int ldus,
                                                                const float* __restrict__ Bi, int M,
                                                                void* __restrict__ out, int imag_only) {
   __shared__ __align__(16) float Us[RK][RP];          // [rank][pixel]
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) reconstruct_simt_kernel(const float* __re
     for (int idx = tid; idx < RK * RP; idx += 256) {
       const int pr = idx / RK, kk = idx % RK;
       const int64_t p = p0 + pr;
-      Us[kk][pr] = (p < n && k0 + kk < k) ? US[p * k + k0 + kk] : 0.f;
+      Us[kk][pr] = (p < n && k0 + kk < k) ? US[p * ldus + k0 + kk] : 0.f;
     }
     for (int idx = tid; idx < RK * RC; idx += 256) {
       const int kk = idx / RC, c = idx % RC;
@@ -89,11 +89,11 @@ __global__ void __launch_bounds__(256) reconstruct_simt_kernel(const float* __re
 
 }  // namespace
 
-void launch_reconstruct_simt(const float* US, int64_t n, int k, const float* Bi, int M, void* out, int out_imag_only,
-                             cudaStream_t s) {
+void launch_reconstruct_simt(const float* US, int64_t n, int k, int ldus, const float* Bi, int M, void* out,
+                             int out_imag_only, cudaStream_t s) {
   if (n <= 0) return;
   dim3 grid((unsigned)((n + RP - 1) / RP), (unsigned)((M + RC - 1) / RC));
-  reconstruct_simt_kernel<<<grid, 256, 0, s>>>(US, n, k, Bi, M, out, out_imag_only);
+  reconstruct_simt_kernel<<<grid, 256, 0, s>>>(US, n, k, ldus, Bi, M, out, out_imag_only);
   check_launch("reconstruct_simt");
 }
 
