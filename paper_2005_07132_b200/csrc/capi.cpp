@@ -87,10 +87,11 @@ struct fkk_basis {
   float* Bi = nullptr;   // k x M x 2
   float* bimg = nullptr; // tensor-core B image (reconstruct_tc)
   bool bimg_valid = false;
+  float* wimg = nullptr; // tensor-core W^T image (project_tc)
   double* V64 = nullptr;
   std::vector<double> s;
   ~fkk_basis() {
-    cudaFree(inv_ref); cudaFree(ref64); cudaFree(f64); cudaFree(W); cudaFree(Bi); cudaFree(V64); cudaFree(bimg);
+    cudaFree(inv_ref); cudaFree(ref64); cudaFree(f64); cudaFree(W); cudaFree(Bi); cudaFree(V64); cudaFree(bimg); cudaFree(wimg);
   }
 };
 
@@ -133,6 +134,7 @@ struct fkk_plan {
          *lam = nullptr, *basis_als_state = nullptr;
   float* Bi = nullptr;
   float* bimg = nullptr;
+  float* wimg = nullptr;
   double* eig_work = nullptr;
   double* lam_d = nullptr;
   // tcgen05 Gram
@@ -166,7 +168,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
@@ -339,6 +341,7 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->basis_als_state = dalloc<double>((size_t)3 * M * (((nqc + 31) / 32) * 32));
   p->Bi = dalloc<float>((size_t)k * M * 2);
   p->bimg = dalloc<float>(fkk::reconstruct_tc_bimg_floats(k, M));
+  p->wimg = dalloc<float>(fkk::project_tc_wimg_floats(M, kp));
   p->eig_work = dalloc<double>(fkk::eig_workspace_doubles(M, k));
   p->lam_d = dalloc<double>(k);
   if (d->world_size > 1) {
@@ -427,8 +430,10 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
 void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_q_in, int nq_in, void* d_out) {
   cudaStream_t s = p->stream;
   const int M = p->M, k = p->k, kp = p->kp;
-  // W = D_f V (fp32) and projection
-  fkk::launch_cast_w(p->V64, p->f64, nullptr, M, k, kp, p->W, s);
+  // W = D_f V (fp32 for the CUDA-core variant; a tf32 hi/lo W^T image for the tensor cores)
+  const bool tcg = p->d.gemm_impl == FKK_GEMM_3XTF32;
+  if (tcg) fkk::launch_build_wimg(p->V64, p->f64, nullptr, M, k, kp, p->wimg, s);
+  else fkk::launch_cast_w(p->V64, p->f64, nullptr, M, k, kp, p->W, s);
   const int shards = std::max(1, p->d.loopback_shards);
   std::vector<float> hv;
   std::vector<int64_t> hi;
@@ -436,8 +441,12 @@ void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
-    fkk::launch_project_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->W, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
-                             p->ext_idx, row0 + r0, s);
+    if (tcg)
+      fkk::launch_project_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->wimg, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
+                             p->ext_idx, row0 + r0, 1, s);
+    else
+      fkk::launch_project_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->W, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
+                               p->ext_idx, row0 + r0, s);
     if (r1 > r0)
       fkk::launch_extremes_reduce(p->ext_val, p->ext_idx, fkk::project_num_blocks(r1 - r0), k,
                                   p->ext_out_val + (size_t)sh * k * 2, p->ext_out_idx + (size_t)sh * k * 2, s);
@@ -555,6 +564,8 @@ fkk_basis* export_basis(fkk_plan* p) {
   double* dc = dalloc<double>(k);
   FKK_CUDA_CHECK(cudaMemcpyAsync(dc, c.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
   fkk::launch_cast_w(p->V64, p->f64, dc, M, k, kp, b->W, s);
+  b->wimg = dalloc<float>(fkk::project_tc_wimg_floats(M, kp));
+  fkk::launch_build_wimg(p->V64, p->f64, dc, M, k, kp, b->wimg, s);
   FKK_CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(dc);
   return b.release();
@@ -608,7 +619,10 @@ void apply_run(fkk_plan* p, fkk_basis* b, const void* d_icars, int64_t n_rows, v
   const int M = p->M;
   fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, b->inv_ref, b->ref64, (float)b->ratio_floor, p->A, p->flags, s);
   p->mark("logratio");
-  fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
+  if (p->d.gemm_impl == FKK_GEMM_3XTF32)
+    fkk::launch_project_tc(p->A, n_rows, M, b->wimg, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, 0, s);
+  else
+    fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
   p->mark("project");
   if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
     if (!b->bimg_valid) { fkk::launch_build_bimg(b->Bi, b->k, M, b->bimg, s); b->bimg_valid = true; }

@@ -67,16 +67,23 @@ __global__ void dgemm_small_kernel(int m, int n, int kk, const double* __restric
 }
 
 // Single CTA: lambda_max(C) by normalised repeated squaring, then the Cholesky factor of C + lam I
-// in Lw (lower, row-major k x k).  work: 2 k x k buffers.
+// in Lw (lower, row-major k x k).  The squarings run in shared memory when 2 k^2 doubles fit
+// (k <= 80), else in the global work buffers.  24 squarings: the final term log lambda_max(B_T) is
+// bracketed within log(k) and weighted 2^-24, i.e. lambda_max to ~3e-7 relative -- far below
+// anything the ridge weight (reading A11) is sensitive to.
+constexpr int kRidgeSquarings = 24;
+
 __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __restrict__ C, int k, double ridge_rel,
                                                             double* __restrict__ Lw, double* __restrict__ work,
                                                             double* __restrict__ lam_out, int* __restrict__ flags) {
+  extern __shared__ __align__(16) double shm[];
   __shared__ double red[32];
   __shared__ double sh_scal[2];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int kk = k * k;
-  double* B0 = work;
-  double* B1 = work + kk;
+  const bool in_smem = k <= 80;
+  double* B0 = in_smem ? shm : work;
+  double* B1 = in_smem ? shm + kk : work + kk;
   // trace
   double t = 0.0;
   for (int i = tid; i < k; i += nt) t += C[i * k + i];
@@ -90,7 +97,7 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
   for (int e = tid; e < kk; e += nt) B0[e] = C[e] / tr;
   __syncthreads();
   double wgt = 0.5;
-  for (int it = 0; it < 40; ++it) {
+  for (int it = 0; it < kRidgeSquarings; ++it) {
     for (int e = tid; e < kk; e += nt) {
       const int i = e / k, j = e % k;
       double s = 0.0;
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
     for (int e = tid; e < kk; e += nt) B0[e] = B1[e] / c;
     __syncthreads();
   }
-  // lambda_max(B_T) ~ ||B_T||_F (between lambda_max and sqrt(rank) lambda_max); weight 2^-40
+  // lambda_max(B_T) ~ ||B_T||_F (between lambda_max and sqrt(rank) lambda_max); weight 2^-T
   double fr = 0.0;
   for (int e = tid; e < kk; e += nt) fr += B0[e] * B0[e];
   fr = warp_sum(fr);
@@ -125,26 +132,29 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
   }
   __syncthreads();
   const double lam = sh_scal[0];
-  for (int e = tid; e < kk; e += nt) { const int i = e / k, j = e % k; Lw[e] = (j <= i) ? C[e] + (i == j ? lam : 0.0) : 0.0; }
+  double* L = in_smem ? shm : Lw;   // factor in smem when it fits, copied out at the end
+  for (int e = tid; e < kk; e += nt) { const int i = e / k, j = e % k; L[e] = (j <= i) ? C[e] + (i == j ? lam : 0.0) : 0.0; }
   __syncthreads();
   // right-looking Cholesky, lower triangle
   for (int j = 0; j < k; ++j) {
     if (tid == 0) {
-      const double d = Lw[j * k + j];
-      if (!(d > 0.0)) { atomicOr(flags, 4); Lw[j * k + j] = 1e-300; }
-      else Lw[j * k + j] = sqrt(d);
+      const double d = L[j * k + j];
+      if (!(d > 0.0)) { atomicOr(flags, 4); L[j * k + j] = 1e-300; }
+      else L[j * k + j] = sqrt(d);
     }
     __syncthreads();
-    const double djj = Lw[j * k + j];
-    for (int i = j + 1 + tid; i < k; i += nt) Lw[i * k + j] /= djj;
+    const double djj = L[j * k + j];
+    for (int i = j + 1 + tid; i < k; i += nt) L[i * k + j] /= djj;
     __syncthreads();
     const int rem = k - j - 1;
     for (int e = tid; e < rem * rem; e += nt) {
       const int i = j + 1 + e / rem, c = j + 1 + e % rem;
-      if (c <= i) Lw[i * k + c] -= Lw[i * k + j] * Lw[c * k + j];
+      if (c <= i) L[i * k + c] -= L[i * k + j] * L[c * k + j];
     }
     __syncthreads();
   }
+  if (in_smem)
+    for (int e = tid; e < kk; e += nt) Lw[e] = L[e];
 }
 
 __global__ void ridge_solve_kernel(const double* __restrict__ Lw, int k, const double* __restrict__ R, int ncol,
@@ -214,7 +224,9 @@ void launch_dgemm_small(int m, int n, int kk, const double* A, int lda, int ta, 
 void launch_ridge(const double* C, int k, const double* R, int ncol, double ridge_rel, double* Phi, double* lam_out,
                   double* work, int* flags, cudaStream_t s) {
   double* Lw = work;
-  ridge_factor_kernel<<<1, 1024, 0, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags);
+  const size_t sm = k <= 80 ? (size_t)2 * k * k * sizeof(double) : 0;
+  if (sm) cudaFuncSetAttribute(ridge_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  ridge_factor_kernel<<<1, 1024, sm, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags);
   check_launch("ridge_factor");
   ridge_solve_kernel<<<(ncol + 127) / 128, 128, 0, s>>>(Lw, k, R, ncol, Phi);
   check_launch("ridge_solve");

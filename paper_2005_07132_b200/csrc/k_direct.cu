@@ -29,6 +29,17 @@ __device__ __forceinline__ bool finite_elem(const TIn v) { return isfinite(v); }
 
 constexpr int kDirectThreads = 256;
 
+// fp64 reciprocal: MUFU seed + two Newton steps (~1 ulp; keeps the IEEE-division slow path off the
+// ALS recurrence's critical path)
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <typename TIn>
 __global__ void __launch_bounds__(kDirectThreads)
 direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
@@ -160,7 +171,7 @@ als_rows_kernel(const TY* __restrict__ y, int64_t n, int M, double lam, double p
             const double a1 = lam * d1;
             const double a2 = (t <= M - 3) ? lam : 0.0;
             const double D = a0 - L1m1 * L1m1 * Dm1 - L2m2 * L2m2 * Dm2;
-            const double rD = 1.0 / D;
+            const double rD = rcp64(D);
             const double l1n = (a1 - L2m1 * L1m1 * Dm1) * rD;
             const double l2n = a2 * rD;
             const double g = w * yv - L1m1 * gm1 - L2m2 * gm2;
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(32) als_rows_smem_kernel(const TY* __restrict_
           const double d1 = (t >= M - 1) ? 0.0 : ((t == 0 || t == M - 2) ? -2.0 : -4.0);
           const double a2 = (t <= M - 3) ? lam : 0.0;
           const double D = w + lam * d0 - L1m1 * L1m1 * Dm1 - L2m2 * L2m2 * Dm2;
-          const double rD = 1.0 / D;
+          const double rD = rcp64(D);
           const double l1n = (lam * d1 - L2m1 * L1m1 * Dm1) * rD;
           const double l2n = a2 * rD;
           const double g = w * yy - L1m1 * gm1 - L2m2 * gm2;

@@ -1,0 +1,293 @@
+// Projection US = A0 W (F5: US = A V_k = U_k S_k, with W = D_f V_k folding in the
+// f-scaling of Eq. 10; also the first GEMM of ML apply, Eq. 25) on the tensor cores, with the
+// per-tile column extremes that feed q (Eqs. 13-15; ties -> lowest pixel).
+// tcgen05.mma kind::tf32, 3xTF32; M = 128 pixels per tile, N = kp, K = channels in stages of 32.
+//   warps 0-3 : producers - A0 tile (128 px x 32 ch) fp32 loads one stage ahead in registers,
+//               tf32 hi/lo split, K-major smem (LBO 144 B pad: conflict-free 16-B stores)
+//   warps 4-7 : epilogue  - tcgen05.ld of the 128 x kp accumulator (TMEM lane = pixel), US row
+//               stores, per-column (max, argmax, min, argmin) by warp shuffles + smem
+//   warp 8    : TMEM alloc, W-stage bulk copies (cp.async.bulk, mbarrier tx), MMA issue
+// W^T is pre-staged (hi, lo) per K-stage in the exact K-major smem image by build_wimg.
+// Persistent CTAs walk pixel tiles.  Accuracy: the tensor-core accumulator truncates on each add
+// (DESIGN.md "Gram accuracy"), so hi*hi accumulates per 512-channel segment in its own TMEM
+// accumulator and the two cross terms in another; the epilogue adds them in fp32 (round to nearest).
+// Two accumulator sets alternate between tiles when they fit in the 512 TMEM columns.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "fkk_internal.h"
+#include "tc_common.cuh"
+
+namespace fkk {
+
+namespace {
+
+constexpr int PTM = 128;           // pixels per tile
+constexpr int PKC = 32;            // channels per stage
+constexpr int PA_LBO = 144, PA_SBO = (PKC / 4) * PA_LBO;     // 1152
+constexpr int PA_BYTES = (PTM / 8) * PA_SBO;                  // 18432 per hi / lo
+constexpr int PB_LBO = 128, PB_SBO = (PKC / 4) * PB_LBO;     // 1024
+constexpr int PTHREADS = 288;
+
+__host__ __device__ inline int pb_part(int kp) { return (kp / 8) * PB_SBO; }       // hi or lo
+__host__ __device__ inline int pb_stage(int kp) { return 2 * pb_part(kp); }
+__host__ __device__ inline int p_stage_bytes(int kp) { return 2 * PA_BYTES + pb_stage(kp); }
+__host__ __device__ inline int p_nstages(int kp) { return kp <= 64 ? 4 : 3; }
+constexpr int PSEG = 512;          // channels per hi*hi accumulator segment
+__host__ __device__ inline int p_nseg(int M) { return (M + PSEG - 1) / PSEG; }
+__host__ __device__ inline int p_set_cols(int M, int kp) { return (p_nseg(M) + 1) * kp; }
+__host__ __device__ inline int p_nbuf(int M, int kp) { return 2 * p_set_cols(M, kp) <= 512 ? 2 : 1; }
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(PTHREADS, 1)
+project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __restrict__ wimg, int kp,
+                  float* __restrict__ US, float* __restrict__ ext_val, int64_t* __restrict__ ext_idx, int k,
+                  int64_t row_offset, int want_ext) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int SB = p_stage_bytes(kp);
+  const int PSTAGES = p_nstages(kp);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PSTAGES * SB);
+  uint64_t* full = bars;                         // [PSTAGES] producers (128) + W tx
+  uint64_t* empty = bars + PSTAGES;              // [PSTAGES] MMA commit
+  uint64_t* acc_full = bars + 2 * PSTAGES;       // [2]
+  uint64_t* acc_empty = acc_full + 2;            // [2] epilogue (128)
+  float* red_v = reinterpret_cast<float*>(acc_empty + 2);      // [4 warps][2][128 cols]
+  int* red_i = reinterpret_cast<int*>(red_v + 4 * 2 * 128);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_i + 4 * 2 * 128);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (n + PTM - 1) / PTM;
+  const int nst = (M + PKC - 1) / PKC;           // K stages per tile
+  if (tid == 0) {
+    for (int s = 0; s < PSTAGES; ++s) { tc::mbar_init(&full[s], 129); tc::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 128); }
+    tc::fence_mbar_init();
+  }
+  const int nseg = p_nseg(M), setc = p_set_cols(M, kp), nbuf = p_nbuf(M, kp);
+  if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    // item (pixel p, channel quad c4): p = idx >> 3, c4 = idx & 7; 8 items per thread per stage
+    float4 x[8];
+    int stage = 0;
+    uint32_t phase = 0;
+    auto load = [&](int64_t t, int st) {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int idx = tid + 128 * h;
+        const int p = idx >> 3, c4 = idx & 7;
+        const int64_t pp = t * PTM + p;
+        const int col = st * PKC + 4 * c4;
+        x[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (pp < n && col < M) x[h] = __ldg(reinterpret_cast<const float4*>(A + pp * (int64_t)M + col));
+      }
+    };
+    int64_t t = blockIdx.x;
+    int st = 0;
+    if (t < ntiles) load(t, 0);
+    while (t < ntiles) {
+      tc::mbar_wait(&empty[stage], phase ^ 1);
+      unsigned char* sa = smem + stage * SB;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int idx = tid + 128 * h;
+        const int p = idx >> 3, c4 = idx & 7;
+        float4 hi, lo;
+        tc::split4(x[h], hi, lo);
+        const int off = (p >> 3) * PA_SBO + c4 * PA_LBO + (p & 7) * 16;
+        *reinterpret_cast<float4*>(sa + off) = hi;
+        *reinterpret_cast<float4*>(sa + PA_BYTES + off) = lo;
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full[stage]);
+      if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+      if (++st == nst) { st = 0; t += gridDim.x; }
+      if (t < ntiles) load(t, st);
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    uint32_t ph[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = (int)(it % nbuf);
+      tc::mbar_wait(&acc_full[b], ph[b]);
+      ph[b] ^= 1;
+      tc::tc_fence_after();
+      const int row = ew * 32 + lane;
+      const int64_t p = t * PTM + row;
+      const bool valid = p < n;
+      const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * setc);
+      for (int c0 = 0; c0 < kp; c0 += 16) {
+        float v[16], w[16];
+        tc::tmem_ld16(tb + nseg * kp + c0, v);                 // cross terms
+        for (int sg = 0; sg < nseg; ++sg) {                     // + hi*hi segments (fp32 RN)
+          tc::tmem_ld16(tb + sg * kp + c0, w);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] += w[q];
+        }
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(US + p * kp + c0 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+        if (want_ext) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float vmax = valid ? v[q] : -INFINITY, vmin = valid ? v[q] : INFINITY;
+            int imax = valid ? row : 0x7fffffff, imin = imax;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, vmax, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
+              if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
+              const float nv = __shfl_xor_sync(0xffffffffu, vmin, o);
+              const int ni = __shfl_xor_sync(0xffffffffu, imin, o);
+              if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
+            }
+            if (lane == 0) {
+              red_v[(ew * 2 + 0) * 128 + c0 + q] = vmax;
+              red_i[(ew * 2 + 0) * 128 + c0 + q] = imax;
+              red_v[(ew * 2 + 1) * 128 + c0 + q] = vmin;
+              red_i[(ew * 2 + 1) * 128 + c0 + q] = imin;
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acc_empty[b]);
+      if (want_ext) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = ew * 32 + lane; c < k; c += 128) {
+          float vM = -INFINITY, vm = INFINITY;
+          int iM = 0x7fffffff, im = 0x7fffffff;
+          for (int w2 = 0; w2 < 4; ++w2) {   // ascending pixel groups: strict compare keeps the lowest row
+            const float a = red_v[(w2 * 2) * 128 + c], bmn = red_v[(w2 * 2 + 1) * 128 + c];
+            const int ia = red_i[(w2 * 2) * 128 + c], ib = red_i[(w2 * 2 + 1) * 128 + c];
+            if (a > vM || (a == vM && ia < iM)) { vM = a; iM = ia; }
+            if (bmn < vm || (bmn == vm && ib < im)) { vm = bmn; im = ib; }
+          }
+          const int64_t o = (t * (int64_t)k + c) * 2;
+          ext_val[o] = vM;
+          ext_idx[o] = iM == 0x7fffffff ? INT64_MAX : row_offset + t * PTM + iM;
+          ext_val[o + 1] = vm;
+          ext_idx[o + 1] = im == 0x7fffffff ? INT64_MAX : row_offset + t * PTM + im;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  } else if (warp == 8 && lane == 0) {
+    // ------------------------------------------------------------ W stages + MMA issue
+    const uint32_t idesc = tc::make_idesc_tf32(PTM, kp, false, false);
+    const uint32_t sbase = tc::smem_u32(smem);
+    const int WB = pb_stage(kp), WP = pb_part(kp);
+    int stage = 0;
+    uint32_t phase = 0, ae[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = (int)(it % nbuf);
+      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], ae[b]); ae[b] ^= 1; tc::tc_fence_after(); }
+      const uint32_t dset = tmem + (uint32_t)(b * setc);
+      const uint32_t dx = dset + nseg * kp;
+      for (int st = 0; st < nst; ++st) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);          // slot free (also for the W copy)
+        const uint32_t sa = sbase + stage * SB;
+        bulk_g2s(sa + 2 * PA_BYTES, reinterpret_cast<const unsigned char*>(wimg) + (size_t)st * WB, WB, &full[stage]);
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t ahi = sa, alo = sa + PA_BYTES, bhi = sa + 2 * PA_BYTES, blo = bhi + WP;
+#pragma unroll
+        for (int ks = 0; ks < PKC / 8; ++ks) {
+          const uint64_t dah = tc::make_sdesc(ahi + ks * 2 * PA_LBO, PA_LBO, PA_SBO);
+          const uint64_t dal = tc::make_sdesc(alo + ks * 2 * PA_LBO, PA_LBO, PA_SBO);
+          const uint64_t dbh = tc::make_sdesc(bhi + ks * 2 * PB_LBO, PB_LBO, PB_SBO);
+          const uint64_t dbl = tc::make_sdesc(blo + ks * 2 * PB_LBO, PB_LBO, PB_SBO);
+          const int sg = (st * PKC) / PSEG;
+          const uint32_t dh = dset + sg * kp;
+          const uint32_t accx = (st > 0 || ks > 0) ? 1u : 0u;
+          const uint32_t acch = ((st * PKC) % PSEG != 0 || ks > 0) ? 1u : 0u;
+          tc::mma_tf32(dx, dal, dbh, idesc, accx);
+          tc::mma_tf32(dx, dah, dbl, idesc, 1u);
+          tc::mma_tf32(dh, dah, dbh, idesc, acch);
+        }
+        tc::mma_commit(&empty[stage]);
+        if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
+      }
+      tc::mma_commit(&acc_full[b]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 8) tc::tmem_dealloc(tmem, 512);
+}
+
+// W^T image per K-stage st: rows n (rank, < kp), K = channel j in the stage, K-major hi/lo.
+__global__ void build_wimg_kernel(const double* __restrict__ V, const double* __restrict__ fscale,
+                                  const double* __restrict__ cscale, int M, int k, int kp, float* __restrict__ wimg) {
+  const int nst = (M + PKC - 1) / PKC;
+  const int64_t total = (int64_t)nst * kp * PKC;
+  const int WB = pb_stage(kp), WP = pb_part(kp);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int jj = (int)(e % PKC);
+    const int nrow = (int)((e / PKC) % kp);
+    const int st = (int)(e / ((int64_t)PKC * kp));
+    const int j = st * PKC + jj;
+    double v = 0.0;
+    if (j < M && nrow < k) {
+      v = V[(int64_t)nrow * M + j];
+      if (fscale) v *= fscale[j];
+      if (cscale) v *= cscale[nrow];
+    }
+    float hi, lo;
+    tc::split_tf32((float)v, hi, lo);
+    const int64_t off = (int64_t)st * WB + (nrow >> 3) * PB_SBO + (jj >> 2) * PB_LBO + (nrow & 7) * 16 + (jj & 3) * 4;
+    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(wimg) + off) = hi;
+    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(wimg) + off + WP) = lo;
+  }
+}
+
+size_t pt_smem(int kp) { return (size_t)p_nstages(kp) * p_stage_bytes(kp) + 2 * 4 * 8 + 4 * 8 + 4 * 2 * 128 * 8 + 64; }
+
+}  // namespace
+
+size_t project_tc_wimg_floats(int M, int kp) { return (size_t)((M + PKC - 1) / PKC) * pb_stage(kp) / 4; }
+
+int project_tc_num_blocks(int64_t n) { return (int)((n + PTM - 1) / PTM); }
+
+void launch_build_wimg(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* wimg,
+                       cudaStream_t s) {
+  build_wimg_kernel<<<256, 256, 0, s>>>(V, fscale, cscale, M, k, kp, wimg);
+  check_launch("build_wimg");
+}
+
+void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int k, int kp, float* US, float* ext_val,
+                       int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s) {
+  if (n <= 0) return;
+  const size_t smem = pt_smem(kp);
+  if (smem > 227 * 1024 || kp > 128 || kp % 16 || p_set_cols(M, kp) > 512)
+    throw Status(10, "project_tc: unsupported rank padding / channel count");
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (n + PTM - 1) / PTM;
+  const int grid = (int)std::min<int64_t>(ntiles, sms);
+  project_tc_kernel<<<grid, PTHREADS, smem, s>>>(A, n, M, wimg, kp, US, ext_val, ext_idx, k, row_offset, want_ext);
+  check_launch("project_tc");
+}
+
+}  // namespace fkk
