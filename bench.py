@@ -30,6 +30,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one gram_tc launch (profiles/)
+GRAM_TRAFFIC = {"cfg3": 6.09e9}
+
 METRIC = "spectra/s for full fKK-EC (and direct KK) at 1/2/4/8 B200; % HBM/TC roofline"
 
 
@@ -160,16 +163,31 @@ def run_ours(args) -> dict:
     stage_ms = {kk: v / args.steps for kk, v in stage_acc.items()}
     value = N / (t / 1e3)
 
-    # roofline of the dominant GPU kernel (the Gram): algorithmic flops N*M^2 (syrk)
+    # roofline of the Gram (F2, tcgen05 3xTF32): algorithmic flops N*M^2 (the syrk: M(M+1)/2 unique
+    # products x 2 flops, rounded to M^2) per pass; 3xTF32 issues three TF32 products per fp32-equivalent
+    # product, so its fp32-equivalent peak is the TF32 peak / 3
     peaks, src = _peaks()
     gram_ms = stage_ms.get("gram", float("nan"))
     gram_flops = float(n_loc) * M * M
-    sm_max = peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12     # TFLOP/s, CUDA-core FP32
+    tf32_peak = peaks["bf16_tflops"] * (1.1 / 2.25)            # guide's nominal TF32/BF16 ratio
+    peak_3x = tf32_peak / 3.0
     achieved = gram_flops / (gram_ms / 1e3) / 1e12
-    roofline = {"kernel": "gram (F2, fp32 CUDA-core SIMT)", "bound": "alu", "achieved": achieved,
-                "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
-                "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
+    roofline = {"kernel": "gram_tc (F2, tcgen05 kind::tf32, 3xTF32 split)", "bound": "tensor", "achieved": achieved,
+                "peak": peak_3x, "unit": "TFLOP/s", "frac": achieved / peak_3x,
+                "traffic": GRAM_TRAFFIC.get(args.workload),
+                "peak_source": f"{src} bf16 {peaks['bf16_tflops']:.0f} TF/s x 1.1/2.25 (TF32) / 3 (3xTF32 products); "
+                               f"algorithmic flops = N*M^2 per pass; timed with CUDA events on the plan stream "
+                               f"(gram_tc + its fp64 split reduction)"}
+    # per-kernel-class rooflines of the other hot kernels (same event timing)
+    hbm = peaks["hbm_gbs"]
+    other = {}
+    for name, nbytes in (("logratio", 8.0 * n_loc * M), ("project", 4.0 * n_loc * M + 4.0 * n_loc * k),
+                         ("reconstruct", 8.0 * n_loc * M + 4.0 * n_loc * k)):
+        ms = stage_ms.get(name)
+        if ms:
+            gbs = nbytes / (ms / 1e3) / 1e9
+            other[name] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm}
+    roofline["others"] = other
 
     # ---------------- direct KK (same image) ----------------
     plan.direct(I, Iref, out)

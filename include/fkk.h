@@ -177,6 +177,16 @@ int64_t fkk_last_launch_count(fkk_plan_t p);
  * Synchronises the device. */
 fkk_status fkk_debug_tc_mma(int32_t mode, const float* d_A, const float* d_B, float* d_D, int32_t N);
 
+/* Test hook (F4, PAPER.md:64, :70 -- the truncated SVD through the Gram eigenproblem): the GPU
+ * eigensolver that fkk_svd/fkk_transform run, on a caller-supplied symmetric M x M fp64 matrix d_G
+ * (device, row-major, both triangles; not modified).  d_V: k x M (vector j contiguous, device),
+ * d_lam: k descending (device).  Sign rule as fkk_svd.  M >= 3, 1 <= k <= M, else INVALID_ARG;
+ * dependent inverse-iteration vectors -> NUMERICAL.  Allocates its own workspace; synchronises. */
+fkk_status fkk_debug_eig_topk(const double* d_G, int32_t M, int32_t k, double* d_V, double* d_lam);
+/* 1 if the eigensolver keeps the working matrix resident in shared memory for this M (the
+ * row-resident tridiagonalisation), 0 if it streams it through L2. */
+int32_t fkk_debug_eig_path(int32_t M);
+
 /* ---------------- host-only helpers (no GPU needed; exercised by the CPU tests) ---------------- */
 /* Top-k eigenpairs of a symmetric M x M fp64 matrix (row-major; only the lower triangle is read):
  * Householder tridiagonalisation, Sturm bisection, inverse iteration, back-transformation.

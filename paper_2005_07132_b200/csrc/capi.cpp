@@ -217,6 +217,7 @@ struct fkk_plan {
       if (f & 1) throw Status(FKK_ERR_BAD_REFERENCE, "reference spectrum has a non-positive or non-finite value");
       if (f & 2) throw Status(FKK_ERR_NONFINITE_INPUT, "non-finite value in the input cube");
       if (f & 4) throw Status(FKK_ERR_NUMERICAL, "ridge system not positive definite (increase ridge_rel)");
+      if (f & 8) throw Status(FKK_ERR_NUMERICAL, "eigensolver: inverse-iteration vectors are linearly dependent");
     }
   }
 
@@ -414,7 +415,7 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   if (p->d.f_mode == FKK_F_EQ9) fkk::launch_scale_gram(p->G, p->f64, M, s);
   p->mark("gram");
   // eig on the GPU (fp64): Householder tridiagonalisation, bisection, inverse iteration
-  fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, s);
+  fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, p->flags, s);
   std::vector<double> hl(k);
   FKK_CUDA_CHECK(cudaMemcpyAsync(hl.data(), p->lam_d, k * sizeof(double), cudaMemcpyDeviceToHost, s));
   p->check_flags_sync();
@@ -967,6 +968,31 @@ fkk_status fkk_debug_tc_mma(int32_t mode, const float* d_A, const float* d_B, fl
     return (fkk_status)e.code;
   }
 }
+
+fkk_status fkk_debug_eig_topk(const double* d_G, int32_t M, int32_t k, double* d_V, double* d_lam) {
+  if (!d_G || !d_V || !d_lam || M < 3 || k < 1 || k > M) return FKK_ERR_INVALID_ARG;
+  double* work = nullptr;
+  int* flags = nullptr;
+  try {
+    work = dalloc<double>(fkk::eig_workspace_doubles(M, k));
+    flags = dalloc<int>(1);
+    FKK_CUDA_CHECK(cudaMemset(flags, 0, sizeof(int)));
+    fkk::launch_eig_topk(d_G, M, k, work, d_V, d_lam, flags, nullptr);
+    FKK_CUDA_CHECK(cudaDeviceSynchronize());
+    int hf = 0;
+    FKK_CUDA_CHECK(cudaMemcpy(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(work);
+    cudaFree(flags);
+    return hf ? FKK_ERR_NUMERICAL : FKK_OK;
+  } catch (const Status& e) {
+    g_create_err = e.what();
+    cudaFree(work);
+    cudaFree(flags);
+    return (fkk_status)e.code;
+  }
+}
+
+int32_t fkk_debug_eig_path(int32_t M) { return fkk::eig_path_rows_resident(M); }
 
 fkk_status fkk_host_eig_topk(const double* G, int32_t M, int32_t k, double* V, double* lam) {
   if (!G || !V || !lam || M < 1 || k < 1 || k > M) return FKK_ERR_INVALID_ARG;

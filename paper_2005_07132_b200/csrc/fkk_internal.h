@@ -115,7 +115,10 @@ void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vse
 // ---- GPU eigensolver (k_eig.cu): top-k eigenpairs of the symmetric M x M fp64 G (device);
 // V: k vectors of length M (= M x k column-major), lam_out: k descending.
 size_t eig_workspace_doubles(int M, int k);
-void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, cudaStream_t s);
+// M >= 3; flags |= 8 if the re-orthogonalisation finds dependent vectors.  G is not modified.
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
+                     cudaStream_t s);
+int eig_path_rows_resident(int M);   // 1: the row-resident (shared-memory) tridiagonalisation is used
 
 void launch_tc_selftest(int mode, const float* A, const float* B, float* D, int N, cudaStream_t s);
 

@@ -160,6 +160,172 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Row-resident variant (default when the owned rows fit in shared memory): CTA c of the cooperative
+// grid keeps rows r = c, c + P, c + 2P, ... of the working matrix in its shared memory for the whole
+// tridiagonalisation, so the per-column pass touches no L2.  Per column j, with (v_{j-1}, w_{j-1})
+// the pending rank-2 update:
+//   after the barrier of column j-1: read p_{j-1} (m values) and the published row j (state
+//     A^(j-1)) in ONE batch of L2 loads; form w_{j-1} = p - (t/2)(p.v) v; x = row j of A^(j);
+//     reflector v_j, t_j (every CTA redundantly);
+//   pass: every owned row r > j gets the pending update (eagerly, in smem) and p_r = t_j A^(j)[r,:] v_j;
+//     the owner of row j+1 publishes it (state A^(j)) for the next column;
+//   one grid barrier.
+// One barrier and one L2 round trip per column (the L2-streaming kernel above needs ~3 round trips).
+constexpr int kTsThreads = 512;
+constexpr int kTsSeg = 2;     // each owned row is split over 2 warps (partial dots summed by readers)
+
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while ((int)(v - target) < 0);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const double* __restrict__ G, double* __restrict__ Wk,
+                                                                   int M, double* __restrict__ d, double* __restrict__ e,
+                                                                   double* __restrict__ tau, double* __restrict__ Pg,
+                                                                   unsigned int* __restrict__ ctr) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = gridDim.x, cta = blockIdx.x;
+  const int R = (M - cta + P - 1) / P;            // owned rows: r = cta + i P, i < R
+  double* rows = sm;                               // R x M
+  double* vbuf0 = rows + (size_t)R * M;            // v_j / v_{j-1} ping-pong (absolute index)
+  double* vbuf1 = vbuf0 + M;
+  double* wp = vbuf1 + M;                          // w_{j-1}
+  double* x = wp + M;                              // row j of A^(j)
+  double* red = x + M;                             // 32
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int i = 0; i < R; ++i) {
+    const double* g = G + (int64_t)(cta + i * P) * M;
+    for (int c = tid; c < M; c += nt) rows[(size_t)i * M + c] = g[c];
+  }
+  unsigned int target = 0;
+  double tprev = 0.0;
+  double* v = vbuf0;
+  double* vp = vbuf1;
+  for (int j = 0; j + 2 < M; ++j) {
+    // ---- x = row j of A^(j)
+    if (j == 0) {
+      for (int c = tid; c < M; c += nt) x[c] = G[c];
+      __syncthreads();
+    } else {
+      double s = 0.0;
+      const double* pub = Wk + (int64_t)j * M;
+      for (int c = j + tid; c < M; c += nt) {
+        double pv = 0.0;
+#pragma unroll
+        for (int sg = 0; sg < kTsSeg; ++sg) pv += __ldcg(Pg + (int64_t)sg * M + c);
+        wp[c] = pv;
+        x[c] = __ldcg(pub + c);
+        s += pv * vp[c];
+      }
+      const double K = 0.5 * tprev * block_sum_d(s, red);
+      for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
+      __syncthreads();
+      const double vj = vp[j], wj = wp[j];
+      for (int c = j + tid; c < M; c += nt) x[c] -= vj * wp[c] + wj * vp[c];
+      // reflector v_{j-1} -> dead row j-1 (every CTA has read that row before the last barrier)
+      if (cta == 0) {
+        double* rj = Wk + (int64_t)(j - 1) * M;
+        for (int c = j + tid; c < M; c += nt) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+      }
+      __syncthreads();
+    }
+    // ---- Householder reflector of x[j+1..M-1]
+    double s2 = 0.0;
+    for (int c = j + 1 + tid; c < M; c += nt) s2 += x[c] * x[c];
+    const double nrm2 = block_sum_d(s2, red);
+    const double x0 = x[j + 1];
+    const double nrm = sqrt(nrm2);
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    const double v0 = x0 - alpha;
+    const double vtv = nrm2 - x0 * x0 + v0 * v0;
+    const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
+    for (int c = j + 1 + tid; c < M; c += nt) v[c] = c == j + 1 ? v0 : x[c];
+    if (cta == 0 && tid == 0) {
+      d[j] = x[j];
+      e[j] = t == 0.0 ? x0 : alpha;
+      tau[j] = t;
+    }
+    __syncthreads();
+    // ---- pass over the owned rows r > j: pending update (eager, smem), p_r = t A^(j)[r,:] v_j
+    const bool pending = j > 0;
+    const int m0 = j + 1, m = M - m0;
+    const int seglen = (m + kTsSeg - 1) / kTsSeg;
+    const bool last = j + 3 == M;
+    for (int task = warp; task < R * kTsSeg; task += nw) {
+      const int i = task / kTsSeg, sg = task - i * kTsSeg;
+      const int r = cta + i * P;
+      if (r <= j) continue;
+      double* row = rows + (size_t)i * M;
+      const int c0 = m0 + sg * seglen, c1 = min(M, c0 + seglen);
+      const bool publish = r == j + 1 || (last && r == M - 1);
+      double* pub = Wk + (int64_t)r * M;
+      double acc = 0.0;
+      if (pending) {
+        const double vr = vp[r], wr = wp[r];
+#pragma unroll 4
+        for (int c = c0 + lane; c < c1; c += 32) {
+          const double a = row[c] - (vr * wp[c] + wr * vp[c]);
+          row[c] = a;
+          if (publish) pub[c] = a;
+          acc = fma(a, v[c], acc);
+        }
+      } else {
+#pragma unroll 4
+        for (int c = c0 + lane; c < c1; c += 32) {
+          const double a = row[c];
+          if (publish) pub[c] = a;
+          acc = fma(a, v[c], acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) Pg[(int64_t)sg * M + r] = t * acc;
+    }
+    grid_barrier(ctr, target);
+    tprev = t;
+    double* tmp = vp; vp = v; v = tmp;
+  }
+  // ---- flush: w_{M-3}, the trailing 2 x 2 block, reflector v_{M-3}
+  if (cta == 0 && M >= 3) {
+    const int j = M - 2;
+    double s = 0.0;
+    for (int c = j + tid; c < M; c += nt) {
+      double pv = 0.0;
+      for (int sg = 0; sg < kTsSeg; ++sg) pv += __ldcg(Pg + (int64_t)sg * M + c);
+      wp[c] = pv;
+      s += pv * vp[c];
+    }
+    const double K = 0.5 * tprev * block_sum_d(s, red);
+    for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
+    __syncthreads();
+    double* rj = Wk + (int64_t)(j - 1) * M;
+    for (int c = j + tid; c < M; c += nt) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+    if (tid == 0) {
+      const double* r0 = Wk + (int64_t)(M - 2) * M;
+      const double* r1 = Wk + (int64_t)(M - 1) * M;
+      d[M - 2] = __ldcg(r0 + M - 2) - 2.0 * vp[M - 2] * wp[M - 2];
+      e[M - 2] = __ldcg(r1 + M - 2) - (vp[M - 1] * wp[M - 2] + wp[M - 1] * vp[M - 2]);
+      d[M - 1] = __ldcg(r1 + M - 1) - 2.0 * vp[M - 1] * wp[M - 1];
+    }
+  }
+}
+
+size_t tridiag_rows_smem(int M, int P) {
+  const int R = (M + P - 1) / P;
+  return ((size_t)R * M + 4 * (size_t)M + 32) * sizeof(double);
+}
+
 // 1/q via the MUFU seed + two Newton steps (full fp64 accuracy for normal q; a Sturm count only
 // needs the sign of each q to be right away from the eigenvalues)
 __device__ __forceinline__ double fast_rcp(double q) {
@@ -393,79 +559,245 @@ __global__ void __launch_bounds__(kEigThreads) backxform_kernel(const double* __
   if (tid == 0) lam_out[jj] = lam[jj];
 }
 
+
+// Back-transformation, reflector-sharing variant: a CTA of nw warps holds nw eigenvectors (one per
+// warp, in shared memory); the reflectors v_j (row j of Wk, columns j+1..M-1) stream through a
+// double-buffered shared-memory stage with cp.async, so each v_j is read from L2 once per CTA and
+// its load overlaps the previous reflector's dot/axpy.  u = H_0 ... H_{M-3} z, then the sign rule.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(256) backxform_shared_kernel(const double* __restrict__ Wk,
+                                                               const double* __restrict__ tau, int M, int k,
+                                                               const double* __restrict__ Z,
+                                                               const double* __restrict__ lam,
+                                                               double* __restrict__ V, double* __restrict__ lam_out) {
+  extern __shared__ __align__(16) double shx[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  double* stage = shx;                 // 2 x M
+  double* z = shx + 2 * (size_t)M + (size_t)warp * M;
+  const int jj = blockIdx.x * nw + warp;
+  const bool active = jj < k;
+  if (active)
+    for (int i = lane; i < M; i += 32) z[i] = Z[(int64_t)jj * M + i];
+  auto issue = [&](int j, int buf) {
+    if (j >= 0)
+      for (int c = j + 1 + tid; c < M; c += blockDim.x) cp_async8(stage + (size_t)buf * M + c, Wk + (int64_t)j * M + c);
+    cp_async_commit();
+  };
+  int buf = 0;
+  issue(M - 3, 0);
+  for (int j = M - 3; j >= 0; --j) {
+    issue(j - 1, buf ^ 1);
+    cp_async_wait1();
+    __syncthreads();
+    const double t = tau[j];
+    if (active && t != 0.0) {
+      const double* vj = stage + (size_t)buf * M;
+      double acc = 0.0;
+      for (int c = j + 1 + lane; c < M; c += 32) acc = fma(vj[c], z[c], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const double f = t * acc;
+      for (int c = j + 1 + lane; c < M; c += 32) z[c] -= f * vj[c];
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  if (!active) return;
+  __syncwarp();
+  // sign rule: entry of largest |.| positive, ties -> lowest index
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = lane; i < M; i += 32) {
+    const double a = fabs(z[i]);
+    if (a > best) { best = a; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  const double sg = z[bi] < 0.0 ? -1.0 : 1.0;
+  for (int i = lane; i < M; i += 32) V[(int64_t)jj * M + i] = sg * z[i];
+  if (lane == 0) lam_out[jj] = lam[jj];
+}
+
+// Re-orthogonalisation by CholeskyQR, applied twice (CholQR2): S = Z Z^T (k x k), S = R^T R,
+// Z <- R^{-T} Z.  In exact arithmetic this is classical Gram-Schmidt of the vectors in their
+// (descending-eigenvalue) order -- the same result as reorth_kernel -- but parallel over M.
+__global__ void gram_rows_kernel(const double* __restrict__ Z, int M, int k, double* __restrict__ S) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int npairs = k * (k + 1) / 2;
+  if (w >= npairs) return;
+  int a = 0, rem = w;
+  while (rem >= k - a) { rem -= k - a; ++a; }
+  const int b = a + rem;
+  const double* za = Z + (int64_t)a * M;
+  const double* zb = Z + (int64_t)b * M;
+  double acc = 0.0;
+  for (int i = lane; i < M; i += 32) acc = fma(za[i], zb[i], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) { S[a * k + b] = acc; S[b * k + a] = acc; }
+}
+
+// one CTA: Cholesky S = R^T R (R upper, row-major), then T = R^{-1} (upper) into Tout
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ S, int k, double* __restrict__ Tout,
+                                                       int* __restrict__ flags) {
+  extern __shared__ __align__(16) double sc[];
+  double* Rm = sc;          // k x k
+  double* Tm = sc + k * k;  // k x k
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < k * k; i += nt) { Rm[i] = S[i]; Tm[i] = 0.0; }
+  __syncthreads();
+  // right-looking Cholesky on the upper triangle: R[c][c] = sqrt(S[c][c]), R[c][j] /= R[c][c], trailing update
+  for (int c = 0; c < k; ++c) {
+    const double dcc = Rm[c * k + c];
+    const double rcc = dcc > 0.0 ? sqrt(dcc) : 0.0;
+    __syncthreads();
+    if (tid == 0 && !(dcc > 0.0)) atomicOr(flags, 8);
+    for (int j = c + 1 + tid; j < k; j += nt) Rm[c * k + j] = rcc > 0.0 ? Rm[c * k + j] / rcc : 0.0;
+    __syncthreads();
+    if (tid == 0) Rm[c * k + c] = rcc;
+    for (int e2 = tid; e2 < (k - c - 1) * (k - c - 1); e2 += nt) {
+      const int i = c + 1 + e2 / (k - c - 1), j = c + 1 + e2 % (k - c - 1);
+      if (j >= i) Rm[i * k + j] -= Rm[c * k + i] * Rm[c * k + j];
+    }
+    __syncthreads();
+  }
+  // T = R^{-1}: column j of T solves R t = e_j (back substitution), thread per column
+  for (int j = tid; j < k; j += nt) {
+    for (int i = j; i >= 0; --i) {
+      double sacc = i == j ? 1.0 : 0.0;
+      for (int l = i + 1; l <= j; ++l) sacc -= Rm[i * k + l] * Tm[l * k + j];
+      Tm[i * k + j] = Rm[i * k + i] > 0.0 ? sacc / Rm[i * k + i] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < k * k; i += nt) Tout[i] = Tm[i];
+}
+
+// Znew[c][i] = sum_{b <= c} Z[b][i] T[b][c]   (Q = Z_mat R^{-1}, Z_mat = M x k with columns z_b)
+__global__ void apply_rinv_kernel(const double* __restrict__ Z, int M, int k, const double* __restrict__ T,
+                                  double* __restrict__ Zn) {
+  const int64_t total = (int64_t)M * k;
+  for (int64_t e2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e2 < total; e2 += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e2 / M), i = (int)(e2 % M);
+    double acc = 0.0;
+    for (int b = 0; b <= c; ++b) acc = fma(Z[(int64_t)b * M + i], __ldg(T + b * k + c), acc);
+    Zn[e2] = acc;
+  }
+}
+
 }  // namespace
 
 size_t eig_workspace_doubles(int M, int k) {
-  // A copy (M*M) + d, e, tau, p (4M) + lam, tnorm (k+1) + Z (k*M) + inviter scratch (4kM + kM/8 + 1)
-  return (size_t)M * M + 3 * (size_t)M + 16 * (size_t)M + (size_t)k + 1 + (size_t)k * M + 16;
+  // d, e, tau (3M) + p (16M) + lam, tnorm (k+1) + Z, Z2 (2kM) + S, T (2k^2) + counter + A copy (M*M)
+  return 19 * (size_t)M + (size_t)k + 1 + 2 * (size_t)k * M + 2 * (size_t)k * k + 16 + (size_t)M * M;
 }
 
-void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, cudaStream_t s) {
-  double* A = work;
-  double* d = A + (size_t)M * M;
+int eig_path_rows_resident(int M) {
+  int dev = 0, sms = 148, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return M >= 3 && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
+}
+
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
+                     cudaStream_t s) {
+  double* d = work;
   double* e = d + M;
   double* tau = e + M;
   double* pg = tau + M;
   double* lam = pg + 16 * (size_t)M;
   double* tnorm = lam + k;
   double* Z = tnorm + 1;
-  FKK_CUDA_CHECK(cudaMemcpyAsync(A, G, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  // tridiagonalisation: one thread-block cluster (16 CTAs, cluster barriers) when available,
-  // else a cooperative grid with grid barriers
-  const size_t smem = (3 * (size_t)M + 32) * sizeof(double);
-  int Mi = M;
-  static int cluster_ok = 0;   // measured: 16-CTA cluster 15.4 ms vs cooperative grid 9.3 ms (M=1000)
-  if (cluster_ok != 0) {
-    auto kc = tridiag_kernel<true>;
-    cudaError_t e1 = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaError_t e2 = cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(16);
-    cfg.blockDim = dim3(kTriThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 16;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int ncl = 0;
-    if (e1 == cudaSuccess && e2 == cudaSuccess && cudaOccupancyMaxActiveClusters(&ncl, kc, &cfg) == cudaSuccess && ncl >= 1) {
-      FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kc, A, Mi, d, e, tau, pg));
-      count_launch();
-      cluster_ok = 1;
-    } else {
-      cudaGetLastError();
-      cluster_ok = 0;
-    }
-  }
-  if (cluster_ok == 0) {
+  double* Z2 = Z + (size_t)k * M;
+  double* S = Z2 + (size_t)k * M;
+  double* T = S + (size_t)k * k;
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(T + (size_t)k * k);
+  double* A = T + (size_t)k * k + 16;      // working matrix / published rows / reflectors (M x M)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (eig_path_rows_resident(M)) {
+    // row-resident cooperative tridiagonalisation (G is read, never copied)
+    const size_t smem = tridiag_rows_smem(M, sms);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(tridiag_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_rows_kernel, kTsThreads, smem));
+    if (per < 1) throw Status(10, "tridiag_rows kernel cannot be co-resident");
+    FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+    int Mi = M;
+    const double* Gc = G;
+    void* args[] = {&Gc, &A, &Mi, &d, &e, &tau, &pg, &ctr};
+    FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_rows_kernel, dim3(sms), dim3(kTsThreads), args, smem, s));
+    count_launch();
+  } else {
+    FKK_CUDA_CHECK(cudaMemcpyAsync(A, G, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    // L2-streaming cooperative tridiagonalisation (large M)
+    const size_t smem = (3 * (size_t)M + 32) * sizeof(double);
+    int Mi = M;
     auto kg = tridiag_kernel<false>;
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 1;
     FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kg, kTriThreads, smem));
     if (per < 1) throw Status(10, "tridiag kernel cannot be co-resident");
     void* args[] = {&A, &Mi, &d, &e, &tau, &pg};
     FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)kg, dim3(sms), dim3(kTriThreads), args, smem, s));
     count_launch();
   }
-  if (M == 1) return;
   bisect_kernel<<<(k * 32 + 127) / 128, 128, 0, s>>>(d, e, M, k, lam, tnorm);
   check_launch("eig_bisect");
   const size_t ism = (size_t)5 * M * sizeof(double) + (size_t)M + 16;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
   inviter_kernel<<<k, 32, ism, s>>>(d, e, M, k, lam, tnorm, Z);
   check_launch("eig_inviter");
-  reorth_kernel<<<1, 1024, 0, s>>>(Z, M, k);
-  check_launch("eig_reorth");
-  const size_t bsm = (size_t)M * sizeof(double);
-  FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-  backxform_kernel<<<k, kEigThreads, bsm, s>>>(A, tau, M, Z, lam, V, lam_out);
-  check_launch("eig_backxform");
+  // CholQR2 re-orthogonalisation (k <= 128: the k x k factor lives in one CTA's shared memory)
+  if (k <= 128) {
+    const size_t csm = 2 * (size_t)k * k * sizeof(double);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    const int npairs = k * (k + 1) / 2;
+    const int agrid = (int)std::min<int64_t>(((int64_t)M * k + 255) / 256, 4 * sms);
+    for (int pass = 0; pass < 2; ++pass) {
+      const double* zin = pass == 0 ? Z : Z2;
+      double* zout = pass == 0 ? Z2 : Z;
+      gram_rows_kernel<<<(npairs * 32 + 255) / 256, 256, 0, s>>>(zin, M, k, S);
+      check_launch("eig_reorth_gram");
+      chol_inv_kernel<<<1, 256, csm, s>>>(S, k, T, flags);
+      check_launch("eig_reorth_chol");
+      apply_rinv_kernel<<<agrid, 256, 0, s>>>(zin, M, k, T, zout);
+      check_launch("eig_reorth_apply");
+    }
+  } else {
+    reorth_kernel<<<1, 1024, 0, s>>>(Z, M, k);
+    check_launch("eig_reorth");
+  }
+  // back-transformation: reflector-sharing CTAs when (2 + nw) M doubles fit in shared memory
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int nw = 8;
+  while (nw > 1 && (size_t)(2 + nw) * M * sizeof(double) > (size_t)maxsm) --nw;
+  const size_t bsm = (size_t)(2 + nw) * M * sizeof(double);
+  if (M >= 3 && bsm <= (size_t)maxsm) {
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+    backxform_shared_kernel<<<(k + nw - 1) / nw, nw * 32, bsm, s>>>(A, tau, M, k, Z, lam, V, lam_out);
+    check_launch("eig_backxform");
+  } else {
+    const size_t bsm1 = (size_t)M * sizeof(double);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm1));
+    backxform_kernel<<<k, kEigThreads, bsm1, s>>>(A, tau, M, Z, lam, V, lam_out);
+    check_launch("eig_backxform");
+  }
 }
 
 }  // namespace fkk

@@ -78,6 +78,8 @@ _SIGS = {
     "fkk_last_launch_count": (_i64, [_vp]),
     "fkk_host_eig_topk": (_i32, [_dp, _i32, _i32, _dp, _dp]),
     "fkk_debug_tc_mma": (_i32, [_i32, _vp, _vp, _vp, _i32]),
+    "fkk_debug_eig_topk": (_i32, [_vp, _i32, _i32, _vp, _vp]),
+    "fkk_debug_eig_path": (_i32, [_i32]),
     "fkk_shard_range": (None, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fkk_merge_extremes": (_i32, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_i64), _i32, _i32,
                                   ctypes.POINTER(_i64)]),
@@ -346,6 +348,20 @@ def fkk_debug_tc_mma(mode: int, A, B):
     D = torch.zeros((128, B.shape[0]), dtype=torch.float32, device=A.device)
     _check(None, _lib.fkk_debug_tc_mma(mode, _dev_ptr(A, "A"), _dev_ptr(B, "B"), _dev_ptr(D, "D"), B.shape[0]))
     return D
+
+
+def fkk_debug_eig_topk(G, k: int):
+    """The GPU eigensolver (F4) on a symmetric CUDA fp64 matrix G: returns (V: M x k, lam: k), CUDA."""
+    torch = _torch()
+    M = G.shape[0]
+    V = torch.zeros((k, M), dtype=torch.float64, device=G.device)
+    lam = torch.zeros(k, dtype=torch.float64, device=G.device)
+    _check(None, _lib.fkk_debug_eig_topk(_dev_ptr(G, "G"), M, k, _dev_ptr(V, "V"), _dev_ptr(lam, "lam")))
+    return V.T, lam
+
+
+def fkk_debug_eig_path(M: int) -> int:
+    return int(_lib.fkk_debug_eig_path(M))
 
 
 def fkk_get_nccl_unique_id() -> bytes:
