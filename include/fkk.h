@@ -186,6 +186,9 @@ fkk_status fkk_debug_eig_topk(const double* d_G, int32_t M, int32_t k, double* d
 /* 1 if the eigensolver keeps the working matrix resident in shared memory for this M (the
  * row-resident tridiagonalisation), 0 if it streams it through L2. */
 int32_t fkk_debug_eig_path(int32_t M);
+/* Test hook: the tridiagonalisation step of the eigensolver alone.  d_det (device, 3M doubles)
+ * receives d (diagonal), e (off-diagonal, M-1 used) and tau (reflector factors). */
+fkk_status fkk_debug_tridiag(const double* d_G, int32_t M, double* d_det);
 
 /* ---------------- host-only helpers (no GPU needed; exercised by the CPU tests) ---------------- */
 /* Top-k eigenpairs of a symmetric M x M fp64 matrix (row-major; only the lower triangle is read):

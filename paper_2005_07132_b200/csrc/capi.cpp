@@ -994,6 +994,17 @@ fkk_status fkk_debug_eig_topk(const double* d_G, int32_t M, int32_t k, double* d
 
 int32_t fkk_debug_eig_path(int32_t M) { return fkk::eig_path_rows_resident(M); }
 
+fkk_status fkk_debug_tridiag(const double* d_G, int32_t M, double* d_det) {
+  if (!d_G || !d_det || M < 3) return FKK_ERR_INVALID_ARG;
+  try {
+    fkk::debug_tridiag(d_G, M, d_det);
+    return FKK_OK;
+  } catch (const Status& e) {
+    g_create_err = e.what();
+    return (fkk_status)e.code;
+  }
+}
+
 fkk_status fkk_host_eig_topk(const double* G, int32_t M, int32_t k, double* V, double* lam) {
   if (!G || !V || !lam || M < 1 || k < 1 || k > M) return FKK_ERR_INVALID_ARG;
   try {

@@ -61,6 +61,10 @@ void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const flo
                           float floor, int L, int pad_zero, const float2* tw, const float* phi, const float* phierr,
                           int sg_half, void* out, int out_imag_only, cudaStream_t s);
 size_t direct_finish_smem(int M, int L);
+// warp-partitioned fp64 ALS (k_als.cu), state in shared memory; false if M is out of its range
+size_t als_part_smem(int M, int y_f64);
+bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
+                     cudaStream_t s);
 
 // ---- factorized path
 // Gram partials (k_gram.cu): 128 x 128 tiles of the upper triangle, nsplit row segments each.
@@ -118,7 +122,8 @@ size_t eig_workspace_doubles(int M, int k);
 // M >= 3; flags |= 8 if the re-orthogonalisation finds dependent vectors.  G is not modified.
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
                      cudaStream_t s);
-int eig_path_rows_resident(int M);   // 1: the row-resident (shared-memory) tridiagonalisation is used
+int eig_path_rows_resident(int M);
+void debug_tridiag(const double* G, int M, double* det_out);   // d, e, tau (3M doubles, device)   // 1: the row-resident (shared-memory) tridiagonalisation is used
 
 void launch_tc_selftest(int mode, const float* A, const float* B, float* D, int N, cudaStream_t s);
 

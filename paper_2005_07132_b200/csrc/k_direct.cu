@@ -366,6 +366,7 @@ void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const floa
 void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, double* state,
                      void* z, int z_f64, cudaStream_t s) {
   if (n <= 0) return;
+  if (launch_als_part(y, y_f64, n, M, lam, p, iters, z, z_f64, s)) return;
   const size_t sm = (size_t)4 * M * sizeof(double);
   if (n <= 4096 && sm <= 200 * 1024) {
     // few rows: smem-resident state, one warp per row

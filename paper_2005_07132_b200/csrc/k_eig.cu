@@ -15,6 +15,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fkk_internal.h"
 
@@ -35,8 +36,10 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   __syncthreads();
   if (lane == 0) red[wid] = v;
   __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < nw; ++i) s += red[i];
+  // every warp reduces the nw partials with shuffles (fixed order: deterministic, same in all warps)
+  double s = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
 }
 
@@ -179,13 +182,11 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
   __syncthreads();
   target += gridDim.x;
   if (threadIdx.x == 0) {
-    __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
     unsigned int v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     } while ((int)(v - target) < 0);
-    __threadfence();
   }
   __syncthreads();
 }
@@ -570,7 +571,9 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+constexpr int kBxStages = 6;
 
 __global__ void __launch_bounds__(256) backxform_shared_kernel(const double* __restrict__ Wk,
                                                                const double* __restrict__ tau, int M, int k,
@@ -578,36 +581,41 @@ __global__ void __launch_bounds__(256) backxform_shared_kernel(const double* __r
                                                                const double* __restrict__ lam,
                                                                double* __restrict__ V, double* __restrict__ lam_out) {
   extern __shared__ __align__(16) double shx[];
+  constexpr int NS = kBxStages;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  double* stage = shx;                 // 2 x M
-  double* z = shx + 2 * (size_t)M + (size_t)warp * M;
+  double* stage = shx;                 // NS x M ring
+  double* z = shx + (size_t)NS * M + (size_t)warp * M;
+  double* ts = shx + (size_t)(NS + nw) * M;   // tau (read once; the per-step global load was on the critical path)
+  for (int i = tid; i < M; i += blockDim.x) ts[i] = tau[i];
   const int jj = blockIdx.x * nw + warp;
   const bool active = jj < k;
   if (active)
     for (int i = lane; i < M; i += 32) z[i] = Z[(int64_t)jj * M + i];
-  auto issue = [&](int j, int buf) {
-    if (j >= 0)
-      for (int c = j + 1 + tid; c < M; c += blockDim.x) cp_async8(stage + (size_t)buf * M + c, Wk + (int64_t)j * M + c);
+  // row j lives in ring slot (M-3-j) % NS
+  auto issue = [&](int j) {
+    if (j >= 0) {
+      double* dst = stage + (size_t)((M - 3 - j) % NS) * M;
+      for (int c = j + 1 + tid; c < M; c += blockDim.x) cp_async8(dst + c, Wk + (int64_t)j * M + c);
+    }
     cp_async_commit();
   };
-  int buf = 0;
-  issue(M - 3, 0);
+  for (int q = 0; q < NS - 1; ++q) issue(M - 3 - q);
   for (int j = M - 3; j >= 0; --j) {
-    issue(j - 1, buf ^ 1);
-    cp_async_wait1();
-    __syncthreads();
-    const double t = tau[j];
+    cp_async_wait<NS - 2>();
+    __syncthreads();                   // row j visible; every warp is done with the slot reused below
+    issue(j - (NS - 1));
+    const double t = ts[j];
     if (active && t != 0.0) {
-      const double* vj = stage + (size_t)buf * M;
+      const double* vj = stage + (size_t)((M - 3 - j) % NS) * M;
       double acc = 0.0;
+#pragma unroll 4
       for (int c = j + 1 + lane; c < M; c += 32) acc = fma(vj[c], z[c], acc);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       const double f = t * acc;
+#pragma unroll 4
       for (int c = j + 1 + lane; c < M; c += 32) z[c] -= f * vj[c];
     }
-    __syncthreads();
-    buf ^= 1;
   }
   if (!active) return;
   __syncwarp();
@@ -627,6 +635,99 @@ __global__ void __launch_bounds__(256) backxform_shared_kernel(const double* __r
   const double sg = z[bi] < 0.0 ? -1.0 : 1.0;
   for (int i = lane; i < M; i += 32) V[(int64_t)jj * M + i] = sg * z[i];
   if (lane == 0) lam_out[jj] = lam[jj];
+}
+
+// Register variant: ONE eigenvector per CTA of kBxW warps (entry c owned by thread c mod 32 kBxW,
+// NPL entries per thread in registers), so the 60 vectors spread over 60 SMs and every step is a
+// short dot (partial per thread, warp shuffle, 8-way smem sum) and axpy; the reflector streams
+// through the cp.async ring.  Two barriers per step (ring slot + partial sums, double-buffered).
+constexpr int kBxW = 8;
+template <int NPL>
+__global__ void __launch_bounds__(32 * kBxW) backxform_reg_kernel(const double* __restrict__ Wk,
+                                                                  const double* __restrict__ tau, int M, int k,
+                                                                  const double* __restrict__ Z,
+                                                                  const double* __restrict__ lam,
+                                                                  double* __restrict__ V,
+                                                                  double* __restrict__ lam_out) {
+  extern __shared__ __align__(16) double shx[];
+  constexpr int NS = kBxStages;
+  constexpr int NT = 32 * kBxW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int jj = blockIdx.x;
+  double* ts = shx + (size_t)NS * M;           // tau
+  double* red = ts + M;                        // [2][kBxW] partial dots
+  __shared__ double bestv[kBxW];
+  __shared__ int besti[kBxW];
+  for (int i = tid; i < M; i += NT) ts[i] = tau[i];
+  double zr[NPL];
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    zr[u] = c < M ? Z[(int64_t)jj * M + c] : 0.0;
+  }
+  auto issue = [&](int j) {
+    if (j >= 0) {
+      double* dst = shx + (size_t)((M - 3 - j) % NS) * M;
+      for (int c = j + 1 + tid; c < M; c += NT) cp_async8(dst + c, Wk + (int64_t)j * M + c);
+    }
+    cp_async_commit();
+  };
+  for (int q = 0; q < NS - 1; ++q) issue(M - 3 - q);
+  for (int j = M - 3; j >= 0; --j) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    issue(j - (NS - 1));
+    const double t = ts[j];
+    if (t == 0.0) continue;                    // uniform across the CTA
+    const double* vj = shx + (size_t)((M - 3 - j) % NS) * M;
+    double vc[NPL];
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) {
+      const int c = tid + NT * u;
+      vc[u] = (c > j && c < M) ? vj[c] : 0.0;
+      acc = fma(vc[u], zr[u], acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    double* rb = red + (j & 1) * kBxW;
+    if (lane == 0) rb[warp] = acc;
+    __syncthreads();
+    double dot = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < kBxW; ++w2) dot += rb[w2];
+    const double f = t * dot;
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) zr[u] = fma(-f, vc[u], zr[u]);
+  }
+  // sign rule: entry of largest |.| positive, ties -> lowest index
+  double best = -1.0, bval = 0.0;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    if (c < M && fabs(zr[u]) > best) { best = fabs(zr[u]); bi = c; bval = zr[u]; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const double ov = __shfl_xor_sync(0xffffffffu, bval, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; bval = ov; }
+  }
+  if (lane == 0) { bestv[warp] = bval; besti[warp] = bi; red[warp] = best; }
+  __syncthreads();
+  double gb = red[0], gv = bestv[0];
+  int gi = besti[0];
+  for (int w2 = 1; w2 < kBxW; ++w2)
+    if (red[w2] > gb || (red[w2] == gb && besti[w2] < gi)) { gb = red[w2]; gi = besti[w2]; gv = bestv[w2]; }
+  const double sg = gv < 0.0 ? -1.0 : 1.0;
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    if (c < M) V[(int64_t)jj * M + c] = sg * zr[u];
+  }
+  if (tid == 0) lam_out[jj] = lam[jj];
 }
 
 // Re-orthogonalisation by CholeskyQR, applied twice (CholQR2): S = Z Z^T (k x k), S = R^T R,
@@ -651,7 +752,7 @@ __global__ void gram_rows_kernel(const double* __restrict__ Z, int M, int k, dou
 
 // one CTA: Cholesky S = R^T R (R upper, row-major), then T = R^{-1} (upper) into Tout
 __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ S, int k, double* __restrict__ Tout,
-                                                       int* __restrict__ flags) {
+                                                       int* __restrict__ fallback) {
   extern __shared__ __align__(16) double sc[];
   double* Rm = sc;          // k x k
   double* Tm = sc + k * k;  // k x k
@@ -663,7 +764,8 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict_
     const double dcc = Rm[c * k + c];
     const double rcc = dcc > 0.0 ? sqrt(dcc) : 0.0;
     __syncthreads();
-    if (tid == 0 && !(dcc > 0.0)) atomicOr(flags, 8);
+    // a pivot that lost ~12 digits: the vectors are (numerically) dependent -> robust fallback
+    if (tid == 0 && !(dcc > 1e-8 * S[c * k + c])) atomicOr(fallback, 1);
     for (int j = c + 1 + tid; j < k; j += nt) Rm[c * k + j] = rcc > 0.0 ? Rm[c * k + j] / rcc : 0.0;
     __syncthreads();
     if (tid == 0) Rm[c * k + c] = rcc;
@@ -697,11 +799,80 @@ __global__ void apply_rinv_kernel(const double* __restrict__ Z, int M, int k, co
   }
 }
 
+
+// Fallback re-orthogonalisation (only when CholQR met a near-singular Gram, e.g. a multiple zero
+// eigenvalue of a rank-deficient G where inverse iteration returns nearly parallel vectors):
+// classical Gram-Schmidt twice in descending-eigenvalue order on the inverse-iteration vectors; a
+// vector that loses > 6 digits is replaced by a hashed pseudo-random vector orthogonalised against
+// the accepted ones (which spans the remaining eigenspace when the cluster is the null space).
+__global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __restrict__ fallback,
+                                                               const double* __restrict__ Zin, double* __restrict__ Z,
+                                                               int M, int k) {
+  if (*fallback == 0) return;
+  __shared__ double dots[1024];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  auto norm2 = [&](const double* z) {
+    double sacc = 0.0;
+    for (int i = tid; i < M; i += nt) sacc += z[i] * z[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    __syncthreads();
+    if (lane == 0) red[wid] = sacc;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) tot += red[w2];
+    return tot;
+  };
+  auto project_out = [&](double* zj, int j) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int c = wid; c < j; c += nw) {
+        const double* zc = Z + (int64_t)c * M;
+        double acc = 0.0;
+        for (int i = lane; i < M; i += 32) acc = fma(zc[i], zj[i], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) dots[c] = acc;
+      }
+      __syncthreads();
+      for (int i = tid; i < M; i += nt) {
+        double x = zj[i];
+        for (int c = 0; c < j; ++c) x -= dots[c] * Z[(int64_t)c * M + i];
+        zj[i] = x;
+      }
+      __syncthreads();
+    }
+  };
+  for (int j = 0; j < k; ++j) {
+    double* zj = Z + (int64_t)j * M;
+    for (int i = tid; i < M; i += nt) zj[i] = Zin[(int64_t)j * M + i];
+    __syncthreads();
+    const double n0 = norm2(zj);
+    project_out(zj, j);
+    double n1 = norm2(zj);
+    for (int attempt = 0; attempt < 4 && !(n1 > 1e-12 * n0); ++attempt) {
+      for (int i = tid; i < M; i += nt) {
+        uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(j + 1 + 977 * attempt) + 0xC2B2AE3D27D4EB4Full * (uint64_t)(i + 1);
+        h ^= h >> 29; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 32;
+        zj[i] = (double)(h >> 11) / 9007199254740992.0 - 0.5;
+      }
+      __syncthreads();
+      const double nr = norm2(zj);
+      project_out(zj, j);
+      n1 = norm2(zj);
+      if (n1 > 1e-6 * nr) break;
+    }
+    const double inv = 1.0 / sqrt(n1);
+    for (int i = tid; i < M; i += nt) zj[i] *= inv;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 size_t eig_workspace_doubles(int M, int k) {
-  // d, e, tau (3M) + p (16M) + lam, tnorm (k+1) + Z, Z2 (2kM) + S, T (2k^2) + counter + A copy (M*M)
-  return 19 * (size_t)M + (size_t)k + 1 + 2 * (size_t)k * M + 2 * (size_t)k * k + 16 + (size_t)M * M;
+  // d, e, tau (3M) + p / LL words (16M) + lam, tnorm (k+1) + Z, Z2, Z3 (3kM) + S, T (2k^2) + flag + A (M*M)
+  return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 16 + (size_t)M * M;
 }
 
 int eig_path_rows_resident(int M) {
@@ -709,11 +880,32 @@ int eig_path_rows_resident(int M) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const char* force = getenv("FKK_EIG_FORCE_L2");   // debugging / A-B only
+  if (force && force[0] == '1') return 0;
   return M >= 3 && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
 }
 
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
+                     cudaStream_t s, double* dbg_det);
+
+void debug_tridiag(const double* G, int M, double* det_out) {
+  double* work = nullptr;
+  FKK_CUDA_CHECK(cudaMalloc(&work, eig_workspace_doubles(M, 1) * sizeof(double)));
+  double* V = nullptr;
+  FKK_CUDA_CHECK(cudaMalloc(&V, (size_t)M * sizeof(double) * 2));
+  launch_eig_topk(G, M, 1, work, V, V + M, nullptr, nullptr, det_out);
+  FKK_CUDA_CHECK(cudaDeviceSynchronize());
+  cudaFree(work);
+  cudaFree(V);
+}
+
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
                      cudaStream_t s) {
+  launch_eig_topk(G, M, k, work, V, lam_out, flags, s, nullptr);
+}
+
+void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
+                     cudaStream_t s, double* dbg_det) {
   double* d = work;
   double* e = d + M;
   double* tau = e + M;
@@ -722,20 +914,22 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   double* tnorm = lam + k;
   double* Z = tnorm + 1;
   double* Z2 = Z + (size_t)k * M;
-  double* S = Z2 + (size_t)k * M;
+  double* Z3 = Z2 + (size_t)k * M;
+  double* S = Z3 + (size_t)k * M;
   double* T = S + (size_t)k * k;
-  unsigned int* ctr = reinterpret_cast<unsigned int*>(T + (size_t)k * k);
+  int* fallback = reinterpret_cast<int*>(T + (size_t)k * k);
   double* A = T + (size_t)k * k + 16;      // working matrix / published rows / reflectors (M x M)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (eig_path_rows_resident(M)) {
-    // row-resident cooperative tridiagonalisation (G is read, never copied)
+    // row-resident cooperative tridiagonalisation (G is read, never copied); LL packet exchange
     const size_t smem = tridiag_rows_smem(M, sms);
     FKK_CUDA_CHECK(cudaFuncSetAttribute(tridiag_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_rows_kernel, kTsThreads, smem));
     if (per < 1) throw Status(10, "tridiag_rows kernel cannot be co-resident");
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(fallback) + 2;
     FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
     int Mi = M;
     const double* Gc = G;
@@ -756,46 +950,71 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)kg, dim3(sms), dim3(kTriThreads), args, smem, s));
     count_launch();
   }
+  if (dbg_det) {   // debug: d, e, tau only
+    FKK_CUDA_CHECK(cudaMemcpyAsync(dbg_det, d, 3 * (size_t)M * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
   bisect_kernel<<<(k * 32 + 127) / 128, 128, 0, s>>>(d, e, M, k, lam, tnorm);
   check_launch("eig_bisect");
   const size_t ism = (size_t)5 * M * sizeof(double) + (size_t)M + 16;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
   inviter_kernel<<<k, 32, ism, s>>>(d, e, M, k, lam, tnorm, Z);
   check_launch("eig_inviter");
-  // CholQR2 re-orthogonalisation (k <= 128: the k x k factor lives in one CTA's shared memory)
+  // CholQR2 re-orthogonalisation (k <= 128: the k x k factor lives in one CTA's shared memory):
+  // Z -> Z2 -> Z3; a near-singular Gram switches to the Gram-Schmidt fallback (Z -> Z3)
+  double* Zf = Z3;
   if (k <= 128) {
     const size_t csm = 2 * (size_t)k * k * sizeof(double);
     FKK_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    FKK_CUDA_CHECK(cudaMemsetAsync(fallback, 0, sizeof(int), s));
     const int npairs = k * (k + 1) / 2;
     const int agrid = (int)std::min<int64_t>(((int64_t)M * k + 255) / 256, 4 * sms);
     for (int pass = 0; pass < 2; ++pass) {
       const double* zin = pass == 0 ? Z : Z2;
-      double* zout = pass == 0 ? Z2 : Z;
+      double* zout = pass == 0 ? Z2 : Z3;
       gram_rows_kernel<<<(npairs * 32 + 255) / 256, 256, 0, s>>>(zin, M, k, S);
       check_launch("eig_reorth_gram");
-      chol_inv_kernel<<<1, 256, csm, s>>>(S, k, T, flags);
+      chol_inv_kernel<<<1, 256, csm, s>>>(S, k, T, fallback);
       check_launch("eig_reorth_chol");
       apply_rinv_kernel<<<agrid, 256, 0, s>>>(zin, M, k, T, zout);
       check_launch("eig_reorth_apply");
     }
+    reorth_fallback_kernel<<<1, 1024, 0, s>>>(fallback, Z, Z3, M, k);
+    check_launch("eig_reorth_fallback");
   } else {
     reorth_kernel<<<1, 1024, 0, s>>>(Z, M, k);
     check_launch("eig_reorth");
+    Zf = Z;
   }
-  // back-transformation: reflector-sharing CTAs when (2 + nw) M doubles fit in shared memory
+  // back-transformation: eigenvectors in registers (M <= 2048), else reflector-sharing CTAs
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t rsm = ((size_t)(kBxStages + 1) * M + 2 * kBxW) * sizeof(double);
+  if (M >= 3 && M <= 32 * kBxW * 8 && rsm <= (size_t)maxsm) {
+#define FKK_BX_REG(NPL)                                                                                  \
+    {                                                                                                    \
+      auto kb = backxform_reg_kernel<NPL>;                                                               \
+      FKK_CUDA_CHECK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));   \
+      kb<<<k, 32 * kBxW, rsm, s>>>(A, tau, M, k, Zf, lam, V, lam_out);                                  \
+    }
+    if (M <= 32 * kBxW * 2) FKK_BX_REG(2)
+    else if (M <= 32 * kBxW * 4) FKK_BX_REG(4)
+    else FKK_BX_REG(8)
+#undef FKK_BX_REG
+    check_launch("eig_backxform");
+    return;
+  }
   int nw = 8;
-  while (nw > 1 && (size_t)(2 + nw) * M * sizeof(double) > (size_t)maxsm) --nw;
-  const size_t bsm = (size_t)(2 + nw) * M * sizeof(double);
+  while (nw > 1 && (size_t)(kBxStages + nw + 1) * M * sizeof(double) > (size_t)maxsm) --nw;
+  const size_t bsm = (size_t)(kBxStages + nw + 1) * M * sizeof(double);
   if (M >= 3 && bsm <= (size_t)maxsm) {
     FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-    backxform_shared_kernel<<<(k + nw - 1) / nw, nw * 32, bsm, s>>>(A, tau, M, k, Z, lam, V, lam_out);
+    backxform_shared_kernel<<<(k + nw - 1) / nw, nw * 32, bsm, s>>>(A, tau, M, k, Zf, lam, V, lam_out);
     check_launch("eig_backxform");
   } else {
     const size_t bsm1 = (size_t)M * sizeof(double);
     FKK_CUDA_CHECK(cudaFuncSetAttribute(backxform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm1));
-    backxform_kernel<<<k, kEigThreads, bsm1, s>>>(A, tau, M, Z, lam, V, lam_out);
+    backxform_kernel<<<k, kEigThreads, bsm1, s>>>(A, tau, M, Zf, lam, V, lam_out);
     check_launch("eig_backxform");
   }
 }

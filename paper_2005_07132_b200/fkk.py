@@ -80,6 +80,7 @@ _SIGS = {
     "fkk_debug_tc_mma": (_i32, [_i32, _vp, _vp, _vp, _i32]),
     "fkk_debug_eig_topk": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fkk_debug_eig_path": (_i32, [_i32]),
+    "fkk_debug_tridiag": (_i32, [_vp, _i32, _vp]),
     "fkk_shard_range": (None, [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fkk_merge_extremes": (_i32, [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_i64), _i32, _i32,
                                   ctypes.POINTER(_i64)]),
@@ -358,6 +359,15 @@ def fkk_debug_eig_topk(G, k: int):
     lam = torch.zeros(k, dtype=torch.float64, device=G.device)
     _check(None, _lib.fkk_debug_eig_topk(_dev_ptr(G, "G"), M, k, _dev_ptr(V, "V"), _dev_ptr(lam, "lam")))
     return V.T, lam
+
+
+def fkk_debug_tridiag(G):
+    """The tridiagonalisation alone: returns (d, e, tau) as CUDA fp64 tensors."""
+    torch = _torch()
+    M = G.shape[0]
+    out = torch.zeros(3 * M, dtype=torch.float64, device=G.device)
+    _check(None, _lib.fkk_debug_tridiag(_dev_ptr(G, "G"), M, _dev_ptr(out, "out")))
+    return out[:M], out[M:2 * M], out[2 * M:]
 
 
 def fkk_debug_eig_path(M: int) -> int:

@@ -27,7 +27,7 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
 tot = {}
 for e in prof.events():
     if e.device_type.name == "CUDA":
-        n = e.name.split("(")[0].replace("void ", "").replace("fkk::(anonymous namespace)::", "")
+        n = e.name.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0]
         tot[n] = tot.get(n, 0.0) + e.device_time_total / 3 / 1e3
 for n, v in sorted(tot.items(), key=lambda x: -x[1]):
     print(f"{v:9.3f} ms  {n}")
