@@ -173,13 +173,15 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
     }
     if (nper == 0)
       for (int q = 0; q < 64; ++q) part[(int64_t)(64 * chalf + q) * GT + i] = 0.0;
-  } else if (lane == 0) {
-    // ------------------------------------------------------------ single-thread MMA issue
+  } else {
+    // ------------------------------------------------------------ MMA issue (warp 16 runs the loop; one
+    // elected lane issues -- descriptors stay in uniform registers)
     constexpr uint32_t idesc = tc::make_idesc_tf32(GT, GT, false, false);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t eph[2] = {0, 0};
     const uint32_t sbase = tc::smem_u32(smem);
+    const uint64_t d00 = tc::make_sdesc(sbase, GLBO, GSBO);
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
       if (pidx >= 2) {
@@ -193,23 +195,26 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
       for (int64_t k0 = p0; k0 < p1; k0 += GKC) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t st = sbase + stage * GSTAGE_BYTES;
-        const uint32_t ahi = st, alo = st + GOP_BYTES;
-        const uint32_t bhi = diag ? ahi : st + 2 * GOP_BYTES, blo = diag ? alo : st + 3 * GOP_BYTES;
+        const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * GSTAGE_BYTES)), dal = tc::sdesc_add(dah, GOP_BYTES);
+        const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, 2 * GOP_BYTES);
+        const uint64_t dbl = diag ? dal : tc::sdesc_add(dah, 3 * GOP_BYTES);
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < GKC / 8; ++ks) {
-          const uint32_t ko = ks * 2 * GLBO;   // 8 pixels = 2 K-core matrices
-          const uint64_t dah = tc::make_sdesc(ahi + ko, GLBO, GSBO), dal = tc::make_sdesc(alo + ko, GLBO, GSBO);
-          const uint64_t dbh = tc::make_sdesc(bhi + ko, GLBO, GSBO), dbl = tc::make_sdesc(blo + ko, GLBO, GSBO);
-          tc::mma_tf32(d_mid, dal, dbh, idesc, acc);   // lo_i * hi_j
-          tc::mma_tf32(d_mid, dah, dbl, idesc, 1);     // hi_i * lo_j
-          tc::mma_tf32(d_hi, dah, dbh, idesc, acc);    // hi_i * hi_j
-          acc = 1;
+          for (int ks = 0; ks < GKC / 8; ++ks) {
+            const uint32_t ko = ks * 2 * GLBO;   // 8 pixels = 2 K-core matrices
+            tc::mma_tf32(d_mid, tc::sdesc_add(dal, ko), tc::sdesc_add(dbh, ko), idesc, acc);   // lo_i * hi_j
+            tc::mma_tf32(d_mid, tc::sdesc_add(dah, ko), tc::sdesc_add(dbl, ko), idesc, 1);     // hi_i * lo_j
+            tc::mma_tf32(d_hi, tc::sdesc_add(dah, ko), tc::sdesc_add(dbh, ko), idesc, acc);    // hi_i * hi_j
+            acc = 1;
+          }
+          tc::mma_commit(&empty[stage]);
         }
-        tc::mma_commit(&empty[stage]);
+        acc = 1;
+        __syncwarp();
         if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
       }
-      tc::mma_commit(&acc_full[b]);
+      if (tc::elect_one()) tc::mma_commit(&acc_full[b]);
+      __syncwarp();
     }
   }
   tc::tc_fence_before();

@@ -2,11 +2,12 @@
 // f-scaling of Eq. 10; also the first GEMM of ML apply, Eq. 25) on the tensor cores, with the
 // per-tile column extremes that feed q (Eqs. 13-15; ties -> lowest pixel).
 // tcgen05.mma kind::tf32, 3xTF32; M = 128 pixels per tile, N = kp, K = channels in stages of 32.
-//   warps 0-3 : producers - A0 tile (128 px x 32 ch) fp32 loads one stage ahead in registers,
+//   warps 0-7 : producers - A0 tile (128 px x 32 ch) fp32 loads FOUR stages ahead in registers (the
+//               kernel streams A0 from HBM: >= 48 KB per SM must be in flight to cover the latency),
 //               tf32 hi/lo split, K-major smem (LBO 144 B pad: conflict-free 16-B stores)
-//   warps 4-7 : epilogue  - tcgen05.ld of the 128 x kp accumulator (TMEM lane = pixel), US row
+//   warps 8-11: epilogue  - tcgen05.ld of the 128 x kp accumulator (TMEM lane = pixel), US row
 //               stores, per-column (max, argmax, min, argmin) by warp shuffles + smem
-//   warp 8    : TMEM alloc, W-stage bulk copies (cp.async.bulk, mbarrier tx), MMA issue
+//   warp 12   : TMEM alloc, W-stage bulk copies (cp.async.bulk, mbarrier tx), MMA issue
 // W^T is pre-staged (hi, lo) per K-stage in the exact K-major smem image by build_wimg.
 // Persistent CTAs walk pixel tiles.  Accuracy: the tensor-core accumulator truncates on each add
 // (DESIGN.md "Gram accuracy"), so hi*hi accumulates per 512-channel segment in its own TMEM
@@ -29,7 +30,8 @@ constexpr int PKC = 32;            // channels per stage
 constexpr int PA_LBO = 144, PA_SBO = (PKC / 4) * PA_LBO;     // 1152
 constexpr int PA_BYTES = (PTM / 8) * PA_SBO;                  // 18432 per hi / lo
 constexpr int PB_LBO = 128, PB_SBO = (PKC / 4) * PB_LBO;     // 1024
-constexpr int PTHREADS = 288;
+constexpr int PTHREADS = 416;
+constexpr int PPROD = 256;         // producer threads
 
 __host__ __device__ inline int pb_part(int kp) { return (kp / 8) * PB_SBO; }       // hi or lo
 __host__ __device__ inline int pb_stage(int kp) { return 2 * pb_part(kp); }
@@ -67,43 +69,43 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
   const int64_t ntiles = (n + PTM - 1) / PTM;
   const int nst = (M + PKC - 1) / PKC;           // K stages per tile
   if (tid == 0) {
-    for (int s = 0; s < PSTAGES; ++s) { tc::mbar_init(&full[s], 129); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < PSTAGES; ++s) { tc::mbar_init(&full[s], PPROD + 1); tc::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 128); }
     tc::fence_mbar_init();
   }
   const int nseg = p_nseg(M), setc = p_set_cols(M, kp), nbuf = p_nbuf(M, kp);
-  if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 12) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
+  if (warp < 8) {
     // ------------------------------------------------------------ producers
-    // item (pixel p, channel quad c4): p = idx >> 3, c4 = idx & 7; 8 items per thread per stage
-    float4 x[8];
+    // item (pixel p, channel quad c4): p = idx >> 3, c4 = idx & 7; 4 items per thread per stage;
+    // register slots X0..X3 rotate and hold the next four stages
+    float4 X0[4], X1[4];
     int stage = 0;
     uint32_t phase = 0;
-    auto load = [&](int64_t t, int st) {
+    auto load = [&](float4 (&x)[4], int64_t pos) {   // pos = linear (tile, stage) index of this CTA
+      const int64_t t = blockIdx.x + (pos / nst) * gridDim.x;
+      const int st = (int)(pos % nst);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        const int idx = tid + 128 * h;
+      for (int h = 0; h < 4; ++h) {
+        const int idx = tid + PPROD * h;
         const int p = idx >> 3, c4 = idx & 7;
         const int64_t pp = t * PTM + p;
         const int col = st * PKC + 4 * c4;
         x[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (pp < n && col < M) x[h] = __ldg(reinterpret_cast<const float4*>(A + pp * (int64_t)M + col));
+        if (t < ntiles && pp < n && col < M) x[h] = __ldg(reinterpret_cast<const float4*>(A + pp * (int64_t)M + col));
       }
     };
-    int64_t t = blockIdx.x;
-    int st = 0;
-    if (t < ntiles) load(t, 0);
-    while (t < ntiles) {
+    auto store = [&](const float4 (&x)[4]) {
       tc::mbar_wait(&empty[stage], phase ^ 1);
       unsigned char* sa = smem + stage * SB;
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        const int idx = tid + 128 * h;
+      for (int h = 0; h < 4; ++h) {
+        const int idx = tid + PPROD * h;
         const int p = idx >> 3, c4 = idx & 7;
         float4 hi, lo;
         tc::split4(x[h], hi, lo);
@@ -114,12 +116,30 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full[stage]);
       if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
-      if (++st == nst) { st = 0; t += gridDim.x; }
-      if (t < ntiles) load(t, st);
+    };
+    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t npos = my_tiles * nst;
+    float4 X2[4], X3[4];
+    load(X0, 0);
+    load(X1, 1);
+    load(X2, 2);
+    load(X3, 3);
+    for (int64_t pos = 0; pos < npos; pos += 4) {   // four register slots: loads run 4 stages ahead
+      store(X0);
+      load(X0, pos + 4);
+      if (pos + 1 >= npos) break;
+      store(X1);
+      load(X1, pos + 5);
+      if (pos + 2 >= npos) break;
+      store(X2);
+      load(X2, pos + 6);
+      if (pos + 3 >= npos) break;
+      store(X3);
+      load(X3, pos + 7);
     }
-  } else if (warp < 8) {
+  } else if (warp < 12) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;
+    const int ew = warp - 8;
     uint32_t ph[2] = {0, 0};
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -189,11 +209,14 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
     }
-  } else if (warp == 8 && lane == 0) {
-    // ------------------------------------------------------------ W stages + MMA issue
+  } else if (warp == 12) {
+    // ------------------------------------------------------------ W stages + MMA issue (whole warp runs
+    // the loop; one elected lane issues -- descriptors stay in uniform registers)
     const uint32_t idesc = tc::make_idesc_tf32(PTM, kp, false, false);
     const uint32_t sbase = tc::smem_u32(smem);
     const int WB = pb_stage(kp), WP = pb_part(kp);
+    const uint64_t da0 = tc::make_sdesc(sbase, PA_LBO, PA_SBO);
+    const uint64_t dw0 = tc::make_sdesc(sbase + 2 * PA_BYTES, PB_LBO, PB_SBO);
     int stage = 0;
     uint32_t phase = 0, ae[2] = {0, 0};
     int64_t it = 0;
@@ -205,34 +228,39 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
       for (int st = 0; st < nst; ++st) {
         tc::mbar_wait(&empty[stage], phase ^ 1);          // slot free (also for the W copy)
         const uint32_t sa = sbase + stage * SB;
-        bulk_g2s(sa + 2 * PA_BYTES, reinterpret_cast<const unsigned char*>(wimg) + (size_t)st * WB, WB, &full[stage]);
+        if (tc::elect_one())
+          bulk_g2s(sa + 2 * PA_BYTES, reinterpret_cast<const unsigned char*>(wimg) + (size_t)st * WB, WB, &full[stage]);
+        __syncwarp();
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t ahi = sa, alo = sa + PA_BYTES, bhi = sa + 2 * PA_BYTES, blo = bhi + WP;
+        const uint64_t dah = tc::sdesc_add(da0, (uint32_t)(stage * SB)), dal = tc::sdesc_add(dah, PA_BYTES);
+        const uint64_t dbh = tc::sdesc_add(dw0, (uint32_t)(stage * SB)), dbl = tc::sdesc_add(dbh, (uint32_t)WP);
+        const int sg = (st * PKC) / PSEG;
+        const uint32_t dh = dset + sg * kp;
+        const bool seg_start = (st * PKC) % PSEG == 0;
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < PKC / 8; ++ks) {
-          const uint64_t dah = tc::make_sdesc(ahi + ks * 2 * PA_LBO, PA_LBO, PA_SBO);
-          const uint64_t dal = tc::make_sdesc(alo + ks * 2 * PA_LBO, PA_LBO, PA_SBO);
-          const uint64_t dbh = tc::make_sdesc(bhi + ks * 2 * PB_LBO, PB_LBO, PB_SBO);
-          const uint64_t dbl = tc::make_sdesc(blo + ks * 2 * PB_LBO, PB_LBO, PB_SBO);
-          const int sg = (st * PKC) / PSEG;
-          const uint32_t dh = dset + sg * kp;
-          const uint32_t accx = (st > 0 || ks > 0) ? 1u : 0u;
-          const uint32_t acch = ((st * PKC) % PSEG != 0 || ks > 0) ? 1u : 0u;
-          tc::mma_tf32(dx, dal, dbh, idesc, accx);
-          tc::mma_tf32(dx, dah, dbl, idesc, 1u);
-          tc::mma_tf32(dh, dah, dbh, idesc, acch);
+          for (int ks = 0; ks < PKC / 8; ++ks) {
+            const uint32_t oa = ks * 2 * PA_LBO, ob = ks * 2 * PB_LBO;
+            const uint32_t accx = (st > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acch = (!seg_start || ks > 0) ? 1u : 0u;
+            tc::mma_tf32(dx, tc::sdesc_add(dal, oa), tc::sdesc_add(dbh, ob), idesc, accx);
+            tc::mma_tf32(dx, tc::sdesc_add(dah, oa), tc::sdesc_add(dbl, ob), idesc, 1u);
+            tc::mma_tf32(dh, tc::sdesc_add(dah, oa), tc::sdesc_add(dbh, ob), idesc, acch);
+          }
+          tc::mma_commit(&empty[stage]);
         }
-        tc::mma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == PSTAGES) { stage = 0; phase ^= 1; }
       }
-      tc::mma_commit(&acc_full[b]);
+      if (tc::elect_one()) tc::mma_commit(&acc_full[b]);
+      __syncwarp();
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 8) tc::tmem_dealloc(tmem, 512);
+  if (warp == 12) tc::tmem_dealloc(tmem, 512);
 }
 
 // W^T image per K-stage st: rows n (rank, < kp), K = channel j in the stage, K-major hi/lo.

@@ -4,11 +4,12 @@
 // (amp_c, ph_c) so TMEM columns (2j, 2j+1) are the exponent and phase of channel j; 3xTF32
 // (hi*hi + hi*lo + lo*hi; K = kr = roundup8(k) is short, so one TMEM accumulator suffices).
 //   warps 0-3  : producers - the US tile (128 x kr) -> tf32 hi/lo -> K-major smem (LBO 144 B pad)
-//   warps 4-11 : epilogue  - tcgen05.ld, exp/sincos into a per-thread smem slot, then one bulk
-//                copy (cp.async.bulk smem -> global) per thread: its pixel row's half of the chunk
-//                (contiguous 128 B of complex64), double-buffered; 4 TMEM accumulators rotate.
-//                (Measured: faster than staging a tile and storing coalesced rows after a named
-//                barrier, 2.77 vs 3.35 ms at cfg3.)
+//   warps 4-11 : epilogue  - tcgen05.ld, exp/sincos into a swizzled smem box [128 px][half chunk]
+//                (one pixel row per thread, conflict-free through the TMA swizzle), then ONE 2-D
+//                TMA tensor store per box (cp.async.bulk.tensor, out-of-range rows / channels
+//                clipped by the TMA unit); boxes double-buffered per half; 4 TMEM accumulators
+//                rotate.  (The previous per-thread 128-B bulk copies issued 44 M TMA operations at
+//                cfg3 and ran at 2.7 ms.)
 //   warp 12    : TMEM alloc; B-chunk bulk copies (cp.async.bulk, mbarrier tx) and the MMA issue
 // B is pre-staged once per basis in global memory in the exact K-major smem image (hi, lo).
 // Persistent CTAs walk pixel tiles; the B chunk sequence repeats per tile (L2-resident, ~1 MB).
@@ -19,16 +20,20 @@
 
 #include "fkk_internal.h"
 #include "tc_common.cuh"
+#include "tma.h"
 
 namespace fkk {
 
 namespace {
 
 constexpr int RTM = 128;          // pixels per tile (UMMA M)
-constexpr int RT_THREADS = 416;
-constexpr int A_LBO = 144;        // padded: conflict-free producer stores
+constexpr int RT_PARTS = 4;       // epilogue: 4 warps per TMEM lane group, each a quarter of the chunk
+constexpr int RT_EPI = 128 * RT_PARTS;
+constexpr int RT_THREADS = 128 + RT_EPI + 32;
+constexpr int A_LBO = 128;        // unpadded (the A tile is stored once per tile; conflicts there are cheap)
 constexpr int B_LBO = 128;
-constexpr int SLOT = 144;         // epilogue staging slot per thread (128 B + pad)
+static_assert(A_LBO == B_LBO, "the MMA loop advances both descriptors by the same K offset");
+constexpr int RT_NBUF = 2;        // epilogue output boxes per part (double buffer)
 
 struct RtGeom {
   int kr, nch, N, nchunks;
@@ -67,34 +72,43 @@ __device__ __forceinline__ float2 cis_exp(float amp, float ph) {
   return make_float2(m * cs, m * sn);
 }
 
+// output box: 128 pixel rows x (nch/2 channels) of one chunk half; row bytes = 16 B granules
+__host__ __device__ inline int rt_row_bytes(const RtGeom& g, int imag_only) {
+  return (g.nch / RT_PARTS) * (imag_only ? 4 : 8);
+}
+__host__ __device__ inline int rt_box_region(const RtGeom& g) { return (RTM * (g.nch / RT_PARTS) * 8 + 1023) / 1024 * 1024; }
+
+// RT_BST: B-chunk stages (bulk copies run RT_BST - 1 chunks ahead); 3 when the smem fits, else 2
+template <int RT_BST>
 __global__ void __launch_bounds__(RT_THREADS, 1)
 reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, const float* __restrict__ bimg, int M,
-                      void* __restrict__ out, int imag_only) {
+                      const __grid_constant__ CUtensorMap tmap_out, int imag_only) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const RtGeom g = rt_geom(k, M);
-  unsigned char* a_hi = smem;
-  unsigned char* a_lo = smem + g.a_bytes;
-  unsigned char* bst = smem + 2 * g.a_bytes;                 // 2 stages
-  unsigned char* stg = bst + 2 * g.b_stage;                  // [2][256 threads][SLOT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 2 * 256 * SLOT);
-  uint64_t* a_full = bars;          // producers -> MMA (count 128)
-  uint64_t* a_empty = bars + 1;     // MMA commit -> producers
-  uint64_t* b_full = bars + 2;      // [2] bulk copy tx
-  uint64_t* b_empty = bars + 4;     // [2] MMA commit
-  uint64_t* acc_full = bars + 6;    // [4] MMA commit -> epilogue
-  uint64_t* acc_empty = bars + 10;  // [4] epilogue (256) -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  // [RT_NBUF][2 halves][box]; the TMA swizzle pattern is a function of the smem address -> 1024-align
+  unsigned char* stg = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
+  unsigned char* a_hi = stg + RT_NBUF * RT_PARTS * rt_box_region(g);
+  unsigned char* a_lo = a_hi + g.a_bytes;
+  unsigned char* bst = a_lo + g.a_bytes;                     // RT_BST stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bst + RT_BST * g.b_stage);
+  uint64_t* a_full = bars;                      // producers -> MMA (count 128)
+  uint64_t* a_empty = bars + 1;                 // MMA commit -> producers
+  uint64_t* b_full = bars + 2;                  // [RT_BST] bulk copy tx
+  uint64_t* b_empty = b_full + RT_BST;          // [RT_BST] MMA commit
+  uint64_t* acc_full = b_empty + RT_BST;        // [4] MMA commit -> epilogue
+  uint64_t* acc_empty = acc_full + 4;           // [4] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (n + RTM - 1) / RTM;
   if (tid == 0) {
     tc::mbar_init(a_full, 128);
     tc::mbar_init(a_empty, 1);
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&b_full[s], 1); tc::mbar_init(&b_empty[s], 1); }
-    for (int b = 0; b < 4; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 256); }
+    for (int s = 0; s < RT_BST; ++s) { tc::mbar_init(&b_full[s], 1); tc::mbar_init(&b_empty[s], 1); }
+    for (int b = 0; b < 4; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], RT_EPI); }
     tc::fence_mbar_init();
   }
-  if (warp == 12) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 4 + RT_EPI / 32) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -121,100 +135,128 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
       tc::mbar_arrive(a_full);
       ph ^= 1;
     }
-  } else if (warp < 12) {
+  } else if (warp < 4 + RT_EPI / 32) {
     // ------------------------------------------------------------ epilogue
-    const int lg = warp & 3, half = (warp - 4) >> 2;
-    const int et = tid - 128;                    // 0..255
-    const int nq = g.nch / 2;                    // channels handled by this thread per chunk
+    const int lg = warp & 3, half = (warp - 4) >> 2;   // half = part (quarter of the chunk)
+    const int nq = g.nch / RT_PARTS;             // channels handled by this thread per chunk
+    const int rb = rt_row_bytes(g, imag_only);   // 64, 32 or 16 B = TMA swizzle width (16: none)
+    const int r = lg * 32 + lane;                // pixel row within the tile
+    const int swz = rb >= 32 ? ((r * rb) >> 7) & (rb / 16 - 1) : 0;
+    const bool issuer = lg == 0 && lane == 0;
+    const uint32_t bar_id = 1 + half;            // named barrier of the 128 threads of this part
+    if (issuer) tma::prefetch_map(&tmap_out);
     uint32_t ph[4] = {0, 0, 0, 0};
     int64_t gq = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t p = t * RTM + lg * 32 + lane;
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
         const int b = (int)(gq & 3);
         tc::mbar_wait(&acc_full[b], ph[b]);
         ph[b] ^= 1;
         tc::tc_fence_after();
-        const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b * g.N + half * g.nch);
-        // the slot written two chunks ago must have been read by its bulk copy
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        unsigned char* slot = stg + ((gq & 1) * 256 + et) * SLOT;
-        for (int j0 = 0; j0 < nq; j0 += 8) {   // 8 channels = 16 TMEM columns per tcgen05.ld
-          float v[16];
-          tc::tmem_ld16(tb + 2 * j0, v);
+        const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b * g.N + half * 2 * nq);
+        // box buffer of this chunk must have been read by its store from RT_NBUF chunks ago
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(RT_NBUF - 1) : "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        unsigned char* box = stg + ((gq % RT_NBUF) * RT_PARTS + half) * rt_box_region(g);
+        unsigned char* row = box + r * rb;
+        auto emit = [&](const float* v, int j0, int cnt) {
 #pragma unroll
           for (int q = 0; q < 8; q += 2) {
+            if (q >= cnt) break;
             const float2 z0 = cis_exp(v[2 * q], v[2 * q + 1]);
             const float2 z1 = cis_exp(v[2 * q + 2], v[2 * q + 3]);
-            if (imag_only) *reinterpret_cast<float2*>(slot + (j0 + q) * 4) = make_float2(z0.y, z1.y);
-            else *reinterpret_cast<float4*>(slot + (j0 + q) * 8) = make_float4(z0.x, z0.y, z1.x, z1.y);
+            if (imag_only) {
+              const int byte = (j0 + q) * 4;     // two floats = 8 B: half a 16-B granule
+              const int gsn = (byte >> 4) ^ swz;
+              *reinterpret_cast<float2*>(row + gsn * 16 + (byte & 15)) = make_float2(z0.y, z1.y);
+            } else {
+              const int gsn = ((j0 + q) >> 1) ^ swz;
+              *reinterpret_cast<float4*>(row + gsn * 16) = make_float4(z0.x, z0.y, z1.x, z1.y);
+            }
           }
+        };
+        if (nq >= 8) {
+          for (int j0 = 0; j0 < nq; j0 += 8) {   // 8 channels = 16 TMEM columns per tcgen05.ld
+            float v[16];
+            tc::tmem_ld16(tb + 2 * j0, v);
+            emit(v, j0, 8);
+          }
+        } else {                                 // 4 channels = 8 TMEM columns
+          float v[16];
+          tc::tmem_ld8(tb, v);
+          emit(v, 0, 4);
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&acc_empty[b]);
-        const int c0 = ch * g.nch + half * nq;
-        const int nvalid = min(nq, M - c0);
-        if (p < n && nvalid > 0) {
-          const uint32_t es = imag_only ? 4u : 8u;
-          unsigned char* gdst = reinterpret_cast<unsigned char*>(out) + ((size_t)p * M + c0) * es;
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-                       "r"(tc::smem_u32(slot)), "r"((uint32_t)nvalid * es)
-                       : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        if (issuer) {
+          const int c0 = ch * g.nch + half * nq;
+          const int x = imag_only ? c0 : 2 * c0;
+          tma::store_2d(&tmap_out, tc::smem_u32(box), x, (int)(t * RTM));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  } else if (warp == 12 && lane == 0) {
-    // ------------------------------------------------------------ B loader + MMA issue
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp == 4 + RT_EPI / 32) {
+    // ------------------------------------------------------------ B loader + MMA issue (whole warp runs
+    // the loop; one elected lane issues -- descriptors stay in uniform registers)
     const uint32_t idesc = tc::make_idesc_tf32(RTM, g.N, false, false);
-    const uint32_t sa_hi = tc::smem_u32(a_hi), sa_lo = tc::smem_u32(a_lo), sb = tc::smem_u32(bst);
-    uint32_t a_ph = 0, bf_ph[2] = {0, 0}, be_ph[2] = {0, 0}, ae_ph[4] = {0, 0, 0, 0};
+    const uint32_t sb = tc::smem_u32(bst);
+    const uint64_t dah0 = tc::make_sdesc(tc::smem_u32(a_hi), A_LBO, g.a_sbo);
+    const uint64_t dal0 = tc::make_sdesc(tc::smem_u32(a_lo), A_LBO, g.a_sbo);
+    const uint64_t db00 = tc::make_sdesc(sb, B_LBO, g.b_sbo);
+    uint32_t a_ph = 0, bf_ph = 0, be_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
     int64_t gq = 0;
     const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t total = my_tiles * g.nchunks;
-    if (total > 0) bulk_g2s(sb, bimg, g.b_stage, &b_full[0]);
+    const int nks = g.kr / 8;
+    auto load_b = [&](int64_t q) {   // chunk sequence position q -> stage q % RT_BST
+      const int s1 = (int)(q % RT_BST);
+      if (q >= RT_BST) { tc::mbar_wait(&b_empty[s1], (be_ph >> s1) & 1); be_ph ^= 1u << s1; }
+      const int ch1 = (int)(q % g.nchunks);
+      if (tc::elect_one())
+        bulk_g2s(sb + s1 * g.b_stage, reinterpret_cast<const unsigned char*>(bimg) + (size_t)ch1 * g.b_stage, g.b_stage,
+                 &b_full[s1]);
+      __syncwarp();
+    };
+    for (int64_t q = 0; q < RT_BST - 1 && q < total; ++q) load_b(q);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       tc::mbar_wait(a_full, a_ph);
       a_ph ^= 1;
       tc::tc_fence_after();
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
-        // prefetch the next chunk's B into the other stage (its previous MMAs must be done)
-        if (gq + 1 < total) {
-          const int s1 = (int)((gq + 1) & 1);
-          if (gq >= 1) { tc::mbar_wait(&b_empty[s1], be_ph[s1]); be_ph[s1] ^= 1; }
-          const int ch1 = (int)((gq + 1) % g.nchunks);
-          bulk_g2s(sb + s1 * g.b_stage, reinterpret_cast<const unsigned char*>(bimg) + (size_t)ch1 * g.b_stage,
-                   g.b_stage, &b_full[s1]);
-        }
-        const int s = (int)(gq & 1);
-        tc::mbar_wait(&b_full[s], bf_ph[s]);
-        bf_ph[s] ^= 1;
+        if (gq + RT_BST - 1 < total) load_b(gq + RT_BST - 1);   // its stage was used by chunk gq - 1
+        const int s = (int)(gq % RT_BST);
+        tc::mbar_wait(&b_full[s], (bf_ph >> s) & 1);
+        bf_ph ^= 1u << s;
         const int b = (int)(gq & 3);
         if (gq >= 4) { tc::mbar_wait(&acc_empty[b], ae_ph[b]); ae_ph[b] ^= 1; }
         tc::tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * g.N);
-        const uint32_t bh = sb + s * g.b_stage, bl = bh + g.b_part;
-        for (int ks = 0; ks < g.kr / 8; ++ks) {
-          const uint64_t dah = tc::make_sdesc(sa_hi + ks * 2 * A_LBO, A_LBO, g.a_sbo);
-          const uint64_t dal = tc::make_sdesc(sa_lo + ks * 2 * A_LBO, A_LBO, g.a_sbo);
-          const uint64_t dbh = tc::make_sdesc(bh + ks * 2 * B_LBO, B_LBO, g.b_sbo);
-          const uint64_t dbl = tc::make_sdesc(bl + ks * 2 * B_LBO, B_LBO, g.b_sbo);
-          tc::mma_tf32(d, dal, dbh, idesc, ks > 0 ? 1u : 0u);
-          tc::mma_tf32(d, dah, dbl, idesc, 1u);
-          tc::mma_tf32(d, dah, dbh, idesc, 1u);
+        const uint64_t dbh0 = tc::sdesc_add(db00, (uint32_t)(s * g.b_stage));
+        const uint64_t dbl0 = tc::sdesc_add(dbh0, (uint32_t)g.b_part);
+        if (tc::elect_one()) {
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint32_t o = ks * 2 * A_LBO;   // A_LBO == B_LBO
+            tc::mma_tf32(d, tc::sdesc_add(dal0, o), tc::sdesc_add(dbh0, o), idesc, ks > 0 ? 1u : 0u);
+            tc::mma_tf32(d, tc::sdesc_add(dah0, o), tc::sdesc_add(dbl0, o), idesc, 1u);
+            tc::mma_tf32(d, tc::sdesc_add(dah0, o), tc::sdesc_add(dbh0, o), idesc, 1u);
+          }
+          tc::mma_commit(&b_empty[s]);
+          tc::mma_commit(&acc_full[b]);
         }
-        tc::mma_commit(&b_empty[s]);
-        tc::mma_commit(&acc_full[b]);
+        __syncwarp();
       }
-      tc::mma_commit(a_empty);
+      if (tc::elect_one()) tc::mma_commit(a_empty);
+      __syncwarp();
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 12) tc::tmem_dealloc(tmem, 512);
+  if (warp == 4 + RT_EPI / 32) tc::tmem_dealloc(tmem, 512);
 }
 
 // B image: per chunk ch, part (hi, lo), row r (= 2*local channel + {amp, ph}), K index i.
@@ -236,9 +278,10 @@ __global__ void build_bimg_kernel(const float* __restrict__ Bi, int k, int M, fl
   }
 }
 
-size_t rt_smem(int k, int M) {
+size_t rt_smem(int k, int M, int RT_BST) {
   const RtGeom g = rt_geom(k, M);
-  return (size_t)2 * g.a_bytes + 2 * (size_t)g.b_stage + 2 * 256 * SLOT + 16 * 8 + 64;
+  return (size_t)RT_NBUF * RT_PARTS * rt_box_region(g) + 2 * (size_t)g.a_bytes + RT_BST * (size_t)g.b_stage + 16 * 8 + 64 +
+         1024;
 }
 
 }  // namespace
@@ -256,15 +299,22 @@ void launch_build_bimg(const float* Bi, int k, int M, float* bimg, cudaStream_t 
 void launch_reconstruct_tc(const float* US, int64_t n, int k, int ldus, const float* bimg, int M, void* out,
                            int out_imag_only, cudaStream_t s) {
   if (n <= 0) return;
-  const size_t smem = rt_smem(k, M);
+  size_t smem = rt_smem(k, M, 3);
+  const int bst = smem <= 227 * 1024 ? 3 : 2;
+  if (bst == 2) smem = rt_smem(k, M, 2);
   if (smem > 227 * 1024) throw Status(10, "reconstruct_tc: k too large for the smem tile");
-  FKK_CUDA_CHECK(cudaFuncSetAttribute(reconstruct_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = bst == 3 ? reconstruct_tc_kernel<3> : reconstruct_tc_kernel<2>;
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t ntiles = (n + RTM - 1) / RTM;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
-  reconstruct_tc_kernel<<<grid, RT_THREADS, smem, s>>>(US, n, k, ldus, bimg, M, out, out_imag_only);
+  const RtGeom g = rt_geom(k, M);
+  const int rb = rt_row_bytes(g, out_imag_only);
+  const uint64_t cols = out_imag_only ? (uint64_t)M : 2 * (uint64_t)M;
+  const CUtensorMap tm = tma::make_2d_f32(out, (uint64_t)n, cols, cols * 4, RTM, rb / 4, rb);
+  kern<<<grid, RT_THREADS, smem, s>>>(US, n, k, ldus, bimg, M, tm, out_imag_only);
   check_launch("reconstruct_tc");
 }
 
