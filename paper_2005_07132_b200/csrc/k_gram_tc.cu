@@ -70,10 +70,10 @@ __device__ __forceinline__ void store_block(const float4 (&x)[4], unsigned char*
     const float v2 = e == 0 ? x[2].x : e == 1 ? x[2].y : e == 2 ? x[2].z : x[2].w;
     const float v3 = e == 0 ? x[3].x : e == 1 ? x[3].y : e == 2 ? x[3].z : x[3].w;
     float4 h, l;
-    tc::split_tf32(v0, h.x, l.x);
-    tc::split_tf32(v1, h.y, l.y);
-    tc::split_tf32(v2, h.z, l.z);
-    tc::split_tf32(v3, h.w, l.w);
+    tc::split_fast(v0, h.x, l.x);
+    tc::split_fast(v1, h.y, l.y);
+    tc::split_fast(v2, h.z, l.z);
+    tc::split_fast(v3, h.w, l.w);
     *reinterpret_cast<float4*>(hi_base + off) = h;
     *reinterpret_cast<float4*>(lo_base + off) = l;
   }

@@ -217,20 +217,33 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
     const int WB = pb_stage(kp), WP = pb_part(kp);
     const uint64_t da0 = tc::make_sdesc(sbase, PA_LBO, PA_SBO);
     const uint64_t dw0 = tc::make_sdesc(sbase + 2 * PA_BYTES, PB_LBO, PB_SBO);
+    // W stage copies run PSTAGES - 1 positions ahead of the MMAs (their L2 latency is not exposed):
+    // position q (tile-major, stage-minor) uses slot q % PSTAGES; its W copy is issued once the slot's
+    // previous MMAs (position q - PSTAGES) have completed.
+    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t npos = my_tiles * nst;
+    uint32_t wph = 0;                                     // bit s: empty-phase of slot s for the W issuer
+    auto issue_w = [&](int64_t q) {
+      const int sl = (int)(q % PSTAGES);
+      if (q >= PSTAGES) tc::mbar_wait(&empty[sl], ((wph >> sl) & 1) ^ 1);
+      wph ^= 1u << sl;
+      const int stq = (int)(q % nst);
+      if (tc::elect_one())
+        bulk_g2s(sbase + sl * SB + 2 * PA_BYTES, reinterpret_cast<const unsigned char*>(wimg) + (size_t)stq * WB, WB,
+                 &full[sl]);
+      __syncwarp();
+    };
+    for (int64_t q = 0; q < PSTAGES - 1 && q < npos; ++q) issue_w(q);
     int stage = 0;
     uint32_t phase = 0, ae[2] = {0, 0};
-    int64_t it = 0;
+    int64_t it = 0, pos = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = (int)(it % nbuf);
       if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], ae[b]); ae[b] ^= 1; tc::tc_fence_after(); }
       const uint32_t dset = tmem + (uint32_t)(b * setc);
       const uint32_t dx = dset + nseg * kp;
-      for (int st = 0; st < nst; ++st) {
-        tc::mbar_wait(&empty[stage], phase ^ 1);          // slot free (also for the W copy)
-        const uint32_t sa = sbase + stage * SB;
-        if (tc::elect_one())
-          bulk_g2s(sa + 2 * PA_BYTES, reinterpret_cast<const unsigned char*>(wimg) + (size_t)st * WB, WB, &full[stage]);
-        __syncwarp();
+      for (int st = 0; st < nst; ++st, ++pos) {
+        if (pos + PSTAGES - 1 < npos) issue_w(pos + PSTAGES - 1);
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
         const uint64_t dah = tc::sdesc_add(da0, (uint32_t)(stage * SB)), dal = tc::sdesc_add(dah, PA_BYTES);

@@ -135,11 +135,19 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
   lo = tf32_rna(x - hi);
 }
+// Hot-loop split (reading A22): hi = tf32 round-to-nearest-away of x done with two integer ops
+// (identical to cvt.rna.tf32 for finite |x| < 2^127; non-finite inputs are rejected upstream), lo =
+// x - hi exactly in fp32, handed to the tensor core as fp32 (it reads the top 19 bits: lo is
+// truncated to tf32, a 2^-11 relative error on a term that is itself 2^-11 of x).
+__device__ __forceinline__ void split_fast(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  lo = x - hi;
+}
 __device__ __forceinline__ void split4(const float4 v, float4& hi, float4& lo) {
-  split_tf32(v.x, hi.x, lo.x);
-  split_tf32(v.y, hi.y, lo.y);
-  split_tf32(v.z, hi.z, lo.z);
-  split_tf32(v.w, hi.w, lo.w);
+  split_fast(v.x, hi.x, lo.x);
+  split_fast(v.y, hi.y, lo.y);
+  split_fast(v.z, hi.z, lo.z);
+  split_fast(v.w, hi.w, lo.w);
 }
 
 }  // namespace tc
