@@ -32,6 +32,15 @@ __device__ __forceinline__ double rcp64a(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
+// one Newton step on the MUFU seed (~2^-44 relative): the LDL^T pivots of the ALS recurrence --
+// a 1e-13 relative perturbation of the factorisation, far below the 1e-5 direct-KK tolerance
+// (the second step was on the recurrence's critical path)
+__device__ __forceinline__ double rcp64n1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 
 // band of lam D^T D (second differences): diagonal d0, first off-diagonal d1 (coupling i, i+1)
 __device__ __forceinline__ double d0v(int i, int M) {
@@ -121,14 +130,19 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
       double gf1 = 0.0, gf2 = 0.0, ga1 = 0.0, ga2 = 0.0, gb1 = 0.0, gb2 = 0.0;
       double Caa = 0.0, Cab = 0.0, Cbb = 0.0, Cfa = 0.0, Cfb = 0.0;
       const double ea0 = hasN ? cpl(i0, na, M, lam) : 0.0, eb0 = hasN ? lam : 0.0, ea1 = hasN ? lam : 0.0;
+      using T_ = std::true_type;
+      using F_ = std::false_type;
       auto passA = [&](auto bsub_c, auto fact_c) {
         constexpr bool BSUB = decltype(bsub_c)::value, FACT = decltype(fact_c)::value;
         int ix = ix0, i = i0;
-        for (int t = 0; t < nn; ++t, ix += dix, i += di) {
+        // one row in elimination order; ea/eb = near-spike entries (t < 2), LASTROW: l1 = 0
+        auto step = [&](auto last_c, double ea, double eb) {
+          constexpr bool LASTROW = decltype(last_c)::value;
           const double yv = (double)sy[ix];
           double wv = 1.0;
           if constexpr (BSUB) {
-            // previous order: this row's l1 / l2 couple to the rows visited just before (z1, z2)
+            // previous order: this row's l1 / l2 couple to the rows visited just before (z1, z2;
+            // both zero at the first rows, where the stored l1 is zero too)
             const double zv = sg[ix] - sl1[ix] * z1 - lam * srd[ix] * z2;
             z2 = z1;
             z1 = zv;
@@ -139,12 +153,11 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
             double ld0 = lam6, ld1 = lamm4;
             if (edge) { ld0 = lam * d0v(i, M); ld1 = lam * d1v(dr ? i - 1 : i, M); }
             const double D = (wv + ld0) - L1m1 * L1m1 * Dm1 - lam2 * rDm2;
-            const double rd = rcp64a(D);
-            const double l1n = t + 1 < nn ? (ld1 - lam * L1m1) * rd : 0.0;
+            const double rd = rcp64n1(D);
+            const double l1n = LASTROW ? 0.0 : (ld1 - lam * L1m1) * rd;
             const double L2m2 = lam * rDm2;
             const double gf = wv * yv - L1m1 * gf1 - L2m2 * gf2;
-            double ga = -L1m1 * ga1 - L2m2 * ga2, gb = -L1m1 * gb1 - L2m2 * gb2;
-            if (t < 2) { ga += t == 0 ? ea0 : ea1; gb += t == 0 ? eb0 : 0.0; }
+            const double ga = ea - L1m1 * ga1 - L2m2 * ga2, gb = eb - L1m1 * gb1 - L2m2 * gb2;
             const double ua = ga * rd, ub = gb * rd;
             Caa = fma(ga, ua, Caa);
             Cab = fma(ga, ub, Cab);
@@ -163,10 +176,17 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
             ga2 = ga1; ga1 = ga;
             gb2 = gb1; gb1 = gb;
           }
-        }
+          ix += dix;
+          i += di;
+        };
+        if (nn == 0) return;                      // lanes beyond the P segments
+        step(F_{}, ea0, eb0);                     // t = 0   (nn >= 2 on active lanes)
+        if (nn == 2) { step(T_{}, ea1, 0.0); return; }
+        step(F_{}, ea1, 0.0);                     // t = 1
+#pragma unroll 2
+        for (int t = 2; t < nn - 1; ++t) step(F_{}, 0.0, 0.0);
+        step(T_{}, 0.0, 0.0);                     // t = nn - 1
       };
-      using T_ = std::true_type;
-      using F_ = std::false_type;
       if (it == 0) passA(F_{}, T_{});
       else if (it < iters) passA(T_{}, T_{});
       else { passA(T_{}, F_{}); break; }
@@ -276,23 +296,37 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
         const int r_last = dr ? b : b + nn - 1;
         const double c0 = cpl(i0, na, M, lam) * x_na + lam * x_nf, c1 = lam * x_na;
         const double cL = cpl(r_last, fa, M, lam) * x_fa + lam * x_ff, cL2 = lam * x_fa;
-        double g1 = 0.0, g2 = 0.0, l1prev = 0.0, rdm1 = 0.0, rdm2 = 0.0;
-        const bool first = it == 0;
-        int ix = ix0;
-        for (int t = 0; t < nn; ++t, ix += dix) {
-          const double wv = first ? 1.0 : (sw[ix] ? p : q);
-          double f = wv * (double)sy[ix];
-          if (t < 2) f -= t == 0 ? c0 : c1;
-          if (t >= nn - 2) f -= t == nn - 1 ? cL : cL2;
-          const double rd = srd[ix];
-          const double g = f - l1prev * g1 - lam * rdm2 * g2;
-          sg[ix] = g * rd;
-          g2 = g1;
-          g1 = g;
-          l1prev = sl1[ix];
-          rdm2 = rdm1;
-          rdm1 = rd;
-        }
+        auto passB = [&](auto first_c) {
+          constexpr bool FIRST = decltype(first_c)::value;
+          double g1 = 0.0, g2 = 0.0, l1prev = 0.0, rdm1 = 0.0, rdm2 = 0.0;
+          int ix = ix0;
+          auto stepB = [&](double corr) {
+            const double wv = FIRST ? 1.0 : (sw[ix] ? p : q);
+            const double f = wv * (double)sy[ix] - corr;
+            const double rd = srd[ix];
+            const double g = f - l1prev * g1 - lam * rdm2 * g2;
+            sg[ix] = g * rd;
+            g2 = g1;
+            g1 = g;
+            l1prev = sl1[ix];
+            rdm2 = rdm1;
+            rdm1 = rd;
+            ix += dix;
+          };
+          if (nn < 5) {
+            for (int t = 0; t < nn; ++t)
+              stepB((t == 0 ? c0 : 0.0) + (t == 1 ? c1 : 0.0) + (t == nn - 2 ? cL2 : 0.0) + (t == nn - 1 ? cL : 0.0));
+          } else {
+            stepB(c0);
+            stepB(c1);
+#pragma unroll 2
+            for (int t = 2; t < nn - 2; ++t) stepB(0.0);
+            stepB(cL2);
+            stepB(cL);
+          }
+        };
+        if (it == 0) passB(T_{});
+        else passB(F_{});
       }
     }
     // ---------------- write z (interior from the last back-substitution, separators from the last solve)
