@@ -12,6 +12,7 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "../../include/fkk.h"
 #include "fkk_internal.h"
@@ -141,6 +142,7 @@ struct fkk_plan {
   int2* gtc_tiles = nullptr;
   int* gtc_tile_of = nullptr;
   int gtc_ntiles = 0, gtc_nTj = 0, gtc_nsplit = 0;
+  bool gtc_pair = false;           // 256 x 256 tiles on CTA pairs (k_gram_tc2.cu); default 128 x 128 (k_gram_tc.cu)
   double* gtc_part = nullptr;
   // direct path (lazy)
   int64_t direct_batch = 0;
@@ -300,14 +302,20 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   if (d->gemm_impl == FKK_GEMM_3XTF32) {
     std::vector<int2> tl;
     std::vector<int> tof;
-    fkk::gram_tc_tiles(M, tl, tof, p->gtc_nTj);
+    // CTA-pair Gram: correct but measured slower at cfg3 (7.9 vs 6.1 ms: its producers are still
+    // global-load-latency bound); opt-in for measurements only
+    const char* pair = getenv("FKK_GRAM_PAIR");
+    p->gtc_pair = pair && pair[0] == '1';
+    if (p->gtc_pair) fkk::gram_tc2_tiles(M, tl, tof, p->gtc_nTj);
+    else fkk::gram_tc_tiles(M, tl, tof, p->gtc_nTj);
     p->gtc_ntiles = (int)tl.size();
-    p->gtc_nsplit = fkk::gram_tc_splits(p->gtc_ntiles, n);
+    p->gtc_nsplit = p->gtc_pair ? fkk::gram_tc2_splits(p->gtc_ntiles, n) : fkk::gram_tc_splits(p->gtc_ntiles, n);
     p->gtc_tiles = dalloc<int2>(tl.size());
     p->gtc_tile_of = dalloc<int>(tof.size());
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tile_of, tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
-    p->gtc_part = dalloc<double>(fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
+    p->gtc_part = dalloc<double>(p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
+                                             : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
   } else {
     p->gram_nsplit_cap = fkk::gram_num_splits(n, M);
     p->gram_part = dalloc<double>((size_t)p->gram_nsplit_cap * fkk::gram_num_tiles(M) * 128 * 128);
@@ -401,9 +409,16 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
     if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
-      const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, std::max<int64_t>(r1 - r0, 1)));
-      fkk::launch_gram_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
-      fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      const int64_t nr = std::max<int64_t>(r1 - r0, 1);
+      if (p->gtc_pair) {
+        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
+        fkk::launch_gram_tc2(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+        fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      } else {
+        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
+        fkk::launch_gram_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+        fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      }
     } else {
       const int ns = std::min(p->gram_nsplit_cap, fkk::gram_num_splits(std::max<int64_t>(r1 - r0, 1), M));
       fkk::launch_gram_simt(p->A + r0 * (int64_t)M, r1 - r0, M, p->gram_part, ns, s);

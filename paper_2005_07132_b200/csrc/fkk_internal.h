@@ -80,6 +80,14 @@ void launch_gram_tc(const float* A, int64_t n, int M, const int2* d_tiles, int n
                     cudaStream_t s);
 void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nTj,
                            double* G, int accumulate, cudaStream_t s);
+// tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.
+void gram_tc2_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nT);
+int gram_tc2_splits(int ntiles, int64_t n);
+size_t gram_tc2_partial_doubles(int ntiles, int nsplit);
+void launch_gram_tc2(const float* A, int64_t n, int M, const int2* d_tiles, int ntiles, int nsplit, double* partials,
+                     cudaStream_t s);
+void launch_gram_tc2_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nT,
+                            double* G, int accumulate, cudaStream_t s);
 // Projection US = A0 W (k_project.cu) with per-block column extremes [blk][c][2].
 int project_num_blocks(int64_t n);
 void launch_project_simt(const float* A, int64_t n, int M, const float* W, int k, int kp, float* US, float* ext_val,

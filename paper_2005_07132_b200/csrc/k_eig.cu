@@ -923,8 +923,11 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (eig_path_rows_resident(M)) {
-    // row-resident cooperative tridiagonalisation (G is read, never copied); LL packet exchange
-    const size_t smem = tridiag_rows_smem(M, sms);
+    // row-resident cooperative tridiagonalisation (G is read, never copied); one grid barrier per column
+    int nct = sms;
+    if (const char* ev = getenv("FKK_TRIDIAG_CTAS")) nct = std::max(1, std::min(sms, atoi(ev)));   // A/B only
+    while (nct > 1 && tridiag_rows_smem(M, nct) > 227 * 1024) ++nct;
+    const size_t smem = tridiag_rows_smem(M, nct);
     FKK_CUDA_CHECK(cudaFuncSetAttribute(tridiag_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_rows_kernel, kTsThreads, smem));
@@ -934,7 +937,7 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     int Mi = M;
     const double* Gc = G;
     void* args[] = {&Gc, &A, &Mi, &d, &e, &tau, &pg, &ctr};
-    FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_rows_kernel, dim3(sms), dim3(kTsThreads), args, smem, s));
+    FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_rows_kernel, dim3(nct), dim3(kTsThreads), args, smem, s));
     count_launch();
   } else {
     FKK_CUDA_CHECK(cudaMemcpyAsync(A, G, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
