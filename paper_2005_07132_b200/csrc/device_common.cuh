@@ -103,6 +103,128 @@ __device__ __forceinline__ void hilbert_pair_inplace(cplx<T>* x, const cplx<T>* 
   ifft_dit_inplace<T>(x, tw, L, log2L);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Stockham autosort FFT, radix 8 (last pass radix 4 or 2), one CTA, in place: each pass loads all of
+// a butterfly's R inputs into registers, barriers, and writes the R outputs (natural order in and
+// out).  Versus the radix-2 loop above: log8 instead of log2 passes over shared memory and two
+// barriers per pass.  tw[t] = exp(-2 pi i t / L) for t < L/2 (tw[t + L/2] = -tw[t]).
+template <typename T>
+__device__ __forceinline__ cplx<T> cmul(cplx<T> a, cplx<T> b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> tw_at(const cplx<T>* tw, int t, int L, bool inv) {
+  const int h = L >> 1;
+  cplx<T> w = tw[t < h ? t : t - h];
+  if (t >= h) { w.x = -w.x; w.y = -w.y; }
+  if (inv) w.y = -w.y;
+  return w;
+}
+// in-register DFT of size R in {2, 4, 8}; forward uses exp(-2 pi i / R), inverse exp(+2 pi i / R)
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void dft_small(cplx<T>* v) {
+  auto mul_mi = [](cplx<T> a) -> cplx<T> { return INV ? cplx<T>{-a.y, a.x} : cplx<T>{a.y, -a.x}; };  // * -i (fwd)
+  if constexpr (R == 2) {
+    const cplx<T> a = v[0], b = v[1];
+    v[0] = {a.x + b.x, a.y + b.y};
+    v[1] = {a.x - b.x, a.y - b.y};
+  } else if constexpr (R == 4) {
+    const cplx<T> t0 = {v[0].x + v[2].x, v[0].y + v[2].y}, t1 = {v[0].x - v[2].x, v[0].y - v[2].y};
+    const cplx<T> t2 = {v[1].x + v[3].x, v[1].y + v[3].y};
+    const cplx<T> t3 = mul_mi(cplx<T>{v[1].x - v[3].x, v[1].y - v[3].y});
+    v[0] = {t0.x + t2.x, t0.y + t2.y};
+    v[2] = {t0.x - t2.x, t0.y - t2.y};
+    v[1] = {t1.x + t3.x, t1.y + t3.y};
+    v[3] = {t1.x - t3.x, t1.y - t3.y};
+  } else {
+    cplx<T> e[4], o[4];
+    e[0] = v[0]; e[1] = v[2]; e[2] = v[4]; e[3] = v[6];
+    o[0] = v[1]; o[1] = v[3]; o[2] = v[5]; o[3] = v[7];
+    dft_small<T, 4, INV>(e);
+    dft_small<T, 4, INV>(o);
+    const T s = (T)0.70710678118654752440;
+    // w8^k, k = 0..3 (forward: exp(-i pi k / 4))
+    const cplx<T> o1 = INV ? cplx<T>{s * (o[1].x - o[1].y), s * (o[1].x + o[1].y)}
+                           : cplx<T>{s * (o[1].x + o[1].y), s * (o[1].y - o[1].x)};
+    const cplx<T> o2 = mul_mi(o[2]);
+    const cplx<T> o3 = INV ? cplx<T>{-s * (o[3].x + o[3].y), s * (o[3].x - o[3].y)}
+                           : cplx<T>{s * (o[3].y - o[3].x), -s * (o[3].x + o[3].y)};
+    v[0] = {e[0].x + o[0].x, e[0].y + o[0].y};
+    v[4] = {e[0].x - o[0].x, e[0].y - o[0].y};
+    v[1] = {e[1].x + o1.x, e[1].y + o1.y};
+    v[5] = {e[1].x - o1.x, e[1].y - o1.y};
+    v[2] = {e[2].x + o2.x, e[2].y + o2.y};
+    v[6] = {e[2].x - o2.x, e[2].y - o2.y};
+    v[3] = {e[3].x + o3.x, e[3].y + o3.y};
+    v[7] = {e[3].x - o3.x, e[3].y - o3.y};
+  }
+}
+// one Stockham pass of radix R with current sub-transform size Ns (L / R butterflies)
+template <typename T, int R, bool INV, int MAXB>
+__device__ __forceinline__ void stockham_pass(cplx<T>* x, const cplx<T>* tw, int L, int Ns) {
+  // MAXB radix-8 butterflies (8 MAXB values) per thread: L <= 8 MAXB blockDim; a radix-4 / radix-2
+  // pass gives each thread 8 / R butterflies so it holds the same 8 MAXB values
+  constexpr int NBT = MAXB * (8 / R);
+  const int nb = L / R;
+  cplx<T> v[NBT][R];
+  int jj[NBT];
+#pragma unroll
+  for (int u = 0; u < NBT; ++u) {
+    const int j = threadIdx.x + u * blockDim.x;
+    jj[u] = j;
+    if (j < nb) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[u][r] = x[j + r * nb];
+      const int k = j % Ns;
+      if (Ns > 1) {
+        const int step = (L / (Ns * R)) * k;
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], tw_at(tw, r * step, L, INV));
+      }
+      dft_small<T, R, INV>(v[u]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < NBT; ++u) {
+    const int j = jj[u];
+    if (j < nb) {
+      const int k = j % Ns;
+      const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[base + r * Ns] = v[u][r];
+    }
+  }
+  __syncthreads();
+}
+template <typename T, bool INV, int MAXB>
+__device__ __forceinline__ void stockham_fft(cplx<T>* x, const cplx<T>* tw, int L, int log2L) {
+  int Ns = 1, rem = log2L;
+  while (rem >= 3) { stockham_pass<T, 8, INV, MAXB>(x, tw, L, Ns); Ns *= 8; rem -= 3; }
+  if (rem == 2) stockham_pass<T, 4, INV, MAXB>(x, tw, L, Ns);
+  else if (rem == 1) stockham_pass<T, 2, INV, MAXB>(x, tw, L, Ns);
+}
+// Hilbert multiplier in natural order: f in (0, L/2) -> -i, f in (L/2, L) -> +i, f in {0, L/2} -> 0
+template <typename T>
+__device__ __forceinline__ void hilbert_multiplier_natural(cplx<T>* x, int L) {
+  for (int f = threadIdx.x; f < L; f += blockDim.x) {
+    const cplx<T> v = x[f];
+    cplx<T> o;
+    if (f == 0 || f == (L >> 1)) { o.x = 0; o.y = 0; }
+    else if (f < (L >> 1)) { o.x = v.y; o.y = -v.x; }   // * (-i)
+    else { o.x = -v.y; o.y = v.x; }                      // * (+i)
+    x[f] = o;
+  }
+  __syncthreads();
+}
+// H{r0} + i H{r1} in x[pl .. pl+M) (unnormalised: the caller scales by 1/L); requires L <= 8 MAXB blockDim
+template <typename T, int MAXB>
+__device__ __forceinline__ void hilbert_pair_stockham(cplx<T>* x, const cplx<T>* tw, int L, int log2L) {
+  stockham_fft<T, false, MAXB>(x, tw, L, log2L);
+  hilbert_multiplier_natural<T>(x, L);
+  stockham_fft<T, true, MAXB>(x, tw, L, log2L);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

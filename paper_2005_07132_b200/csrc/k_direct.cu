@@ -40,8 +40,8 @@ __device__ __forceinline__ double rcp64(double x) {
   return fma(r, e, r);
 }
 
-template <typename TIn>
-__global__ void __launch_bounds__(kDirectThreads)
+template <typename TIn, int MAXB>
+__global__ void __launch_bounds__(kDirectThreads, 2)
 direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
                     const double* __restrict__ ref64, float floor, int L, int log2L, int pad_zero,
                     const float2* __restrict__ tw_g, float* __restrict__ phi, int* __restrict__ flags) {
@@ -74,7 +74,7 @@ direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __
     }
     __syncthreads();
     pad_pair<float, float>(x, a0, a1, M, L, pad_zero);
-    hilbert_pair_inplace<float>(x, tw, L, log2L);
+    hilbert_pair_stockham<float, MAXB>(x, tw, L, log2L);
     float* p0 = phi + r0 * (int64_t)M;
     float* p1 = phi + r1 * (int64_t)M;
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(32) als_rows_smem_kernel(const TY* __restrict_
   for (int i = lane; i < M; i += 32) z[(int64_t)row * M + i] = (TZ)yv[i];
 }
 
-template <typename TIn>
-__global__ void __launch_bounds__(kDirectThreads)
+template <typename TIn, int MAXB>
+__global__ void __launch_bounds__(kDirectThreads, 2)
 direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
                      const double* __restrict__ ref64, float floor, int L, int log2L, int pad_zero,
                      const float2* __restrict__ tw_g, const float* __restrict__ phi,
@@ -285,7 +285,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       a1[j] = has1 ? log_ratio_elem<TIn>(I[r1 * (int64_t)M + j], inv_ref[j], ref64[j], floor) : 0.f;
     }
     pad_pair<float, float>(x, e0, e1, M, L, pad_zero);   // (syncs)
-    hilbert_pair_inplace<float>(x, tw, L, log2L);
+    hilbert_pair_stockham<float, MAXB>(x, tw, L, log2L);
     for (int r = 0; r < 2; ++r) {
       if (r == 1 && !has1) break;
       const int64_t row = r0 + r;
@@ -351,14 +351,18 @@ void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const floa
   if (n <= 0) return;
   const size_t smem = (size_t)(L / 2 + L) * sizeof(float2) + 2 * (size_t)M * sizeof(float);
   const int grid = grid_for((n + 1) / 2, 6);
+  const bool big = L > 8 * kDirectThreads;
+  if (L > 16 * kDirectThreads) throw Status(11, "direct path: FFT length above 4096");
+  auto launch = [&](auto kf, const auto* in) {
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kf<<<grid, kDirectThreads, smem, s>>>(in, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw, phi, flags);
+  };
   if (in_f64) {
-    auto k = direct_phase_kernel<double>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, kDirectThreads, smem, s>>>((const double*)I, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw, phi, flags);
+    if (big) launch(direct_phase_kernel<double, 2>, (const double*)I);
+    else launch(direct_phase_kernel<double, 1>, (const double*)I);
   } else {
-    auto k = direct_phase_kernel<float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, kDirectThreads, smem, s>>>((const float*)I, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw, phi, flags);
+    if (big) launch(direct_phase_kernel<float, 2>, (const float*)I);
+    else launch(direct_phase_kernel<float, 1>, (const float*)I);
   }
   check_launch("direct_phase");
 }
@@ -409,16 +413,19 @@ void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const flo
   if (n <= 0) return;
   const size_t smem = direct_finish_smem(M, L);
   const int grid = grid_for((n + 1) / 2, 2);
+  const bool big = L > 8 * kDirectThreads;
+  if (L > 16 * kDirectThreads) throw Status(11, "direct path: FFT length above 4096");
+  auto launch = [&](auto kf, const auto* in) {
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kf<<<grid, kDirectThreads, smem, s>>>(in, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw, phi, phierr,
+                                          sg_half, out, out_imag_only);
+  };
   if (in_f64) {
-    auto k = direct_finish_kernel<double>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, kDirectThreads, smem, s>>>((const double*)I, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw,
-                                         phi, phierr, sg_half, out, out_imag_only);
+    if (big) launch(direct_finish_kernel<double, 2>, (const double*)I);
+    else launch(direct_finish_kernel<double, 1>, (const double*)I);
   } else {
-    auto k = direct_finish_kernel<float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, kDirectThreads, smem, s>>>((const float*)I, n, M, inv_ref, ref64, floor, L, ilog2(L), pad_zero, tw,
-                                         phi, phierr, sg_half, out, out_imag_only);
+    if (big) launch(direct_finish_kernel<float, 2>, (const float*)I);
+    else launch(direct_finish_kernel<float, 1>, (const float*)I);
   }
   check_launch("direct_finish");
 }
