@@ -142,7 +142,8 @@ struct fkk_plan {
   int2* gtc_tiles = nullptr;
   int* gtc_tile_of = nullptr;
   int gtc_ntiles = 0, gtc_nTj = 0, gtc_nsplit = 0;
-  bool gtc_pair = false;           // 256 x 256 tiles on CTA pairs (k_gram_tc2.cu); default 128 x 128 (k_gram_tc.cu)
+  bool gtc_pair = false;
+  unsigned char* apre = nullptr;   // pre-split MMA image of A0 (fp32 input, 3xTF32, no loopback shards)           // 256 x 256 tiles on CTA pairs (k_gram_tc2.cu); default 128 x 128 (k_gram_tc.cu)
   double* gtc_part = nullptr;
   // direct path (lazy)
   int64_t direct_batch = 0;
@@ -170,7 +171,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, phi, phierr, als_state, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_state, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
@@ -314,6 +315,9 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     p->gtc_tile_of = dalloc<int>(tof.size());
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tile_of, tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
+    const char* nopre = getenv("FKK_GRAM_NOPRE");   // A/B switch: in-kernel producers instead of the image
+    if (!p->gtc_pair && !d->in_dtype && d->loopback_shards <= 1 && !(nopre && nopre[0] == '1'))
+      p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, M));
     p->gtc_part = dalloc<double>(p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
                                              : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
   } else {
@@ -392,7 +396,12 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   cudaStream_t s = p->stream;
   const int M = p->M, k = p->k;
   fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
-  fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
+  const bool pre = p->apre != nullptr;
+  if (pre)
+    fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->inv_ref, (float)p->d.ratio_floor, p->A,
+                             p->apre, p->flags, s);
+  else
+    fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
   if (p->d.f_mode == FKK_F_EQ9) {
     FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
     fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);
@@ -410,7 +419,11 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
     if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
       const int64_t nr = std::max<int64_t>(r1 - r0, 1);
-      if (p->gtc_pair) {
+      if (pre) {
+        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
+        fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+        fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      } else if (p->gtc_pair) {
         const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
         fkk::launch_gram_tc2(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
         fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);

@@ -80,6 +80,13 @@ void launch_gram_tc(const float* A, int64_t n, int M, const int2* d_tiles, int n
                     cudaStream_t s);
 void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nTj,
                            double* G, int accumulate, cudaStream_t s);
+// Pre-split Gram (k_gram_tc.cu): the log-ratio pass also writes the MMA smem image of A0 (tf32 hi/lo
+// K-major blocks per 128-channel block and 32-pixel stage); the Gram bulk-copies it (no producers).
+size_t gram_pre_bytes(int64_t n, int M);
+void launch_logratio_pre(const float* I, int64_t n, int M, const float* inv_ref, float floor, float* A,
+                         unsigned char* Apre, int* flags, cudaStream_t s);
+void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
+                     double* partials, cudaStream_t s);
 // tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.
 void gram_tc2_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nT);
 int gram_tc2_splits(int ntiles, int64_t n);

@@ -223,6 +223,244 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
   if (warp == 16) tc::tmem_dealloc(tmem, GTMEM_COLS);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Pre-split variant.  The log-ratio pass (F1) also writes A0 in the exact smem image the MMA reads:
+// per 128-channel block cb and 32-pixel stage q, the tf32 hi and lo K-major core-matrix blocks
+// (GOP_BYTES each, padding included) at Apre + ((cb nq + q) 2 + part) GOP_BYTES.  The Gram CTA then
+// needs no producer threads: one loader lane bulk-copies (cp.async.bulk, mbarrier tx) 2 or 4 blocks
+// per stage, so the A0 stream has no register lookahead limit and no transposes on the Gram's SMs.
+// Pixels >= n and channels >= M are zero in the image; split boundaries are stage aligned.
+__global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restrict__ I, int64_t n, int M,
+                                                           const float* __restrict__ inv_ref, float floor,
+                                                           float* __restrict__ A, unsigned char* __restrict__ Apre,
+                                                           int64_t nq, int nT, int* __restrict__ flags) {
+  // the image block (hi + lo, 2 GOP_BYTES) is assembled in shared memory and leaves with ONE bulk
+  // copy (full-line writes); double-buffered; the next item's I loads are issued before this item's
+  // arithmetic (register prefetch)
+  extern __shared__ __align__(128) unsigned char simg[];   // [2][2 GOP_BYTES]
+  const int c4 = threadIdx.x & 31, p4 = threadIdx.x >> 5;
+  int bad = 0;
+  const int64_t items = nq * nT;
+  float4 xn[4];
+  auto load = [&](int64_t it) {
+    const int64_t q = it / nT;
+    const int col = (int)(it - q * nT) * GT + 4 * c4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t px = q * GKC + 4 * p4 + e;
+      xn[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (it < items && px < n && col < M) xn[e] = __ldcs(reinterpret_cast<const float4*>(I + px * (int64_t)M + col));
+    }
+  };
+  load(blockIdx.x);
+  int buf = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, buf ^= 1) {
+    const int64_t q = it / nT;
+    const int cb = (int)(it - q * nT);
+    const int col = cb * GT + 4 * c4;
+    float4 x[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = xn[e];
+    load(it + gridDim.x);
+    float4 ir = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col < M) ir = *reinterpret_cast<const float4*>(inv_ref + col);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t px = q * GKC + 4 * p4 + e;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (px < n && col < M) {
+        const float4 v = x[e];
+        bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+        o.x = 0.5f * logf(fmaxf(v.x * ir.x, floor));     // same arithmetic as logratio_kernel
+        o.y = 0.5f * logf(fmaxf(v.y * ir.y, floor));
+        o.z = 0.5f * logf(fmaxf(v.z * ir.z, floor));
+        o.w = 0.5f * logf(fmaxf(v.w * ir.w, floor));
+        *reinterpret_cast<float4*>(A + px * (int64_t)M + col) = o;
+      }
+      x[e] = o;
+    }
+    // buffer `buf` was last read by the bulk store issued two items ago
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    unsigned char* hi = simg + buf * 2 * GOP_BYTES;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = c4 * 4 + e;
+      const int off = (r >> 3) * GSBO + p4 * GLBO + (r & 7) * 16;
+      const float v0 = e == 0 ? x[0].x : e == 1 ? x[0].y : e == 2 ? x[0].z : x[0].w;
+      const float v1 = e == 0 ? x[1].x : e == 1 ? x[1].y : e == 2 ? x[1].z : x[1].w;
+      const float v2 = e == 0 ? x[2].x : e == 1 ? x[2].y : e == 2 ? x[2].z : x[2].w;
+      const float v3 = e == 0 ? x[3].x : e == 1 ? x[3].y : e == 2 ? x[3].z : x[3].w;
+      float4 h, l;
+      tc::split_fast(v0, h.x, l.x);
+      tc::split_fast(v1, h.y, l.y);
+      tc::split_fast(v2, h.z, l.z);
+      tc::split_fast(v3, h.w, l.w);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(hi + GOP_BYTES + off) = l;
+    }
+    tc::fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned char* dst = Apre + ((size_t)(cb * nq + q) * 2) * GOP_BYTES;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(tc::smem_u32(hi)),
+                   "r"((uint32_t)(2 * GOP_BYTES))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 2);
+}
+
+__device__ __forceinline__ void bulk_g2s_g(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+constexpr int GPTHREADS = 320;   // warps 0-7 epilogue, 8 MMA issue, 9 bulk loader
+
+__global__ void __launch_bounds__(GPTHREADS, 1)
+gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, const int2* __restrict__ tiles,
+                int ntiles, double* __restrict__ partials) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GSTAGES * GSTAGE_BYTES);
+  uint64_t* full = bars;                  // [GSTAGES]  bulk copies (tx) -> MMA
+  uint64_t* empty = bars + GSTAGES;       // [GSTAGES]  MMA commit -> loader
+  uint64_t* acc_full = bars + 2 * GSTAGES;    // [2] MMA commit -> epilogue
+  uint64_t* acc_empty = acc_full + 2;         // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = blockIdx.x % ntiles, split = blockIdx.x / ntiles, nsplit = gridDim.x / ntiles;
+  const int ti = tiles[t].x, tj = tiles[t].y;
+  const bool diag = ti == tj;
+  const int64_t qb = nq * split / nsplit, qe = nq * (split + 1) / nsplit;     // stage range
+  constexpr int SPP = GPERIOD / GKC;                                            // stages per period
+  const int64_t nper = qe > qb ? (qe - qb + SPP - 1) / SPP : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < GSTAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 256); }
+    tc::fence_mbar_init();
+  }
+  if (warp == 8) tc::tmem_alloc(tmem_slot, GTMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 8) {
+    // ------------------------------------------------------------ epilogue (as gram_tc_kernel)
+    const int lg = warp & 3;
+    const int chalf = warp >> 2;
+    const int i = lg * 32 + lane;
+    double* part = partials + (int64_t)blockIdx.x * (GT * GT);   // [j][i]
+    float S[64];
+#pragma unroll
+    for (int q = 0; q < 64; ++q) S[q] = 0.f;
+    uint32_t ph[2] = {0, 0};
+    bool first = true;
+    for (int64_t pidx = 0; pidx < nper; ++pidx) {
+      const int b = (int)(pidx & 1);
+      tc::mbar_wait(&acc_full[b], ph[b]);
+      ph[b] ^= 1;
+      tc::tc_fence_after();
+      const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 64 * chalf);
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        float h[16];
+        tc::tmem_ld16(tb + cb * 16, h);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) S[cb * 16 + q] += h[q];
+        tc::tmem_ld16(tb + 128 + cb * 16, h);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) S[cb * 16 + q] += h[q];
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acc_empty[b]);
+      const bool last = pidx == nper - 1;
+      if (last || ((pidx + 1) * GPERIOD) % GFLUSH == 0) {
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          double* p = part + (int64_t)(64 * chalf + q) * GT + i;
+          *p = (first ? 0.0 : *p) + (double)S[q];
+          S[q] = 0.f;
+        }
+        first = false;
+      }
+    }
+    if (nper == 0)
+      for (int q = 0; q < 64; ++q) part[(int64_t)(64 * chalf + q) * GT + i] = 0.0;
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issue
+    constexpr uint32_t idesc = tc::make_idesc_tf32(GT, GT, false, false);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t eph[2] = {0, 0};
+    const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), GLBO, GSBO);
+    for (int64_t pidx = 0; pidx < nper; ++pidx) {
+      const int b = (int)(pidx & 1);
+      if (pidx >= 2) {
+        tc::mbar_wait(&acc_empty[b], eph[b]);
+        eph[b] ^= 1;
+        tc::tc_fence_after();
+      }
+      const uint32_t d_hi = tmem + 256 * b, d_mid = d_hi + 128;
+      const int64_t q0 = qb + pidx * SPP, q1 = (qe < q0 + SPP) ? qe : (q0 + SPP);
+      uint32_t acc = 0;
+      for (int64_t q = q0; q < q1; ++q) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * GSTAGE_BYTES)), dal = tc::sdesc_add(dah, GOP_BYTES);
+        const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, 2 * GOP_BYTES);
+        const uint64_t dbl = diag ? dal : tc::sdesc_add(dah, 3 * GOP_BYTES);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < GKC / 8; ++ks) {
+            const uint32_t ko = ks * 2 * GLBO;
+            tc::mma_tf32(d_mid, tc::sdesc_add(dal, ko), tc::sdesc_add(dbh, ko), idesc, acc);   // lo_i * hi_j
+            tc::mma_tf32(d_mid, tc::sdesc_add(dah, ko), tc::sdesc_add(dbl, ko), idesc, 1);     // hi_i * lo_j
+            tc::mma_tf32(d_hi, tc::sdesc_add(dah, ko), tc::sdesc_add(dbh, ko), idesc, acc);    // hi_i * hi_j
+            acc = 1;
+          }
+          tc::mma_commit(&empty[stage]);
+        }
+        acc = 1;
+        __syncwarp();
+        if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
+      }
+      if (tc::elect_one()) tc::mma_commit(&acc_full[b]);
+      __syncwarp();
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------ bulk loader (warp 9, one lane)
+    const uint32_t sbase = tc::smem_u32(smem);
+    const uint32_t bytes = (diag ? 2u : 4u) * GOP_BYTES;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t q = qb; q < qe; ++q) {
+      tc::mbar_wait(&empty[stage], phase ^ 1);
+      const uint32_t st = sbase + stage * GSTAGE_BYTES;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[stage])),
+                   "r"(bytes)
+                   : "memory");
+      const unsigned char* a = Apre + ((size_t)(ti * nq + q) * 2) * GOP_BYTES;
+      bulk_g2s_g(st, a, 2 * GOP_BYTES, &full[stage]);                       // A hi, A lo (adjacent)
+      if (!diag) {
+        const unsigned char* bsrc = Apre + ((size_t)(tj * nq + q) * 2) * GOP_BYTES;
+        bulk_g2s_g(st + 2 * GOP_BYTES, bsrc, 2 * GOP_BYTES, &full[stage]);  // B hi, B lo
+      }
+      if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 8) tc::tmem_dealloc(tmem, GTMEM_COLS);
+}
+
 __global__ void gram_tc_reduce_kernel(const double* __restrict__ partials, int ntiles, int nsplit, int M,
                                       const int* __restrict__ tile_of, int nT, double* __restrict__ G, int accumulate) {
   const int64_t total = (int64_t)M * M;
@@ -274,6 +512,40 @@ void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M
                            double* G, int accumulate, cudaStream_t s) {
   gram_tc_reduce_kernel<<<1024, 256, 0, s>>>(partials, ntiles, nsplit, M, d_tile_of, nT, G, accumulate);
   check_launch("gram_tc_reduce");
+}
+
+}  // namespace fkk
+
+namespace fkk {
+
+size_t gram_pre_bytes(int64_t n, int M) {
+  const int64_t nq = (n + GKC - 1) / GKC;
+  const int nT = (M + GT - 1) / GT;
+  return (size_t)nT * nq * 2 * GOP_BYTES;
+}
+
+void launch_logratio_pre(const float* I, int64_t n, int M, const float* inv_ref, float floor, float* A,
+                         unsigned char* Apre, int* flags, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t nq = (n + GKC - 1) / GKC;
+  const int nT = (M + GT - 1) / GT;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = nq * nT;
+  const int grid = (int)std::min<int64_t>(items, (int64_t)sms * 3);
+  const int smem = 4 * GOP_BYTES;
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(logratio_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  logratio_pre_kernel<<<grid, 256, smem, s>>>(I, n, M, inv_ref, floor, A, Apre, nq, nT, flags);
+  check_launch("logratio_pre");
+}
+
+void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
+                     double* partials, cudaStream_t s) {
+  const int64_t nq = (n + GKC - 1) / GKC;
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(gram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM));
+  gram_pre_kernel<<<ntiles * nsplit, GPTHREADS, GSMEM, s>>>(Apre, n, nq, d_tiles, ntiles, partials);
+  check_launch("gram_pre");
 }
 
 }  // namespace fkk
