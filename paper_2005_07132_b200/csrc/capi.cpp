@@ -142,8 +142,13 @@ struct fkk_plan {
   int2* gtc_tiles = nullptr;
   int* gtc_tile_of = nullptr;
   int gtc_ntiles = 0, gtc_nTj = 0, gtc_nsplit = 0;
+  // Gram variants (3xTF32): 0 = 1-CTA 128x128 fed by the pre-split A0 image (default), 1 = CTA pairs
+  // 256x256 fed by the image (same speed at cfg3), 2 = 1-CTA with in-kernel producers (fp64 input /
+  // loopback shards), 3 = CTA pairs with in-kernel producers (measurement only).  FKK_GRAM_MODE overrides.
+  int gram_mode = 0;
   bool gtc_pair = false;
-  unsigned char* apre = nullptr;   // pre-split MMA image of A0 (fp32 input, 3xTF32, no loopback shards)           // 256 x 256 tiles on CTA pairs (k_gram_tc2.cu); default 128 x 128 (k_gram_tc.cu)
+  unsigned char* apre = nullptr;   // pre-split MMA image of A0
+  int apre_blocks = 0;
   double* gtc_part = nullptr;
   // direct path (lazy)
   int64_t direct_batch = 0;
@@ -303,10 +308,11 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   if (d->gemm_impl == FKK_GEMM_3XTF32) {
     std::vector<int2> tl;
     std::vector<int> tof;
-    // CTA-pair Gram: correct but measured slower at cfg3 (7.9 vs 6.1 ms: its producers are still
-    // global-load-latency bound); opt-in for measurements only
-    const char* pair = getenv("FKK_GRAM_PAIR");
-    p->gtc_pair = pair && pair[0] == '1';
+    int mode = 0;
+    if (const char* ev = getenv("FKK_GRAM_MODE")) mode = atoi(ev) & 3;
+    if ((mode == 0 || mode == 1) && (d->in_dtype || d->loopback_shards > 1)) mode = 2;   // image needs fp32, 1 shard
+    p->gram_mode = mode;
+    p->gtc_pair = mode == 1 || mode == 3;
     if (p->gtc_pair) fkk::gram_tc2_tiles(M, tl, tof, p->gtc_nTj);
     else fkk::gram_tc_tiles(M, tl, tof, p->gtc_nTj);
     p->gtc_ntiles = (int)tl.size();
@@ -315,9 +321,10 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     p->gtc_tile_of = dalloc<int>(tof.size());
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tile_of, tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
-    const char* nopre = getenv("FKK_GRAM_NOPRE");   // A/B switch: in-kernel producers instead of the image
-    if (!p->gtc_pair && !d->in_dtype && d->loopback_shards <= 1 && !(nopre && nopre[0] == '1'))
-      p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, M));
+    if (mode <= 1) {
+      p->apre_blocks = mode == 1 ? fkk::gram_pre2_image_blocks(M) : (M + 127) / 128;
+      p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, p->apre_blocks));
+    }
     p->gtc_part = dalloc<double>(p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
                                              : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
   } else {
@@ -398,8 +405,8 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
   const bool pre = p->apre != nullptr;
   if (pre)
-    fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->inv_ref, (float)p->d.ratio_floor, p->A,
-                             p->apre, p->flags, s);
+    fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->apre_blocks, p->inv_ref,
+                             (float)p->d.ratio_floor, p->A, p->apre, p->flags, s);
   else
     fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
   if (p->d.f_mode == FKK_F_EQ9) {
@@ -419,7 +426,11 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
     if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
       const int64_t nr = std::max<int64_t>(r1 - r0, 1);
-      if (pre) {
+      if (pre && p->gtc_pair) {
+        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
+        fkk::launch_gram_pre2(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+        fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      } else if (pre) {
         const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
         fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
         fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
@@ -456,7 +467,8 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
 }
 
 // F5..F11 given V64 (device) and s (host); q computed unless given (h_q != nullptr).
-void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_q_in, int nq_in, void* d_out) {
+void transform_rest(fkk_plan* p, const void* cube, int64_t n_rows, int64_t row0, const int64_t* h_q_in, int nq_in,
+                    void* d_out) {
   cudaStream_t s = p->stream;
   const int M = p->M, k = p->k, kp = p->kp;
   // W = D_f V (fp32 for the CUDA-core variant; a tf32 hi/lo W^T image for the tensor cores)
@@ -470,6 +482,7 @@ void transform_rest(fkk_plan* p, int64_t n_rows, int64_t row0, const int64_t* h_
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
+    (void)cube;
     if (tcg)
       fkk::launch_project_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->wimg, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
                              p->ext_idx, row0 + r0, 1, s);
@@ -790,7 +803,7 @@ fkk_status fkk_transform(fkk_plan_t p, const void* d_icars, int64_t n_rows, cons
     if (ng < p->k) throw Status(FKK_ERR_INVALID_ARG, "rank_k exceeds the global number of spectra");
     p->last_global_rows = ng;
     svd_stage(p, d_icars, n_rows, d_iref, ng);
-    transform_rest(p, n_rows, row0, nullptr, 0, d_out);
+    transform_rest(p, d_icars, n_rows, row0, nullptr, 0, d_out);
     p->check_flags_sync();
     if (basis_out) *basis_out = export_basis(p);
     p->end_call();
@@ -825,7 +838,7 @@ fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows,
     FKK_CUDA_CHECK(cudaMemcpyAsync(p->V64, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice, s));
     FKK_CUDA_CHECK(cudaStreamSynchronize(s));
     p->h_s.assign(h_s, h_s + k);
-    transform_rest(p, n_rows, row0, h_q, nq, d_out);
+    transform_rest(p, d_icars, n_rows, row0, h_q, nq, d_out);
     p->check_flags_sync();
     p->end_call();
   });

@@ -82,9 +82,14 @@ void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M
                            double* G, int accumulate, cudaStream_t s);
 // Pre-split Gram (k_gram_tc.cu): the log-ratio pass also writes the MMA smem image of A0 (tf32 hi/lo
 // K-major blocks per 128-channel block and 32-pixel stage); the Gram bulk-copies it (no producers).
-size_t gram_pre_bytes(int64_t n, int M);
-void launch_logratio_pre(const float* I, int64_t n, int M, const float* inv_ref, float floor, float* A,
+// nT = number of 128-channel image blocks (>= ceil(M / 128); blocks past M are zero)
+size_t gram_pre_bytes(int64_t n, int nT);
+void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* inv_ref, float floor, float* A,
                          unsigned char* Apre, int* flags, cudaStream_t s);
+// CTA-pair Gram fed by the image (k_gram_pre2.cu): 256 x 256 tiles (gram_tc2_tiles / _splits / _reduce)
+int gram_pre2_image_blocks(int M);
+void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
+                      double* partials, cudaStream_t s);
 void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
                      double* partials, cudaStream_t s);
 // tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.

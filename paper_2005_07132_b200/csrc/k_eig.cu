@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict
 //   one grid barrier.
 // One barrier and one L2 round trip per column (the L2-streaming kernel above needs ~3 round trips).
 constexpr int kTsThreads = 512;
-constexpr int kTsSeg = 2;     // each owned row is split over 2 warps (partial dots summed by readers)
+constexpr int kTsSeg = 1;     // one warp per owned row (readers fetch one p value per row)
+constexpr int kTsMaxU = 4;    // c values per thread in the post-barrier loads (M <= 4 x 512)
 
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
   __syncthreads();
@@ -194,7 +195,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
 __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const double* __restrict__ G, double* __restrict__ Wk,
                                                                    int M, double* __restrict__ d, double* __restrict__ e,
                                                                    double* __restrict__ tau, double* __restrict__ Pg,
-                                                                   unsigned int* __restrict__ ctr) {
+                                                                   unsigned int* __restrict__ ctr, int dbg) {
   extern __shared__ __align__(16) double sm[];
   const int P = gridDim.x, cta = blockIdx.x;
   const int R = (M - cta + P - 1) / P;            // owned rows: r = cta + i P, i < R
@@ -213,7 +214,12 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
   double tprev = 0.0;
   double* v = vbuf0;
   double* vp = vbuf1;
+  long long tsr[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // dbg 3: phase clocks of CTA 0 at column 500
+  auto stamp = [&](int j, int ph) {
+    if (dbg == 3 && cta == 0 && tid == 0 && j == 500) tsr[ph] = clock64();
+  };
   for (int j = 0; j + 2 < M; ++j) {
+    stamp(j, 0);
     // ---- x = row j of A^(j)
     if (j == 0) {
       for (int c = tid; c < M; c += nt) x[c] = G[c];
@@ -221,15 +227,31 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
     } else {
       double s = 0.0;
       const double* pub = Wk + (int64_t)j * M;
-      for (int c = j + tid; c < M; c += nt) {
-        double pv = 0.0;
+      // every L2 load of this thread in flight at once (one round trip after the barrier)
+      double pvr[kTsMaxU], xrr[kTsMaxU];
 #pragma unroll
-        for (int sg = 0; sg < kTsSeg; ++sg) pv += __ldcg(Pg + (int64_t)sg * M + c);
-        wp[c] = pv;
-        x[c] = __ldcg(pub + c);
-        s += pv * vp[c];
+      for (int u = 0; u < kTsMaxU; ++u) {
+        const int c = j + tid + u * nt;
+        pvr[u] = 0.0;
+        xrr[u] = 0.0;
+        if (c < M) {
+#pragma unroll
+          for (int sg = 0; sg < kTsSeg; ++sg) pvr[u] += __ldcg(Pg + (int64_t)sg * M + c);
+          xrr[u] = __ldcg(pub + c);
+        }
       }
+#pragma unroll
+      for (int u = 0; u < kTsMaxU; ++u) {
+        const int c = j + tid + u * nt;
+        if (c < M) {
+          wp[c] = pvr[u];
+          x[c] = xrr[u];
+          s += pvr[u] * vp[c];
+        }
+      }
+      stamp(j, 1);
       const double K = 0.5 * tprev * block_sum_d(s, red);
+      stamp(j, 2);
       for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
       __syncthreads();
       const double vj = vp[j], wj = wp[j];
@@ -241,10 +263,12 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
       }
       __syncthreads();
     }
+    stamp(j, 3);
     // ---- Householder reflector of x[j+1..M-1]
     double s2 = 0.0;
     for (int c = j + 1 + tid; c < M; c += nt) s2 += x[c] * x[c];
     const double nrm2 = block_sum_d(s2, red);
+    stamp(j, 4);
     const double x0 = x[j + 1];
     const double nrm = sqrt(nrm2);
     const double alpha = x0 >= 0.0 ? -nrm : nrm;
@@ -258,12 +282,13 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
       tau[j] = t;
     }
     __syncthreads();
+    stamp(j, 5);
     // ---- pass over the owned rows r > j: pending update (eager, smem), p_r = t A^(j)[r,:] v_j
     const bool pending = j > 0;
     const int m0 = j + 1, m = M - m0;
     const int seglen = (m + kTsSeg - 1) / kTsSeg;
     const bool last = j + 3 == M;
-    for (int task = warp; task < R * kTsSeg; task += nw) {
+    for (int task = warp; task < (dbg == 1 ? 0 : R * kTsSeg); task += nw) {   // dbg 1: timing without the pass
       const int i = task / kTsSeg, sg = task - i * kTsSeg;
       const int r = cta + i * P;
       if (r <= j) continue;
@@ -293,7 +318,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) Pg[(int64_t)sg * M + r] = t * acc;
     }
-    grid_barrier(ctr, target);
+    stamp(j, 6);
+    if (dbg != 2) grid_barrier(ctr, target);   // dbg 2: timing without the barrier (wrong results)
+    stamp(j, 7);
     tprev = t;
     double* tmp = vp; vp = v; v = tmp;
   }
@@ -320,6 +347,8 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
       d[M - 1] = __ldcg(r1 + M - 1) - 2.0 * vp[M - 1] * wp[M - 1];
     }
   }
+  if (dbg == 3 && cta == 0 && tid == 0)
+    for (int q = 0; q < 8; ++q) e[q] = (double)tsr[q];
 }
 
 size_t tridiag_rows_smem(int M, int P) {
@@ -882,7 +911,7 @@ int eig_path_rows_resident(int M) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const char* force = getenv("FKK_EIG_FORCE_L2");   // debugging / A-B only
   if (force && force[0] == '1') return 0;
-  return M >= 3 && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
+  return M >= 3 && M <= kTsMaxU * kTsThreads && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
 }
 
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
@@ -936,7 +965,9 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
     int Mi = M;
     const double* Gc = G;
-    void* args[] = {&Gc, &A, &Mi, &d, &e, &tau, &pg, &ctr};
+    int dbg = 0;
+    if (const char* ev = getenv("FKK_TRIDIAG_DBG")) dbg = atoi(ev);   // timing experiments only
+    void* args[] = {&Gc, &A, &Mi, &d, &e, &tau, &pg, &ctr, &dbg};
     FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_rows_kernel, dim3(nct), dim3(kTsThreads), args, smem, s));
     count_launch();
   } else {

@@ -518,17 +518,15 @@ void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M
 
 namespace fkk {
 
-size_t gram_pre_bytes(int64_t n, int M) {
+size_t gram_pre_bytes(int64_t n, int nT) {
   const int64_t nq = (n + GKC - 1) / GKC;
-  const int nT = (M + GT - 1) / GT;
   return (size_t)nT * nq * 2 * GOP_BYTES;
 }
 
-void launch_logratio_pre(const float* I, int64_t n, int M, const float* inv_ref, float floor, float* A,
+void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* inv_ref, float floor, float* A,
                          unsigned char* Apre, int* flags, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t nq = (n + GKC - 1) / GKC;
-  const int nT = (M + GT - 1) / GT;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -137,3 +137,17 @@ def test_two_rank_gloo_sharded_q_matches_single_process():
     A = O.log_ratio(I, Iref, O.Params())
     assert np.max(np.abs(G - A.T @ A)) / np.max(np.abs(G)) < 1e-13
     assert list(q) == list(O.select_q(A @ V))
+
+
+def test_library_has_no_undefined_internal_symbols():
+    """Every fkk:: function the C-ABI library calls is defined in it (a shared library links with
+    undefined symbols and would only fail when the call is made)."""
+    import shutil
+    import subprocess
+    from paper_2005_07132_b200 import build as b
+    if shutil.which("nm") is None:
+        import pytest
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--undefined-only", b.LIB], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if ln.split()[0] == "U" and "fkk" in ln]
+    assert not bad, bad
