@@ -17,7 +17,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "device_common.cuh"
 #include "fkk_internal.h"
+#include "tc_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -168,16 +170,17 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double* __restrict
 // grid keeps rows r = c, c + P, c + 2P, ... of the working matrix in its shared memory for the whole
 // tridiagonalisation, so the per-column pass touches no L2.  Per column j, with (v_{j-1}, w_{j-1})
 // the pending rank-2 update:
-//   after the barrier of column j-1: read p_{j-1} (m values) and the published row j (state
-//     A^(j-1)) in ONE batch of L2 loads; form w_{j-1} = p - (t/2)(p.v) v; x = row j of A^(j);
-//     reflector v_j, t_j (every CTA redundantly);
+//   after the barrier of column j-1: read p_{j-1} and column j of A^(j-1) (= row j, symmetry) in ONE
+//     batch of L2 loads; form w_{j-1} = p - (t/2)(p.v) v; x = row j of A^(j); reflector v_j, t_j
+//     (every CTA redundantly, on 4 warps: the "column chain");
 //   pass: every owned row r > j gets the pending update (eagerly, in smem) and p_r = t_j A^(j)[r,:] v_j;
-//     the owner of row j+1 publishes it (state A^(j)) for the next column;
+//     each row also emits its entry A^(j)[r][j+1] (column j+1 = row j+1 for the next chain);
 //   one grid barrier.
-// One barrier and one L2 round trip per column (the L2-streaming kernel above needs ~3 round trips).
+// The last columns (trailing block small enough for the shared memory of ONE thread-block cluster)
+// continue in tridiag_tail_kernel with cluster barriers (~0.2 us) instead of grid barriers (~1.5-2 us).
 constexpr int kTsThreads = 512;
-constexpr int kTsSeg = 1;     // one warp per owned row (readers fetch one p value per row)
-constexpr int kTsMaxU = 4;    // c values per thread in the post-barrier loads (M <= 4 x 512)
+constexpr int kTsChain = 128;   // threads of the per-column chain (warps 0-3)
+constexpr int kTsMaxM = 16 * kTsChain;   // chain registers: 16 entries per chain thread
 
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
   __syncthreads();
@@ -192,10 +195,144 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
   __syncthreads();
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// sum over the 128 chain threads: warp sums, then every chain thread adds the 4 partials in a fixed order
+__device__ __forceinline__ double chain_sum(double v, double* buf) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  return (buf[0] + buf[1]) + (buf[2] + buf[3]);
+}
+
+// The column chain of column j, run by the 128 chain threads; chain thread ct owns the entries
+// c = j + ct + 128 i (i < NPL) in registers: Pv = p_{j-1}[c], X = A^(j-1)[j][c] on entry (zero past M).
+//   K = (t_{j-1}/2) p.v_{j-1};  w_{j-1} = p - K v_{j-1} -> wp;  x = X - v_{j-1}[j] w - w[j] v_{j-1}
+//   (= row j of A^(j));  reflector v_j (x below the diagonal with v[j+1] = x[j+1] - alpha) -> v,
+//   t_j = 2 / v.v -> red[8];  d[j], e[j], tau[j] by the writer.
+// Only the two 128-thread sums synchronise.  pj = p_{j-1}[j], vj = v_{j-1}[j] are read by every thread
+// before any wp write.
+template <int NPL>
+__device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], double (&X)[NPL], double pj,
+                                             const double* vp, double* wp, double* v, double* red, double tprev,
+                                             bool writer, double* d, double* e, double* tau) {
+  const int ct = threadIdx.x;
+  if (j > 0) {
+    double V[NPL];
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int c = j + ct + kTsChain * i;
+      V[i] = c < M ? vp[c] : 0.0;
+      s = fma(Pv[i], V[i], s);
+    }
+    const double vj = vp[j];
+    const double K = 0.5 * tprev * chain_sum(s, red);
+    const double wj = tprev != 0.0 ? pj - K * vj : 0.0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int c = j + ct + kTsChain * i;
+      const double w = tprev != 0.0 ? Pv[i] - K * V[i] : 0.0;
+      X[i] -= vj * w + wj * V[i];
+      if (c < M) wp[c] = w;
+    }
+  }
+  double s2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int c = j + ct + kTsChain * i;
+    if (c > j && c < M) {
+      s2 = fma(X[i], X[i], s2);
+      v[c] = X[i];
+    }
+  }
+  if (ct == 1) red[12] = X[0];   // x[j+1]
+  if (ct == 0) red[13] = X[0];   // x[j]
+  const double nrm2 = chain_sum(s2, red + 4);
+  const double x0 = red[12];
+  const double nrm = sqrt(nrm2);
+  const double alpha = x0 >= 0.0 ? -nrm : nrm;
+  const double v0 = x0 - alpha;
+  const double vtv = nrm2 - x0 * x0 + v0 * v0;
+  const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
+  if (ct == 1) v[j + 1] = v0;
+  if (ct == 0) {
+    red[8] = t;
+    if (writer) {
+      d[j] = red[13];
+      e[j] = t == 0.0 ? x0 : alpha;
+      tau[j] = t;
+    }
+  }
+}
+
+// The pass over one owned row r > j (one warp): pending update row -= v_{j-1}[r] w + w[r] v_{j-1} (if
+// pending) and the dot A^(j)[r,:] v_j over c > j.  Lane 0 handles c = j + 1 first, so row[j+1]
+// (= A^(j)[r][j+1]) is its own write.
+__device__ __forceinline__ double row_pass(double* row, int m0, int M, bool pending, double vr, double wr,
+                                           const double* vp, const double* wp, const double* v, double* pub) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  if (pending) {
+#pragma unroll 4
+    for (int c = m0 + lane; c < M; c += 32) {
+      const double a = row[c] - (vr * wp[c] + wr * vp[c]);
+      row[c] = a;
+      if (pub) pub[c] = a;
+      acc = fma(a, v[c], acc);
+    }
+  } else {
+#pragma unroll 4
+    for (int c = m0 + lane; c < M; c += 32) {
+      const double a = row[c];
+      if (pub) pub[c] = a;
+      acc = fma(a, v[c], acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Trailing 2 x 2 block after the last column (j = M-3): w_{M-3} from p_{M-3} (pcur), the reflector
+// v_{M-3} -> row M-3 of Wk, and d[M-2], e[M-2], d[M-1] from rows M-2, M-1 of A^(M-3) (published to Wk).
+// One CTA; p read with loader(c).
+template <typename PL>
+__device__ __forceinline__ void tail_flush(int M, PL pload, const double* vp, double* wp, double tprev, double* red,
+                                           double* Wk, double* d, double* e) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int j = M - 2;
+  double s = 0.0;
+  for (int c = j + tid; c < M; c += nt) {
+    const double pv = pload(c);
+    wp[c] = pv;
+    s += pv * vp[c];
+  }
+  const double K = 0.5 * tprev * block_sum_d(s, red);
+  for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
+  __syncthreads();
+  double* rj = Wk + (int64_t)(j - 1) * M;
+  for (int c = j + tid; c < M; c += nt) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+  if (tid == 0) {
+    const double* r0 = Wk + (int64_t)(M - 2) * M;
+    const double* r1 = Wk + (int64_t)(M - 1) * M;
+    d[M - 2] = __ldcg(r0 + M - 2) - 2.0 * vp[M - 2] * wp[M - 2];
+    e[M - 2] = __ldcg(r1 + M - 2) - (vp[M - 1] * wp[M - 2] + wp[M - 1] * vp[M - 2]);
+    d[M - 1] = __ldcg(r1 + M - 1) - 2.0 * vp[M - 1] * wp[M - 1];
+  }
+}
+
+// Grid phase: columns j < jend (jend = M - 2: all).  With jend < M - 2 every CTA leaves its owned rows
+// r >= jend (state A^(jend-1), columns >= jend) in Wk and CTA 0 the reflector v_{jend-1} in row jend-1,
+// for tridiag_tail_kernel.
+template <int NPL>
 __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const double* __restrict__ G, double* __restrict__ Wk,
-                                                                   int M, double* __restrict__ d, double* __restrict__ e,
-                                                                   double* __restrict__ tau, double* __restrict__ Pg,
-                                                                   unsigned int* __restrict__ ctr, int dbg) {
+                                                                   int M, int jend, double* __restrict__ d,
+                                                                   double* __restrict__ e, double* __restrict__ tau,
+                                                                   double* __restrict__ Pg, unsigned int* __restrict__ ctr,
+                                                                   int dbg) {
   extern __shared__ __align__(16) double sm[];
   const int P = gridDim.x, cta = blockIdx.x;
   const int R = (M - cta + P - 1) / P;            // owned rows: r = cta + i P, i < R
@@ -203,13 +340,14 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
   double* vbuf0 = rows + (size_t)R * M;            // v_j / v_{j-1} ping-pong (absolute index)
   double* vbuf1 = vbuf0 + M;
   double* wp = vbuf1 + M;                          // w_{j-1}
-  double* x = wp + M;                              // row j of A^(j)
-  double* red = x + M;                             // 32
+  double* red = wp + M;                            // 32
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int i = 0; i < R; ++i) {
     const double* g = G + (int64_t)(cta + i * P) * M;
     for (int c = tid; c < M; c += nt) rows[(size_t)i * M + c] = g[c];
   }
+  for (int c = tid; c < 3 * M; c += nt) vbuf0[c] = 0.0;   // no uninitialised value ever meets a zero weight
+  __syncthreads();
   unsigned int target = 0;
   double tprev = 0.0;
   double* v = vbuf0;
@@ -218,142 +356,195 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
   auto stamp = [&](int j, int ph) {
     if (dbg == 3 && cta == 0 && tid == 0 && j == 500) tsr[ph] = clock64();
   };
-  for (int j = 0; j + 2 < M; ++j) {
+  const int jstop = min(jend, M - 2);
+  for (int j = 0; j < jstop; ++j) {
     stamp(j, 0);
-    // ---- x = row j of A^(j)
-    if (j == 0) {
-      for (int c = tid; c < M; c += nt) x[c] = G[c];
-      __syncthreads();
-    } else {
-      double s = 0.0;
-      const double* pub = Wk + (int64_t)j * M;
-      // every L2 load of this thread in flight at once (one round trip after the barrier)
-      double pvr[kTsMaxU], xrr[kTsMaxU];
+    if (tid < kTsChain) {
+      double X[NPL], Pv[NPL];
+      double pj = 0.0;
+      if (j == 0) {
 #pragma unroll
-      for (int u = 0; u < kTsMaxU; ++u) {
-        const int c = j + tid + u * nt;
-        pvr[u] = 0.0;
-        xrr[u] = 0.0;
-        if (c < M) {
-#pragma unroll
-          for (int sg = 0; sg < kTsSeg; ++sg) pvr[u] += __ldcg(Pg + (int64_t)sg * M + c);
-          xrr[u] = __ldcg(pub + c);
+        for (int i = 0; i < NPL; ++i) {
+          const int c = tid + kTsChain * i;
+          X[i] = c < M ? G[c] : 0.0;
+          Pv[i] = 0.0;
         }
-      }
+      } else {
+        const double* pprev = Pg + ((j - 1) & 1) * M;         // p_{j-1}
+        const double* cprev = Pg + (2 + ((j - 1) & 1)) * M;   // column j of A^(j-1) = row j
 #pragma unroll
-      for (int u = 0; u < kTsMaxU; ++u) {
-        const int c = j + tid + u * nt;
-        if (c < M) {
-          wp[c] = pvr[u];
-          x[c] = xrr[u];
-          s += pvr[u] * vp[c];
+        for (int i = 0; i < NPL; ++i) {
+          const int c = j + tid + kTsChain * i;
+          Pv[i] = c < M ? __ldcg(pprev + c) : 0.0;
+          X[i] = c < M ? __ldcg(cprev + c) : 0.0;
         }
+        pj = __ldcg(pprev + j);
       }
       stamp(j, 1);
-      const double K = 0.5 * tprev * block_sum_d(s, red);
+      column_chain<NPL>(j, M, Pv, X, pj, vp, wp, v, red, tprev, cta == 0, d, e, tau);
       stamp(j, 2);
-      for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
-      __syncthreads();
-      const double vj = vp[j], wj = wp[j];
-      for (int c = j + tid; c < M; c += nt) x[c] -= vj * wp[c] + wj * vp[c];
-      // reflector v_{j-1} -> dead row j-1 (every CTA has read that row before the last barrier)
-      if (cta == 0) {
-        double* rj = Wk + (int64_t)(j - 1) * M;
-        for (int c = j + tid; c < M; c += nt) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
-      }
-      __syncthreads();
-    }
-    stamp(j, 3);
-    // ---- Householder reflector of x[j+1..M-1]
-    double s2 = 0.0;
-    for (int c = j + 1 + tid; c < M; c += nt) s2 += x[c] * x[c];
-    const double nrm2 = block_sum_d(s2, red);
-    stamp(j, 4);
-    const double x0 = x[j + 1];
-    const double nrm = sqrt(nrm2);
-    const double alpha = x0 >= 0.0 ? -nrm : nrm;
-    const double v0 = x0 - alpha;
-    const double vtv = nrm2 - x0 * x0 + v0 * v0;
-    const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
-    for (int c = j + 1 + tid; c < M; c += nt) v[c] = c == j + 1 ? v0 : x[c];
-    if (cta == 0 && tid == 0) {
-      d[j] = x[j];
-      e[j] = t == 0.0 ? x0 : alpha;
-      tau[j] = t;
+    } else if (j > 0 && dbg != 5) {   // dbg 5: timing without the reflector stores (wrong results)
+      // reflector v_{j-1} -> dead row j-1, a 1/P slice per CTA
+      double* rj = Wk + (int64_t)(j - 1) * M;
+      const int len = (M - j + P - 1) / P, c0 = j + cta * len, c1 = min(M, c0 + len);
+      for (int c = c0 + tid - kTsChain; c < c1; c += nt - kTsChain) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
     }
     __syncthreads();
-    stamp(j, 5);
+    const double t = red[8];
+    stamp(j, 3);
     // ---- pass over the owned rows r > j: pending update (eager, smem), p_r = t A^(j)[r,:] v_j
-    const bool pending = j > 0;
-    const int m0 = j + 1, m = M - m0;
-    const int seglen = (m + kTsSeg - 1) / kTsSeg;
+    const int m0 = j + 1;
     const bool last = j + 3 == M;
-    for (int task = warp; task < (dbg == 1 ? 0 : R * kTsSeg); task += nw) {   // dbg 1: timing without the pass
-      const int i = task / kTsSeg, sg = task - i * kTsSeg;
+    for (int i = warp; i < (dbg == 1 ? 0 : R); i += nw) {   // one warp per owned row; dbg 1: timing without the pass
       const int r = cta + i * P;
       if (r <= j) continue;
       double* row = rows + (size_t)i * M;
-      const int c0 = m0 + sg * seglen, c1 = min(M, c0 + seglen);
-      const bool publish = r == j + 1 || (last && r == M - 1);
-      double* pub = Wk + (int64_t)r * M;
-      double acc = 0.0;
-      if (pending) {
-        const double vr = vp[r], wr = wp[r];
-#pragma unroll 4
-        for (int c = c0 + lane; c < c1; c += 32) {
-          const double a = row[c] - (vr * wp[c] + wr * vp[c]);
-          row[c] = a;
-          if (publish) pub[c] = a;
-          acc = fma(a, v[c], acc);
-        }
-      } else {
-#pragma unroll 4
-        for (int c = c0 + lane; c < c1; c += 32) {
-          const double a = row[c];
-          if (publish) pub[c] = a;
-          acc = fma(a, v[c], acc);
-        }
+      const bool publish = last && (r == j + 1 || r == M - 1);   // rows for the trailing 2 x 2 flush
+      const double acc = row_pass(row, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
+      // p_r and A^(j)[r][j+1] into the column-parity buffers: a fast CTA's next pass never overwrites
+      // what a slow CTA still reads
+      if (lane == 0) {
+        Pg[(j & 1) * M + r] = t * acc;
+        Pg[(2 + (j & 1)) * M + r] = row[m0];
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) Pg[(int64_t)sg * M + r] = t * acc;
     }
-    stamp(j, 6);
-    if (dbg != 2) grid_barrier(ctr, target);   // dbg 2: timing without the barrier (wrong results)
+    stamp(j, 4);
+    if (dbg != 2) {   // dbg 2: timing without the barrier (wrong results); = grid_barrier with stamps
+      __syncthreads();
+      stamp(j, 5);
+      target += gridDim.x;
+      if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+        unsigned int cv;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cv) : "l"(ctr) : "memory");
+        } while ((int)(cv - target) < 0);
+      }
+      stamp(j, 6);
+      __syncthreads();
+    }
     stamp(j, 7);
     tprev = t;
     double* tmp = vp; vp = v; v = tmp;
   }
-  // ---- flush: w_{M-3}, the trailing 2 x 2 block, reflector v_{M-3}
-  if (cta == 0 && M >= 3) {
-    const int j = M - 2;
-    double s = 0.0;
-    for (int c = j + tid; c < M; c += nt) {
-      double pv = 0.0;
-      for (int sg = 0; sg < kTsSeg; ++sg) pv += __ldcg(Pg + (int64_t)sg * M + c);
-      wp[c] = pv;
-      s += pv * vp[c];
+  if (jstop < M - 2) {
+    // hand-over to the cluster tail: owned rows r >= jend (columns >= jend), reflector v_{jend-1}
+    for (int i = 0; i < R; ++i) {
+      const int r = cta + i * P;
+      if (r < jend) continue;
+      for (int c = jend + tid; c < M; c += nt) Wk[(int64_t)r * M + c] = rows[(size_t)i * M + c];
     }
-    const double K = 0.5 * tprev * block_sum_d(s, red);
-    for (int c = j + tid; c < M; c += nt) wp[c] = tprev != 0.0 ? wp[c] - K * vp[c] : 0.0;
-    __syncthreads();
-    double* rj = Wk + (int64_t)(j - 1) * M;
-    for (int c = j + tid; c < M; c += nt) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
-    if (tid == 0) {
-      const double* r0 = Wk + (int64_t)(M - 2) * M;
-      const double* r1 = Wk + (int64_t)(M - 1) * M;
-      d[M - 2] = __ldcg(r0 + M - 2) - 2.0 * vp[M - 2] * wp[M - 2];
-      e[M - 2] = __ldcg(r1 + M - 2) - (vp[M - 1] * wp[M - 2] + wp[M - 1] * vp[M - 2]);
-      d[M - 1] = __ldcg(r1 + M - 1) - 2.0 * vp[M - 1] * wp[M - 1];
-    }
+    if (cta == 0 && jend > 0)
+      for (int c = jend + tid; c < M; c += nt) Wk[(int64_t)(jend - 1) * M + c] = tprev != 0.0 ? vp[c] : 0.0;
+  } else if (cta == 0 && M >= 3) {
+    const double* pcur = Pg + ((M - 3) & 1) * M;
+    tail_flush(M, [&](int c) { return __ldcg(pcur + c); }, vp, wp, tprev, red, Wk, d, e);
   }
   if (dbg == 3 && cta == 0 && tid == 0)
     for (int q = 0; q < 8; ++q) e[q] = (double)tsr[q];
 }
 
+// Cluster tail: columns j >= jend of the same algorithm on ONE cluster of CL CTAs, the trailing
+// (M - jend)^2 block resident in their shared memory (rows r = jend + rank + i CL).  p_r and
+// A^(j)[r][j+1] are pushed into every CTA's shared memory with st.shared::cluster during the pass
+// (parity-buffered), so a column costs the chain, the pass and one cluster barrier -- no L2 round trip.
+// Entry state (jend > 0): rows r >= jend of A^(jend-1) in Wk, v_{jend-1} in Wk row jend-1, p_{jend-1}
+// and column jend of A^(jend-1) in the Pg parity buffers, t_{jend-1} = tau[jend-1].  jend = 0: G.
+template <int NPL>
+__global__ void __launch_bounds__(kTsThreads, 1) tridiag_tail_kernel(const double* __restrict__ G, double* __restrict__ Wk,
+                                                                   int M, int jend, double* __restrict__ d,
+                                                                   double* __restrict__ e, double* __restrict__ tau,
+                                                                   const double* __restrict__ Pg) {
+  extern __shared__ __align__(16) double sm[];
+  uint32_t rank, CL;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CL));
+  const int mt = M - jend;
+  const int R = (mt - (int)rank + (int)CL - 1) / (int)CL;   // owned rows r = jend + rank + i CL
+  double* rows = sm - jend;                                 // row i: rows + i mt, valid for c >= jend
+  double* base = sm + (size_t)((mt + CL - 1) / CL) * mt;    // same layout in every CTA of the cluster
+  double* vbuf0 = base - jend;
+  double* vbuf1 = vbuf0 + mt;
+  double* wp = vbuf1 + mt;
+  double* pb = wp + mt;     // pb + parity * mt: p of the column with that parity (absolute index c)
+  double* cb = pb + 2 * mt; // cb + parity * mt: column j+1 of A^(j) (absolute index c)
+  double* red = base + 7 * mt;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int pprev0 = (jend - 1) & 1;
+  for (int i = 0; i < R; ++i) {
+    const int r = jend + (int)rank + i * (int)CL;
+    const double* src = jend > 0 ? Wk + (int64_t)r * M : G + (int64_t)r * M;
+    for (int c = jend + tid; c < M; c += nt) rows[(size_t)i * mt + c] = src[c];
+  }
+  for (int c = jend + tid; c < M; c += nt) {
+    vbuf0[c] = 0.0;
+    wp[c] = 0.0;
+    vbuf1[c] = jend > 0 ? __ldcg(Wk + (int64_t)(jend - 1) * M + c) : 0.0;
+    pb[pprev0 * mt + c] = jend > 0 ? __ldcg(Pg + pprev0 * M + c) : 0.0;
+    cb[pprev0 * mt + c] = jend > 0 ? __ldcg(Pg + (2 + pprev0) * M + c) : G[c];
+  }
+  double tprev = jend > 0 ? tau[jend - 1] : 0.0;
+  // remote addresses of the p / column buffers in every CTA of the cluster (lane q < CL: CTA q)
+  uint32_t rpb = 0, rcb = 0;
+  if (lane < (int)CL) {
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpb) : "r"(tc::smem_u32(pb + jend)), "r"(lane));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rcb) : "r"(tc::smem_u32(cb + jend)), "r"(lane));
+  }
+  cluster_sync_all();
+  double* v = vbuf0;
+  double* vp = vbuf1;
+  for (int j = jend; j + 2 < M; ++j) {
+    const int pp = (j - 1) & 1, pc = j & 1;
+    if (tid < kTsChain) {
+      double X[NPL], Pv[NPL];
+      const double* pprev = pb + pp * mt;
+      const double* cprev = cb + pp * mt;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const int c = j + tid + kTsChain * i;
+        Pv[i] = c < M ? pprev[c] : 0.0;
+        X[i] = c < M ? cprev[c] : 0.0;
+      }
+      column_chain<NPL>(j, M, Pv, X, pprev[j], vp, wp, v, red, tprev, rank == 0, d, e, tau);
+    } else if (j > 0) {
+      double* rj = Wk + (int64_t)(j - 1) * M;
+      const int len = (M - j + CL - 1) / CL, c0 = j + rank * len, c1 = min(M, c0 + len);
+      for (int c = c0 + tid - kTsChain; c < c1; c += nt - kTsChain) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+    }
+    __syncthreads();
+    const double t = red[8];
+    const int m0 = j + 1;
+    const bool last = j + 3 == M;
+    for (int i = warp; i < R; i += nw) {
+      const int r = jend + (int)rank + i * (int)CL;
+      if (r <= j) continue;
+      double* row = rows + (size_t)i * mt;
+      const bool publish = last && (r == j + 1 || r == M - 1);
+      const double acc = row_pass(row, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
+      const double cval = __shfl_sync(0xffffffffu, lane == 0 ? row[m0] : 0.0, 0);
+      if (lane < (int)CL) {
+        const uint32_t off = (uint32_t)((pc * mt + (r - jend)) * 8);
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rpb + off), "d"(t * acc) : "memory");
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rcb + off), "d"(cval) : "memory");
+      }
+    }
+    cluster_sync_all();
+    tprev = t;
+    double* tmp = vp; vp = v; v = tmp;
+  }
+  if (rank == 0 && M >= 3) {
+    const double* pcur = pb + ((M - 3) & 1) * mt;
+    tail_flush(M, [&](int c) { return pcur[c]; }, vp, wp, tprev, red, Wk, d, e);
+  }
+}
+
 size_t tridiag_rows_smem(int M, int P) {
   const int R = (M + P - 1) / P;
-  return ((size_t)R * M + 4 * (size_t)M + 32) * sizeof(double);
+  return ((size_t)R * M + 3 * (size_t)M + 32) * sizeof(double);
+}
+
+size_t tridiag_tail_smem(int mt, int CL) {
+  return ((size_t)((mt + CL - 1) / CL) * mt + 7 * (size_t)mt + 32) * sizeof(double);
 }
 
 // 1/q via the MUFU seed + two Newton steps (full fp64 accuracy for normal q; a Sturm count only
@@ -901,7 +1092,7 @@ __global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __rest
 
 size_t eig_workspace_doubles(int M, int k) {
   // d, e, tau (3M) + p / LL words (16M) + lam, tnorm (k+1) + Z, Z2, Z3 (3kM) + S, T (2k^2) + flag + A (M*M)
-  return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 16 + (size_t)M * M;
+  return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 18 + (size_t)M * M;
 }
 
 int eig_path_rows_resident(int M) {
@@ -911,11 +1102,12 @@ int eig_path_rows_resident(int M) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const char* force = getenv("FKK_EIG_FORCE_L2");   // debugging / A-B only
   if (force && force[0] == '1') return 0;
-  return M >= 3 && M <= kTsMaxU * kTsThreads && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
+  return M >= 3 && M <= kTsMaxM && tridiag_rows_smem(M, sms) <= (size_t)maxsm;
 }
 
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
                      cudaStream_t s, double* dbg_det);
+
 
 void debug_tridiag(const double* G, int M, double* det_out) {
   double* work = nullptr;
@@ -947,29 +1139,69 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   double* S = Z3 + (size_t)k * M;
   double* T = S + (size_t)k * k;
   int* fallback = reinterpret_cast<int*>(T + (size_t)k * k);
-  double* A = T + (size_t)k * k + 16;      // working matrix / published rows / reflectors (M x M)
+  // working matrix / published rows / reflectors (M x M), 16-byte aligned for the bulk copies
+  double* A = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(T + (size_t)k * k + 16) + 15) & ~(uintptr_t)15);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (eig_path_rows_resident(M)) {
-    // row-resident cooperative tridiagonalisation (G is read, never copied); one grid barrier per column
-    int nct = sms;
-    if (const char* ev = getenv("FKK_TRIDIAG_CTAS")) nct = std::max(1, std::min(sms, atoi(ev)));   // A/B only
-    while (nct > 1 && tridiag_rows_smem(M, nct) > 227 * 1024) ++nct;
-    const size_t smem = tridiag_rows_smem(M, nct);
-    FKK_CUDA_CHECK(cudaFuncSetAttribute(tridiag_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per = 0;
-    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_rows_kernel, kTsThreads, smem));
-    if (per < 1) throw Status(10, "tridiag_rows kernel cannot be co-resident");
-    unsigned int* ctr = reinterpret_cast<unsigned int*>(fallback) + 2;
-    FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
-    int Mi = M;
+    // row-resident tridiagonalisation (G is read, never copied): grid phase (cooperative, one grid
+    // barrier per column) for j < jend, then the cluster tail (one cluster barrier per column) for the
+    // trailing block that fits in the shared memory of CL CTAs
+    int maxsm = 0;
+    FKK_CUDA_CHECK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int CL = 8;
+    if (const char* ev = getenv("FKK_TRIDIAG_TAIL")) CL = atoi(ev);   // cluster size of the tail; 0: none
+    if (CL != 0 && CL != 8 && CL != 16) CL = 8;
+    int mt = 0;
+    if (CL > 0) {
+      int cap = 200;   // per-column cost of the tail grows with m^2 / CL; below ~200 it beats the grid barrier
+      if (const char* ev = getenv("FKK_TRIDIAG_MT")) cap = std::max(3, atoi(ev));   // A/B only
+      mt = std::min(M, cap);
+      while (mt > 2 && tridiag_tail_smem(mt, CL) > (size_t)maxsm) --mt;
+    }
+    int jend = CL > 0 ? M - mt : M - 2;
+    if (jend < 2 && CL > 0) jend = 0;   // whole problem in the tail
+    int Mi = M, jendi = jend;
     const double* Gc = G;
-    int dbg = 0;
-    if (const char* ev = getenv("FKK_TRIDIAG_DBG")) dbg = atoi(ev);   // timing experiments only
-    void* args[] = {&Gc, &A, &Mi, &d, &e, &tau, &pg, &ctr, &dbg};
-    FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)tridiag_rows_kernel, dim3(nct), dim3(kTsThreads), args, smem, s));
-    count_launch();
+    if (jend > 0) {
+      unsigned int* ctr = reinterpret_cast<unsigned int*>(fallback) + 2;
+      FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
+      int dbg = 0;
+      if (const char* ev = getenv("FKK_TRIDIAG_DBG")) dbg = atoi(ev);   // timing experiments only
+      void* args[] = {&Gc, &A, &Mi, &jendi, &d, &e, &tau, &pg, &ctr, &dbg};
+      int nct = sms;
+      if (const char* ev = getenv("FKK_TRIDIAG_CTAS")) nct = std::max(1, std::min(sms, atoi(ev)));   // A/B only
+      const size_t smem = tridiag_rows_smem(M, nct);
+      auto kr = M <= 8 * kTsChain ? tridiag_rows_kernel<8> : tridiag_rows_kernel<16>;
+      FKK_CUDA_CHECK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per = 0;
+      FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kr, kTsThreads, smem));
+      if (per < 1) throw Status(10, "tridiag_rows kernel cannot be co-resident");
+      FKK_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)kr, dim3(nct), dim3(kTsThreads), args, smem, s));
+      count_launch();
+    }
+    if (jend < M - 2) {
+      const size_t smem = tridiag_tail_smem(M - jend, CL);
+      auto kt = tridiag_tail_kernel<8>;
+      FKK_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (CL > 8) FKK_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(CL);
+      cfg.blockDim = dim3(kTsThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const double* Pc = pg;
+      FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kt, Gc, A, Mi, jendi, d, e, tau, Pc));
+      count_launch();
+    }
   } else {
     FKK_CUDA_CHECK(cudaMemcpyAsync(A, G, (size_t)M * M * sizeof(double), cudaMemcpyDeviceToDevice, s));
     // L2-streaming cooperative tridiagonalisation (large M)
