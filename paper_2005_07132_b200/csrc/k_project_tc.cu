@@ -17,9 +17,11 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fkk_internal.h"
 #include "tc_common.cuh"
+#include "tma.h"
 
 namespace fkk {
 
@@ -276,6 +278,319 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
   if (warp == 12) tc::tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA + TMEM-A variant (default when the A0 row pitch is a multiple of 16 B).  The A0 tile (128 px x
+// 32 ch fp32) arrives by TMA (SWIZZLE_128B, conflict-free row reads); four converter warps read one
+// pixel row per thread, split it into tf32 hi/lo (round to nearest) and write both into TENSOR
+// memory (tcgen05.st), where the MMAs read the A operand.  The only shared-memory operand stream is
+// W (bulk copies from L2), so the kernel is bounded by HBM rather than by shared-memory bandwidth
+// (the smem-A version moved ~136 KB of smem traffic per 16 KB of A0, this one ~72 KB).
+//   warp 0   : A0 TMA producer (raw ring)        warp 2: W stage producer (W ring)
+//   warp 1   : TMEM alloc, MMA issue            warps 4-7: converters (warp % 4 = TMEM lane quadrant)
+//   warps 8-11: epilogue (as above)
+constexpr int QKC = 32;                       // channels per stage (one 128-B swizzle row)
+constexpr int QA_BYTES = PTM * QKC * 4;       // 16 KB raw tile
+constexpr int QTHREADS = 384;
+__host__ __device__ inline int q_w_part(int kp) { return kp * QKC * 4; }     // hi or lo: kp rows x 128 B
+__host__ __device__ inline int q_nw(int kp) { return kp <= 64 ? 6 : 3; }    // W ring slots
+__host__ __device__ inline int q_nraw(int kp) { return (208 * 1024 - q_nw(kp) * 2 * q_w_part(kp)) / QA_BYTES; }
+__host__ __device__ inline int q_ring_bytes(int kp) { return q_nraw(kp) * QA_BYTES + q_nw(kp) * 2 * q_w_part(kp); }
+// TMEM: accumulator sets at columns [0, nbuf setc), then NA A slots of 2 x 32 columns (hi | lo)
+__host__ __device__ inline int q_nbuf(int M, int kp) { return ((2 * p_set_cols(M, kp) + 127) & ~127) + 2 * 2 * QKC <= 512 ? 2 : 1; }
+__host__ __device__ inline int q_abase(int M, int kp) { return (q_nbuf(M, kp) * p_set_cols(M, kp) + 127) & ~127; }
+__host__ __device__ inline int q_na(int M, int kp) { return (512 - q_abase(M, kp)) / (2 * QKC); }
+
+// SWIZZLE_128B K-major descriptor: 8-row x 128-B atoms stacked at SBO = 1024 B, LBO unused,
+// layout type 2 (bits 61-63); the K offset inside the atom advances the start address.
+__device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// ring cursor: slot and phase parity of consecutive positions in a ring of n slots
+struct Ring {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) { slot = 0; phase ^= 1; }
+  }
+};
+
+__global__ void __launch_bounds__(QTHREADS, 1)
+project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, const float* __restrict__ wimg, int kp,
+                   float* __restrict__ US, float* __restrict__ ext_val, int64_t* __restrict__ ext_idx, int k,
+                   int64_t row_offset, int want_ext, int nbuf, int abase, int NA) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int NR = q_nraw(kp), NW = q_nw(kp);
+  const int WP = q_w_part(kp);
+  unsigned char* ring_a = smem;                              // [NR][16 KB]
+  unsigned char* ring_w = ring_a + NR * QA_BYTES;            // [NW][2 WP]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + q_ring_bytes(kp));
+  uint64_t* a_full = bars;               // [NR] TMA tx
+  uint64_t* a_empty = a_full + NR;       // [NR] converters (4 warps)
+  uint64_t* w_full = a_empty + NR;       // [NW] bulk tx
+  uint64_t* w_empty = w_full + NW;       // [NW] MMA commit
+  uint64_t* t_full = w_empty + NW;       // [NA] converters (4 warps): A hi/lo in TMEM
+  uint64_t* t_empty = t_full + NA;       // [NA] MMA commit
+  uint64_t* acc_full = t_empty + NA;     // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2] epilogue (128)
+  float* red_v = reinterpret_cast<float*>(acc_empty + 2);      // [4 warps][2][128 cols]
+  int* red_i = reinterpret_cast<int*>(red_v + 4 * 2 * 128);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_i + 4 * 2 * 128);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (n + PTM - 1) / PTM;
+  const int nst = (M + QKC - 1) / QKC;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < NR; ++s2) { tc::mbar_init(&a_full[s2], 1); tc::mbar_init(&a_empty[s2], 4); }
+    for (int s2 = 0; s2 < NW; ++s2) { tc::mbar_init(&w_full[s2], 1); tc::mbar_init(&w_empty[s2], 1); }
+    for (int s2 = 0; s2 < NA; ++s2) { tc::mbar_init(&t_full[s2], 4); tc::mbar_init(&t_empty[s2], 1); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 128); }
+    tc::fence_mbar_init();
+    tma::prefetch_map(&amap);
+  }
+  const int nseg = p_nseg(M), setc = p_set_cols(M, kp);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + (uint32_t)abase;   // A slots
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t npos = my_tiles * nst;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ A0 TMA producer (raw ring)
+    Ring ra;
+    for (int64_t pos = 0; pos < npos; ++pos, ra.next(NR)) {
+      const int64_t t = blockIdx.x + (pos / nst) * gridDim.x;
+      const int st = (int)(pos % nst);
+      tc::mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
+      if (tc::elect_one()) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&a_full[ra.slot])),
+                     "r"((uint32_t)QA_BYTES)
+                     : "memory");
+        tma::load_2d(&amap, tc::smem_u32(ring_a + ra.slot * QA_BYTES), tc::smem_u32(&a_full[ra.slot]), st * QKC,
+                     (int)(t * PTM));
+      }
+      __syncwarp();
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ W stage producer (W ring, from L2)
+    Ring rw;
+    for (int64_t pos = 0; pos < npos; ++pos, rw.next(NW)) {
+      const int st = (int)(pos % nst);
+      tc::mbar_wait(&w_empty[rw.slot], rw.phase ^ 1);
+      if (tc::elect_one()) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&w_full[rw.slot])),
+                     "r"((uint32_t)(2 * WP))
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         tc::smem_u32(ring_w + rw.slot * 2 * WP)),
+                     "l"(reinterpret_cast<const unsigned char*>(wimg) + (size_t)st * 2 * WP), "r"((uint32_t)(2 * WP)),
+                     "r"(tc::smem_u32(&w_full[rw.slot]))
+                     : "memory");
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ converters: smem row -> TMEM hi | lo
+    const int q = warp & 3, r = q * 32 + lane;            // pixel row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    Ring ra, rt;
+    for (int64_t pos = 0; pos < npos; ++pos, ra.next(NR), rt.next(NA)) {
+      tc::mbar_wait(&a_full[ra.slot], ra.phase);
+      const unsigned char* rowp = ring_a + ra.slot * QA_BYTES + r * 128;
+      float x[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+        x[4 * c] = v.x;
+        x[4 * c + 1] = v.y;
+        x[4 * c + 2] = v.z;
+        x[4 * c + 3] = v.w;
+      }
+      float hi[32], lo[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) tc::split_fast(x[i], hi[i], lo[i]);
+      tc::mbar_wait(&t_empty[rt.slot], rt.phase ^ 1);
+      tc::tc_fence_after();
+      const uint32_t ta = tmem_a + lane_off + (uint32_t)(rt.slot * 2 * QKC);
+      tc::tmem_st16(ta, hi);
+      tc::tmem_st16(ta + 16, hi + 16);
+      tc::tmem_st16(ta + QKC, lo);
+      tc::tmem_st16(ta + QKC + 16, lo + 16);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&a_empty[ra.slot]);
+        tc::mbar_arrive(&t_full[rt.slot]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue (as project_tc_kernel)
+    const int ew = warp - 8;
+    uint32_t ph[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = (int)(it % nbuf);
+      tc::mbar_wait(&acc_full[b], ph[b]);
+      ph[b] ^= 1;
+      tc::tc_fence_after();
+      const int row = ew * 32 + lane;
+      const int64_t p = t * PTM + row;
+      const bool valid = p < n;
+      const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * setc);
+      for (int c0 = 0; c0 < kp; c0 += 16) {
+        float v[16], w[16];
+        tc::tmem_ld16(tb + nseg * kp + c0, v);
+        for (int sg = 0; sg < nseg; ++sg) {
+          tc::tmem_ld16(tb + sg * kp + c0, w);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] += w[q];
+        }
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(US + p * kp + c0 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+        if (want_ext) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float vmax = valid ? v[q] : -INFINITY, vmin = valid ? v[q] : INFINITY;
+            int imax = valid ? row : 0x7fffffff, imin = imax;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const float ov = __shfl_xor_sync(0xffffffffu, vmax, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
+              if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
+              const float nv = __shfl_xor_sync(0xffffffffu, vmin, o);
+              const int ni = __shfl_xor_sync(0xffffffffu, imin, o);
+              if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
+            }
+            if (lane == 0) {
+              red_v[(ew * 2 + 0) * 128 + c0 + q] = vmax;
+              red_i[(ew * 2 + 0) * 128 + c0 + q] = imax;
+              red_v[(ew * 2 + 1) * 128 + c0 + q] = vmin;
+              red_i[(ew * 2 + 1) * 128 + c0 + q] = imin;
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acc_empty[b]);
+      if (want_ext) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = ew * 32 + lane; c < k; c += 128) {
+          float vM = -INFINITY, vm = INFINITY;
+          int iM = 0x7fffffff, im = 0x7fffffff;
+          for (int w2 = 0; w2 < 4; ++w2) {
+            const float a = red_v[(w2 * 2) * 128 + c], bmn = red_v[(w2 * 2 + 1) * 128 + c];
+            const int ia = red_i[(w2 * 2) * 128 + c], ib = red_i[(w2 * 2 + 1) * 128 + c];
+            if (a > vM || (a == vM && ia < iM)) { vM = a; iM = ia; }
+            if (bmn < vm || (bmn == vm && ib < im)) { vm = bmn; im = ib; }
+          }
+          const int64_t o = (t * (int64_t)k + c) * 2;
+          ext_val[o] = vM;
+          ext_idx[o] = iM == 0x7fffffff ? INT64_MAX : row_offset + t * PTM + iM;
+          ext_val[o + 1] = vm;
+          ext_idx[o + 1] = im == 0x7fffffff ? INT64_MAX : row_offset + t * PTM + im;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issue (A from TMEM, W from smem)
+    const uint32_t idesc = tc::make_idesc_tf32(PTM, kp, false, false);
+    Ring rw, rt;
+    uint32_t ae[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = (int)(it % nbuf);
+      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], ae[b]); ae[b] ^= 1; tc::tc_fence_after(); }
+      const uint32_t dset = tmem + (uint32_t)(b * setc);
+      const uint32_t dx = dset + nseg * kp;
+      for (int st = 0; st < nst; ++st, rw.next(NW), rt.next(NA)) {
+        tc::mbar_wait(&w_full[rw.slot], rw.phase);
+        tc::mbar_wait(&t_full[rt.slot], rt.phase);
+        tc::tc_fence_after();
+        const uint32_t sw = tc::smem_u32(ring_w + rw.slot * 2 * WP);
+        const uint64_t dbh = make_sdesc_sw128(sw), dbl = make_sdesc_sw128(sw + WP);
+        const uint32_t tah = tmem_a + (uint32_t)(rt.slot * 2 * QKC), tal = tah + QKC;
+        const int sg = (st * QKC) / PSEG;
+        const uint32_t dh = dset + sg * kp;
+        const bool seg_start = (st * QKC) % PSEG == 0;
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < QKC / 8; ++ks) {
+            const uint32_t o = ks * 32;   // 8 tf32 = 32 B along K inside the 128-B swizzle row
+            const uint32_t accx = (st > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acch = (!seg_start || ks > 0) ? 1u : 0u;
+            tc::mma_tf32_ts(dx, tal + ks * 8, tc::sdesc_add(dbh, o), idesc, accx);
+            tc::mma_tf32_ts(dx, tah + ks * 8, tc::sdesc_add(dbl, o), idesc, 1u);
+            tc::mma_tf32_ts(dh, tah + ks * 8, tc::sdesc_add(dbh, o), idesc, acch);
+          }
+          tc::mma_commit(&t_empty[rt.slot]);
+          tc::mma_commit(&w_empty[rw.slot]);
+          if (st == nst - 1) tc::mma_commit(&acc_full[b]);   // same issuing thread as the MMAs
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// W^T image for the TMA variant, per K-stage st: [hi | lo], each kp rows x 128 B in the SWIZZLE_128B
+// K-major layout (16-B chunk index XOR row mod 8).
+__global__ void build_wimg_sw_kernel(const double* __restrict__ V, const double* __restrict__ fscale,
+                                     const double* __restrict__ cscale, int M, int k, int kp, float* __restrict__ wimg) {
+  const int nst = (M + QKC - 1) / QKC;
+  const int64_t total = (int64_t)nst * kp * QKC;
+  const int WP = q_w_part(kp);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int jj = (int)(e % QKC);
+    const int nrow = (int)((e / QKC) % kp);
+    const int st = (int)(e / ((int64_t)QKC * kp));
+    const int j = st * QKC + jj;
+    double v = 0.0;
+    if (j < M && nrow < k) {
+      v = V[(int64_t)nrow * M + j];
+      if (fscale) v *= fscale[j];
+      if (cscale) v *= cscale[nrow];
+    }
+    float hi, lo;
+    tc::split_tf32((float)v, hi, lo);
+    const int64_t off = (int64_t)st * 2 * WP + nrow * 128 + (((jj >> 2) ^ (nrow & 7)) << 4) + (jj & 3) * 4;
+    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(wimg) + off) = hi;
+    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(wimg) + off + WP) = lo;
+  }
+}
+
+size_t qt_smem(int kp) {
+  return 1024 + (size_t)q_ring_bytes(kp) + 2 * (q_nraw(kp) + q_nw(kp) + 8) * 8 + 4 * 8 + 4 * 2 * 128 * 8 + 64;
+}
+
+// TMA variant unless FKK_PROJECT_MODE=0 or the A0 pitch is not a multiple of 16 B
+bool project_use_tma(int M, int kp) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* ev = getenv("FKK_PROJECT_MODE");
+    mode = ev ? atoi(ev) : 1;
+  }
+  return mode != 0 && M % 4 == 0 && qt_smem(kp) <= 227 * 1024 && q_na(M, kp) >= 2;
+}
+
 // W^T image per K-stage st: rows n (rank, < kp), K = channel j in the stage, K-major hi/lo.
 __global__ void build_wimg_kernel(const double* __restrict__ V, const double* __restrict__ fscale,
                                   const double* __restrict__ cscale, int M, int k, int kp, float* __restrict__ wimg) {
@@ -311,13 +626,39 @@ int project_tc_num_blocks(int64_t n) { return (int)((n + PTM - 1) / PTM); }
 
 void launch_build_wimg(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* wimg,
                        cudaStream_t s) {
-  build_wimg_kernel<<<256, 256, 0, s>>>(V, fscale, cscale, M, k, kp, wimg);
+  if (project_use_tma(M, kp))
+    build_wimg_sw_kernel<<<256, 256, 0, s>>>(V, fscale, cscale, M, k, kp, wimg);
+  else
+    build_wimg_kernel<<<256, 256, 0, s>>>(V, fscale, cscale, M, k, kp, wimg);
   check_launch("build_wimg");
 }
 
 void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int k, int kp, float* US, float* ext_val,
                        int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s) {
   if (n <= 0) return;
+  if (project_use_tma(M, kp)) {
+    if (kp > 128 || kp % 16 || p_set_cols(M, kp) > 512)
+      throw Status(10, "project_tc: unsupported rank padding / channel count");
+    const size_t smem = qt_smem(kp);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(project_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const CUtensorMap amap = tma::make_2d_f32(A, (uint64_t)n, (uint64_t)M, (uint64_t)M * 4, PTM, QKC, 128);
+    const int64_t ntiles = (n + PTM - 1) / PTM;
+    const int grid = (int)std::min<int64_t>(ntiles, sms);
+    int nbuf = q_nbuf(M, kp), abase = q_abase(M, kp), na = q_na(M, kp);
+    if (const char* ev = getenv("FKK_PROJECT_NBUF")) {   // A/B only
+      nbuf = 1;
+      abase = (p_set_cols(M, kp) + 127) & ~127;
+      na = std::min(8, (512 - abase) / (2 * QKC));
+      if (atoi(ev) > 0) na = std::min(na, atoi(ev));
+    }
+    project_tma_kernel<<<grid, QTHREADS, smem, s>>>(amap, n, M, wimg, kp, US, ext_val, ext_idx, k, row_offset, want_ext,
+                                                    nbuf, abase, na);
+    check_launch("project_tma");
+    return;
+  }
   const size_t smem = pt_smem(kp);
   if (smem > 227 * 1024 || kp > 128 || kp % 16 || p_set_cols(M, kp) > 512)
     throw Status(10, "project_tc: unsupported rank padding / channel count");

@@ -181,6 +181,21 @@ def test_factorized_cfg2(torch_cuda, fkk, cfg2, gemm):
     _factorized_check(torch_cuda, fkk, I, Iref, 40, gemm=gemm)
 
 
+def test_projection_repeatable_multi_tile(torch_cuda, fkk, cfg2):
+    """US = A0 V on the tensor cores (TMA + TMEM-A pipeline) against float64 A0 V, repeated: every CTA
+    walks several tiles with its rings and accumulator sets wrapping, so an early slot release (a
+    pipeline race) shows up as scattered wrong rows after the first tile."""
+    I, Iref = cfg2
+    A = O.log_ratio(I, Iref, O.Params())
+    plan = fkk.Plan(1000, 40, I.shape[0])
+    Id, Rd = _dev(torch_cuda, I), _dev(torch_cuda, Iref)
+    for _ in range(3):
+        plan.transform(Id, Rd)
+        V, US = plan.stage("V"), plan.stage("US")
+        ref = A @ V
+        assert np.max(np.abs(US - ref)) / np.max(np.abs(ref)) <= 1e-5
+
+
 def test_gram_tc_equals_simt_in_fp32_accuracy(torch_cuda, fkk, cfg2):
     """3xTF32 tcgen05 Gram vs the exact-fp32 CUDA-core Gram vs fp64 (max-norm relative)."""
     I, Iref = cfg2
