@@ -3,7 +3,10 @@
 // as one GEMM D = US . B^T per 128-pixel tile and NCH-channel chunk, B's rows interleaved
 // (amp_c, ph_c) so TMEM columns (2j, 2j+1) are the exponent and phase of channel j; 3xTF32
 // (hi*hi + hi*lo + lo*hi; K = kr = roundup8(k) is short, so one TMEM accumulator suffices).
-//   warps 0-3  : producers - the US tile (128 x kr) -> tf32 hi/lo -> K-major smem (LBO 144 B pad)
+//   warps 0-3  : producers - the US tile (128 x kr), one pixel row per thread -> tf32 hi/lo ->
+//                TENSOR memory (tcgen05.st; A slots double-buffered when they fit), where the MMAs
+//                read the A operand: shared memory carries only the B chunks (the smem-A version
+//                re-read the 128 x kr A tile for every 64-column chunk: ~4.6 MB of smem reads per tile)
 //   warps 4-11 : epilogue  - tcgen05.ld, exp/sincos into a swizzled smem box [128 px][half chunk]
 //                (one pixel row per thread, conflict-free through the TMA swizzle), then ONE 2-D
 //                TMA tensor store per box (cp.async.bulk.tensor, out-of-range rows / channels
@@ -55,6 +58,10 @@ __host__ __device__ inline RtGeom rt_geom(int k, int M) {
   return g;
 }
 
+// TMEM: 4 rotating accumulators (columns [0, 4 N)), then the A slots (hi kr | lo kr), 128-aligned
+__host__ __device__ inline int rt_a_base(const RtGeom& g) { return (4 * g.N + 127) & ~127; }
+__host__ __device__ inline int rt_a_slots(const RtGeom& g) { return rt_a_base(g) + 4 * g.kr <= 512 ? 2 : 1; }
+
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
@@ -87,13 +94,11 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
   const RtGeom g = rt_geom(k, M);
   // [RT_NBUF][2 halves][box]; the TMA swizzle pattern is a function of the smem address -> 1024-align
   unsigned char* stg = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
-  unsigned char* a_hi = stg + RT_NBUF * RT_PARTS * rt_box_region(g);
-  unsigned char* a_lo = a_hi + g.a_bytes;
-  unsigned char* bst = a_lo + g.a_bytes;                     // RT_BST stages
+  unsigned char* bst = stg + RT_NBUF * RT_PARTS * rt_box_region(g);   // RT_BST stages
   uint64_t* bars = reinterpret_cast<uint64_t*>(bst + RT_BST * g.b_stage);
-  uint64_t* a_full = bars;                      // producers -> MMA (count 128)
-  uint64_t* a_empty = bars + 1;                 // MMA commit -> producers
-  uint64_t* b_full = bars + 2;                  // [RT_BST] bulk copy tx
+  uint64_t* a_full = bars;                      // [2] producers -> MMA (count 128)
+  uint64_t* a_empty = bars + 2;                 // [2] MMA commit -> producers
+  uint64_t* b_full = bars + 4;                  // [RT_BST] bulk copy tx
   uint64_t* b_empty = b_full + RT_BST;          // [RT_BST] MMA commit
   uint64_t* acc_full = b_empty + RT_BST;        // [4] MMA commit -> epilogue
   uint64_t* acc_empty = acc_full + 4;           // [4] epilogue -> MMA
@@ -102,8 +107,7 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (n + RTM - 1) / RTM;
   if (tid == 0) {
-    tc::mbar_init(a_full, 128);
-    tc::mbar_init(a_empty, 1);
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(&a_full[a], 128); tc::mbar_init(&a_empty[a], 1); }
     for (int s = 0; s < RT_BST; ++s) { tc::mbar_init(&b_full[s], 1); tc::mbar_init(&b_empty[s], 1); }
     for (int b = 0; b < 4; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], RT_EPI); }
     tc::fence_mbar_init();
@@ -113,27 +117,39 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int nas = rt_a_slots(g);
+  const uint32_t tmem_a = tmem + (uint32_t)rt_a_base(g);   // A slot a: [hi kr | lo kr] columns
 
   if (warp < 4) {
-    // ------------------------------------------------------------ producers: US tile
-    uint32_t ph = 0;
-    const int kq = g.kr / 4;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      tc::mbar_wait(a_empty, ph ^ 1);
-      const int64_t p0 = t * RTM;
-      for (int idx = tid; idx < RTM * kq; idx += 128) {
-        const int p = idx / kq, c = idx - p * kq;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (p0 + p < n) v = __ldg(reinterpret_cast<const float4*>(US + (p0 + p) * (int64_t)ldus + 4 * c));
-        float4 hi, lo;
-        tc::split4(v, hi, lo);
-        const int off = (p >> 3) * g.a_sbo + c * A_LBO + (p & 7) * 16;
-        *reinterpret_cast<float4*>(a_hi + off) = hi;
-        *reinterpret_cast<float4*>(a_lo + off) = lo;
+    // ------------------------------------------------------------ producers: US tile -> TMEM
+    const int r = tid;                                        // pixel row = TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t ph[2] = {0, 0};
+    int64_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int a = (int)(it % nas);
+      tc::mbar_wait(&a_empty[a], ph[a] ^ 1);
+      ph[a] ^= 1;
+      tc::tc_fence_after();
+      const int64_t p = t * RTM + r;
+      const float* src = US + p * (int64_t)ldus;
+      const uint32_t ta = tmem_a + lane_off + (uint32_t)(a * 2 * g.kr);
+      for (int c = 0; c < g.kr; c += 8) {
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        if (p < n) {
+          v0 = __ldg(reinterpret_cast<const float4*>(src + c));
+          v1 = __ldg(reinterpret_cast<const float4*>(src + c + 4));
+        }
+        float hi[8], lo[8];
+        const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) tc::split_fast(x[i], hi[i], lo[i]);
+        tc::tmem_st8(ta + c, hi);
+        tc::tmem_st8(ta + g.kr + c, lo);
       }
-      tc::fence_proxy_async_smem();
-      tc::mbar_arrive(a_full);
-      ph ^= 1;
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&a_full[a]);
     }
   } else if (warp < 4 + RT_EPI / 32) {
     // ------------------------------------------------------------ epilogue
@@ -204,10 +220,9 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     // the loop; one elected lane issues -- descriptors stay in uniform registers)
     const uint32_t idesc = tc::make_idesc_tf32(RTM, g.N, false, false);
     const uint32_t sb = tc::smem_u32(bst);
-    const uint64_t dah0 = tc::make_sdesc(tc::smem_u32(a_hi), A_LBO, g.a_sbo);
-    const uint64_t dal0 = tc::make_sdesc(tc::smem_u32(a_lo), A_LBO, g.a_sbo);
     const uint64_t db00 = tc::make_sdesc(sb, B_LBO, g.b_sbo);
-    uint32_t a_ph = 0, bf_ph = 0, be_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
+    uint32_t a_ph[2] = {0, 0}, bf_ph = 0, be_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
+    int64_t it = 0;
     int64_t gq = 0;
     const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t total = my_tiles * g.nchunks;
@@ -222,10 +237,12 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
       __syncwarp();
     };
     for (int64_t q = 0; q < RT_BST - 1 && q < total; ++q) load_b(q);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      tc::mbar_wait(a_full, a_ph);
-      a_ph ^= 1;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int a = (int)(it % nas);
+      tc::mbar_wait(&a_full[a], a_ph[a]);
+      a_ph[a] ^= 1;
       tc::tc_fence_after();
+      const uint32_t tah = tmem_a + (uint32_t)(a * 2 * g.kr), tal = tah + (uint32_t)g.kr;
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
         if (gq + RT_BST - 1 < total) load_b(gq + RT_BST - 1);   // its stage was used by chunk gq - 1
         const int s = (int)(gq % RT_BST);
@@ -239,18 +256,17 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
         const uint64_t dbl0 = tc::sdesc_add(dbh0, (uint32_t)g.b_part);
         if (tc::elect_one()) {
           for (int ks = 0; ks < nks; ++ks) {
-            const uint32_t o = ks * 2 * A_LBO;   // A_LBO == B_LBO
-            tc::mma_tf32(d, tc::sdesc_add(dal0, o), tc::sdesc_add(dbh0, o), idesc, ks > 0 ? 1u : 0u);
-            tc::mma_tf32(d, tc::sdesc_add(dah0, o), tc::sdesc_add(dbl0, o), idesc, 1u);
-            tc::mma_tf32(d, tc::sdesc_add(dah0, o), tc::sdesc_add(dbh0, o), idesc, 1u);
+            const uint32_t o = ks * 2 * B_LBO;
+            tc::mma_tf32_ts(d, tal + ks * 8, tc::sdesc_add(dbh0, o), idesc, ks > 0 ? 1u : 0u);
+            tc::mma_tf32_ts(d, tah + ks * 8, tc::sdesc_add(dbl0, o), idesc, 1u);
+            tc::mma_tf32_ts(d, tah + ks * 8, tc::sdesc_add(dbh0, o), idesc, 1u);
           }
           tc::mma_commit(&b_empty[s]);
           tc::mma_commit(&acc_full[b]);
+          if (ch == g.nchunks - 1) tc::mma_commit(&a_empty[a]);
         }
         __syncwarp();
       }
-      if (tc::elect_one()) tc::mma_commit(a_empty);
-      __syncwarp();
     }
   }
   tc::tc_fence_before();
@@ -280,8 +296,7 @@ __global__ void build_bimg_kernel(const float* __restrict__ Bi, int k, int M, fl
 
 size_t rt_smem(int k, int M, int RT_BST) {
   const RtGeom g = rt_geom(k, M);
-  return (size_t)RT_NBUF * RT_PARTS * rt_box_region(g) + 2 * (size_t)g.a_bytes + RT_BST * (size_t)g.b_stage + 16 * 8 + 64 +
-         1024;
+  return (size_t)RT_NBUF * RT_PARTS * rt_box_region(g) + RT_BST * (size_t)g.b_stage + 20 * 8 + 64 + 1024;
 }
 
 }  // namespace
@@ -299,11 +314,13 @@ void launch_build_bimg(const float* Bi, int k, int M, float* bimg, cudaStream_t 
 void launch_reconstruct_tc(const float* US, int64_t n, int k, int ldus, const float* bimg, int M, void* out,
                            int out_imag_only, cudaStream_t s) {
   if (n <= 0) return;
-  size_t smem = rt_smem(k, M, 3);
-  const int bst = smem <= 227 * 1024 ? 3 : 2;
-  if (bst == 2) smem = rt_smem(k, M, 2);
+  const RtGeom g0 = rt_geom(k, M);
+  if (rt_a_base(g0) + 2 * g0.kr > 512) throw Status(10, "reconstruct_tc: k too large for tensor memory");
+  int bst = 4;
+  while (bst > 2 && rt_smem(k, M, bst) > 227 * 1024) --bst;
+  const size_t smem = rt_smem(k, M, bst);
   if (smem > 227 * 1024) throw Status(10, "reconstruct_tc: k too large for the smem tile");
-  auto kern = bst == 3 ? reconstruct_tc_kernel<3> : reconstruct_tc_kernel<2>;
+  auto kern = bst == 4 ? reconstruct_tc_kernel<4> : bst == 3 ? reconstruct_tc_kernel<3> : reconstruct_tc_kernel<2>;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
