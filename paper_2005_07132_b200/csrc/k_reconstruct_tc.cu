@@ -70,7 +70,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uin
 }
 
 __device__ __forceinline__ float2 cis_exp(float amp, float ph) {
-  const float kq = rintf(ph * 0.15915494309189535f);
+  // nearest integer by the 1.5 x 2^23 trick (two FADDs on the FMA pipe instead of FRND on the
+  // multi-function unit, which the sin / cos / ex2 already load; |ph| / 2 pi < 2^22)
+  const float kq = __fsub_rn(__fadd_rn(ph * 0.15915494309189535f, 12582912.0f), 12582912.0f);
   const float r = fmaf(-kq, 6.2831854820251465f, ph);
   const float r2 = fmaf(kq, 1.7484556e-07f, r);
   float sn, cs;
