@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one gram_tc launch (profiles/)
-GRAM_TRAFFIC = {"cfg3": 6.09e9}
+GRAM_TRAFFIC = {"cfg3": 7.73e9}   # ncu --set full, gram_pre_kernel at cfg3: dram read 7.32 GB + write 0.41 GB
 
 METRIC = "spectra/s for full fKK-EC (and direct KK) at 1/2/4/8 B200; % HBM/TC roofline"
 
@@ -172,12 +172,12 @@ def run_ours(args) -> dict:
     tf32_peak = peaks["bf16_tflops"] * (1.1 / 2.25)            # guide's nominal TF32/BF16 ratio
     peak_3x = tf32_peak / 3.0
     achieved = gram_flops / (gram_ms / 1e3) / 1e12
-    roofline = {"kernel": "gram_tc (F2, tcgen05 kind::tf32, 3xTF32 split)", "bound": "tensor", "achieved": achieved,
+    roofline = {"kernel": "gram_pre (F2, tcgen05 kind::tf32, 3xTF32 from the pre-split A0 image)", "bound": "tensor", "achieved": achieved,
                 "peak": peak_3x, "unit": "TFLOP/s", "frac": achieved / peak_3x,
                 "traffic": GRAM_TRAFFIC.get(args.workload),
                 "peak_source": f"{src} bf16 {peaks['bf16_tflops']:.0f} TF/s x 1.1/2.25 (TF32) / 3 (3xTF32 products); "
                                f"algorithmic flops = N*M^2 per pass; timed with CUDA events on the plan stream "
-                               f"(gram_tc + its fp64 split reduction)"}
+                               f"(gram_pre + its fp64 split reduction)"}
     # per-kernel-class rooflines of the other hot kernels (same event timing)
     hbm = peaks["hbm_gbs"]
     other = {}

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+CMD="python tools/run_once.py --workload cfg3 --direct-rows 0"
+timeout 600 $CMD > gpurun_out/plain_rt.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:reconstruct_tc_kernel|project_tma_kernel" -c 2 -o gpurun_out/prof_rt $CMD > gpurun_out/ncu_rt.log 2>&1; echo ncu=$?
