@@ -575,8 +575,17 @@ __device__ __forceinline__ int sturm_count_dev(const double* d, const double* e,
 // warp per eigenvalue index jj (jj-th largest); also computes ||T|| bounds
 __global__ void bisect_kernel(const double* __restrict__ d, const double* __restrict__ e, int M, int k,
                               double* __restrict__ lam, double* __restrict__ tnorm_out) {
-  const int lane = threadIdx.x & 31;
-  const int jj = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  extern __shared__ double bsm[];
+  double* sd = bsm;          // d
+  double* se2 = bsm + M;     // se2[i] = e[i-1]^2
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    sd[i] = d[i];
+    se2[i] = i > 0 ? e[i - 1] * e[i - 1] : 0.0;
+  }
+  __shared__ int gred[2][32];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int jj = blockIdx.x;   // one CTA per eigenvalue
   if (jj >= k) return;
   double gl = 1e300, gu = -1e300, tn = 0.0;
   for (int i = lane; i < M; i += 32) {
@@ -595,18 +604,88 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   const double pivmin = fmax(1e-300, tn * 1e-300);
   double lo = gl - 2.0 * eps * tn * M - 1e-300, hi = gu + 2.0 * eps * tn * M + 1e-300;
   const int idx = M - 1 - jj;   // ascending index
+  // 256-point multisection per round (one CTA of 128 threads per eigenvalue, 2 interleaved Sturm
+  // chains per thread).  The count uses the
+  // division-free three-term form p_{i+1} = (d_i - x) p_i - e_{i-1}^2 p_{i-1} (q_i = p_{i+1} / p_i,
+  // the LDL^T pivots of T - x I; #{q_i < 0} = #sign changes): one DFMA on the dependent chain per
+  // step instead of a reciprocal; rescaled by a power of two every 8 steps (the ratios, hence the
+  // signs, are unchanged).  Rounding: fl((d-x)p - e^2 p') = (...)(1 + delta) gives q_i with the same
+  // relative error per step as the ratio form.
+  constexpr int NCH = 2;
+  const int NPT = blockDim.x * NCH;   // points per round over the whole CTA
   for (int round = 0; round < 64; ++round) {
     if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-    const int c = sturm_count_dev(d, e, M, x, pivmin);
-    const unsigned ball = __ballot_sync(0xffffffffu, c > idx);
-    double xlo = __shfl_sync(0xffffffffu, x, ball ? (__ffs(ball) - 2 < 0 ? 0 : __ffs(ball) - 2) : 31);
-    double xhi = __shfl_sync(0xffffffffu, x, ball ? __ffs(ball) - 1 : 31);
-    if (ball == 0) { lo = xhi; }                       // eigenvalue above the last point
-    else if (__ffs(ball) == 1) { hi = xhi; }           // below the first point
-    else { lo = xlo; hi = xhi; }
+    const double w = (hi - lo) / (double)(NPT + 1);
+    double x[NCH], p1[NCH], p2[NCH];
+    int cnt[NCH];
+#pragma unroll
+    for (int u = 0; u < NCH; ++u) {
+      x[u] = lo + w * (double)(threadIdx.x * NCH + u + 1);   // point g = tid * NCH + u at lo + w (g + 1)
+      p2[u] = 1.0;
+      p1[u] = d[0] - x[u];
+      if (p1[u] == 0.0) p1[u] = -pivmin;
+      cnt[u] = p1[u] < 0.0 ? 1 : 0;
+    }
+    auto step = [&](double dvh, double evh) {
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        // an exact zero needs no pivmin patch here: with p_{i+1} = +-0, q_i and q_{i+1} = -e^2 p_i / 0
+        // have opposite signs, so the pair contributes exactly one negative pivot, as in the ratio
+        // form with q_i -> -pivmin
+        const double pn = fma(dvh - x[u], p1[u], -evh * p2[u]);
+        cnt[u] += (int)(((unsigned)__double2hiint(pn) ^ (unsigned)__double2hiint(p1[u])) >> 31);
+        p2[u] = p1[u];
+        p1[u] = pn;
+      }
+    };
+    auto rescale = [&]() {
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        const int ex = ((__double2hiint(p1[u]) >> 20) & 0x7ff) - 1023;
+        if (ex > 256 || ex < -256) {
+          const double sc = __hiloint2double((1023 - ex) << 20, 0);   // 2^-ex
+          p1[u] *= sc;
+          p2[u] *= sc;
+        }
+      }
+    };
+    int i = 1;
+    if (i + 8 <= M) {
+      // full blocks of 8 steps; the next block's (d, e^2) are loaded while this block computes
+      double dv[8], ev[8], dn[8], en[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) { dv[h] = sd[i + h]; ev[h] = se2[i + h]; }
+      for (; i + 8 <= M; i += 8) {
+        const bool more = i + 16 <= M;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          dn[h] = more ? sd[i + 8 + h] : 0.0;
+          en[h] = more ? se2[i + 8 + h] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) step(dv[h], ev[h]);
+        rescale();
+#pragma unroll
+        for (int h = 0; h < 8; ++h) { dv[h] = dn[h]; ev[h] = en[h]; }
+      }
+    }
+    for (; i < M; ++i) step(sd[i], se2[i]);
+    // first point (in ascending order) with more than idx eigenvalues below it
+    int g = NPT;
+#pragma unroll
+    for (int u = NCH - 1; u >= 0; --u)
+      if (cnt[u] > idx) g = threadIdx.x * NCH + u;
+    g = (int)__reduce_min_sync(0xffffffffu, (unsigned)g);
+    if (lane == 0) gred[round & 1][wid] = g;   // parity slots: one barrier per round
+    __syncthreads();
+    g = gred[round & 1][0];
+    for (int w2 = 1; w2 < nwarp; ++w2) g = min(g, gred[round & 1][w2]);
+    const double nlo = lo + w * (double)g;            // point g-1 (or lo)
+    const double nhi = g == NPT ? hi : lo + w * (double)(g + 1);
+    lo = nlo;
+    hi = nhi;
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     lam[jj] = 0.5 * (lo + hi);
     if (jj == 0) tnorm_out[0] = tn;
   }
@@ -1220,7 +1299,9 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     FKK_CUDA_CHECK(cudaMemcpyAsync(dbg_det, d, 3 * (size_t)M * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return;
   }
-  bisect_kernel<<<(k * 32 + 127) / 128, 128, 0, s>>>(d, e, M, k, lam, tnorm);
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(2 * (size_t)M * sizeof(double))));
+  bisect_kernel<<<k, 128, 2 * (size_t)M * sizeof(double), s>>>(d, e, M, k, lam, tnorm);
   check_launch("eig_bisect");
   const size_t ism = (size_t)5 * M * sizeof(double) + (size_t)M + 16;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));

@@ -60,6 +60,13 @@ __device__ __forceinline__ void arrive_on(uint64_t* bar, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
+// relaxed remote arrive (no MEMBAR.ALL.GPU): for signals that order no memory, e.g. "TMEM drained"
+// after tcgen05.wait::ld + tcgen05.fence::before_thread_sync
+__device__ __forceinline__ void arrive_on_relaxed(uint64_t* bar, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_on(&acc_empty[b], 0);   // one cluster-scope (membar-carrying) arrive per warp
+      if (lane == 0) arrive_on_relaxed(&acc_empty[b], 0);   // TMEM drained: orders no memory
       const bool last = pidx == nper - 1;
       if (last || ((pidx + 1) * PERIOD) % FLUSH == 0) {
 #pragma unroll
