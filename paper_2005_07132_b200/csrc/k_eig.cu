@@ -721,23 +721,37 @@ __global__ void __launch_bounds__(32) inviter_kernel(const double* __restrict__ 
   }
   __syncwarp();
   if (lane == 0) {
+    // LU with partial pivoting of the tridiagonal T - l I (LAPACK dgttrf order); the modified
+    // diagonal and super-diagonal entries of the next row travel in registers (no smem round trip
+    // on the dependent chain), reciprocals by MUFU seed + two Newton steps
+    double di = dd[0], ui = M > 1 ? du[0] : 0.0;
+#pragma unroll 2
     for (int i = 0; i < M - 1; ++i) {
-      if (fabs(dd[i]) >= fabs(dl[i])) {
-        if (dd[i] == 0.0) dd[i] = tiny;
-        const double f = dl[i] / dd[i];
+      const double li = dl[i], dnext = dd[i + 1];
+      const double unext = i < M - 2 ? du[i + 1] : 0.0;
+      double dn, un;
+      if (fabs(di) >= fabs(li)) {
+        if (di == 0.0) di = tiny;
+        const double f = li * fast_rcp(di);
         dl[i] = f;
-        dd[i + 1] -= f * du[i];
+        dd[i] = di;
+        du[i] = ui;
+        dn = dnext - f * ui;
+        un = unext;
       } else {
-        const double f = dd[i] / dl[i];
-        dd[i] = dl[i];
+        const double f = di * fast_rcp(li);
+        dd[i] = li;
         dl[i] = f;
-        const double tmp = du[i];
-        du[i] = dd[i + 1];
-        dd[i + 1] = tmp - f * dd[i + 1];
-        if (i < M - 2) { du2[i] = du[i + 1]; du[i + 1] = -f * du[i + 1]; }
+        du[i] = dnext;
+        dn = ui - f * dnext;
+        if (i < M - 2) du2[i] = unext;
+        un = -f * unext;
         piv[i] = 1;
       }
+      di = dn;
+      ui = un;
     }
+    dd[M - 1] = di;
   }
   __syncwarp();
   for (int i = lane; i < M; i += 32) {
@@ -748,14 +762,34 @@ __global__ void __launch_bounds__(32) inviter_kernel(const double* __restrict__ 
   __syncwarp();
   for (int it = 0; it < 3; ++it) {
     if (lane == 0) {
-      for (int i = 0; i < M - 1; ++i) {
-        const double bi = z[i], bi1 = z[i + 1];
-        if (piv[i]) { z[i] = bi1; z[i + 1] = bi - dl[i] * bi1; }
-        else { z[i + 1] = bi1 - dl[i] * bi; }
+      // forward: apply P and L^-1 (the running entry in a register)
+      double zi = z[0];
+#pragma unroll 4
+      for (int i = 0; i < M - 1; ++i) {   // branch-free: a = stored entry, b - f a = next running entry
+        const double bi1 = z[i + 1], f = dl[i];
+        const bool pv = piv[i] != 0;
+        const double a = pv ? bi1 : zi, b = pv ? zi : bi1;
+        z[i] = a;
+        zi = fma(-f, a, b);
       }
-      z[M - 1] *= dd[M - 1];
-      if (M > 1) z[M - 2] = (z[M - 2] - du[M - 2] * z[M - 1]) * dd[M - 2];
-      for (int i = M - 3; i >= 0; --i) z[i] = (z[i] - du[i] * z[i + 1] - du2[i] * z[i + 2]) * dd[i];
+      // backward: U^-1 (three-band), the two following entries in registers
+      double z1 = zi * dd[M - 1], z2 = 0.0;
+      z[M - 1] = z1;
+      if (M > 1) {
+        const double zz = (z[M - 2] - du[M - 2] * z1) * dd[M - 2];
+        z[M - 2] = zz;
+        z2 = z1;
+        z1 = zz;
+      }
+#pragma unroll 4
+      for (int i = M - 3; i >= 0; --i) {   // one DFMA on the dependent chain per step
+        const double r = dd[i];
+        const double t = fma(-du2[i], z2, z[i]) * r;
+        const double zz = fma(-du[i] * r, z1, t);
+        z[i] = zz;
+        z2 = z1;
+        z1 = zz;
+      }
     }
     __syncwarp();
     double nz = 0.0;
