@@ -1063,6 +1063,170 @@ __global__ void __launch_bounds__(32 * kBxW) backxform_reg_kernel(const double* 
   if (tid == 0) lam_out[jj] = lam[jj];
 }
 
+// Blocked back-transformation (compact WY).  Q = H_0 H_1 ... H_{M-3}, H_j = I - tau_j v_j v_j^T (v_j in
+// row j of Wk, entries c > j).  Blocks of kWyB consecutive reflectors: H_{j0} ... H_{j0+nb-1} =
+// I - V T V^T with T upper triangular (forward accumulation, LAPACK dlarft):
+//   T(i,i) = tau_i,  T(0:i, i) = -tau_i T(0:i, 0:i) (V(:, 0:i)^T v_i).
+// Each eigenvector z then needs one reduction per block (w = V^T z, all kWyB dots at once) instead of
+// one per reflector: y = B_0 (B_1 (... B_last z)).
+constexpr int kWyB = 16;   // reflectors per block: the block's V entries stay in registers between w = V^T z and z -= V w'
+
+// one CTA per block: S = V^T V (upper), then the T recurrence on warp 0
+__global__ void __launch_bounds__(256) wy_t_kernel(const double* __restrict__ Wk, const double* __restrict__ tau, int M,
+                                                   int nrefl, double* __restrict__ Tout) {
+  extern __shared__ double vs[];   // [kWyB][M]: the block's reflectors (zero at c <= j)
+  __shared__ double S[kWyB][kWyB + 1];
+  __shared__ double T[kWyB][kWyB + 1];
+  const int p = blockIdx.x, j0 = p * kWyB, nb = min(kWyB, nrefl - j0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int q = threadIdx.x; q < kWyB * M; q += blockDim.x) {
+    const int a = q / M, c = q - a * M;
+    vs[q] = (a < nb && c > j0 + a) ? Wk[(int64_t)(j0 + a) * M + c] : 0.0;
+  }
+  __syncthreads();
+  for (int q = warp; q < kWyB * kWyB; q += nw) {
+    const int a = q / kWyB, b = q - a * kWyB;
+    if (a > b) continue;
+    double acc = 0.0;
+    for (int c = j0 + b + 1 + lane; c < M; c += 32) acc = fma(vs[a * M + c], vs[b * M + c], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) S[a][b] = acc;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int r = lane;
+    for (int i = 0; i < kWyB; ++i) {
+      const double ti = i < nb ? tau[j0 + i] : 0.0;
+      const double y = (r < i) ? S[r < kWyB ? r : 0][i] : 0.0;
+      double w = 0.0;
+      for (int c = 0; c < i; ++c) {
+        const double yc = __shfl_sync(0xffffffffu, y, c);
+        if (r <= c) w = fma(T[r][c], yc, w);
+      }
+      if (r < kWyB) T[r][i] = r < i ? -ti * w : (r == i ? ti : 0.0);
+      __syncwarp();
+    }
+    for (int q = lane; q < kWyB * kWyB; q += 32) Tout[(int64_t)p * kWyB * kWyB + q] = T[q / kWyB][q % kWyB];
+  }
+}
+
+// sum over the 32 lanes of kWyB (16) per-lane values v[]: on return lane l holds the sum of column
+// l mod 16 (recursive halving: 8 + 4 + 2 + 1 shuffles, then one xor-16 add)
+__device__ __forceinline__ double transpose_sum16(double (&v)[kWyB]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = kWyB / 2; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = upper ? v[i] : v[i + h];
+      const double keep = upper ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+// one eigenvector per CTA (entries in registers, c = tid + NT u); blocks applied last to first
+template <int NPL>
+__global__ void __launch_bounds__(32 * kBxW) backxform_wy_kernel(const double* __restrict__ Wk, const double* __restrict__ Tg,
+                                                                 int M, int nrefl, int k, const double* __restrict__ Z,
+                                                                 const double* __restrict__ lam, double* __restrict__ V,
+                                                                 double* __restrict__ lam_out) {
+  constexpr int NT = 32 * kBxW;
+  __shared__ double red[2][kBxW][kWyB];   // parity-buffered: one barrier pair per block
+  __shared__ double wv[2][kWyB];
+  __shared__ double bestv[kBxW], bestm[kBxW];
+  __shared__ int besti[kBxW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int jj = blockIdx.x;
+  double zr[NPL];
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    zr[u] = c < M ? Z[(int64_t)jj * M + c] : 0.0;
+  }
+  const int nblk = (nrefl + kWyB - 1) / kWyB;
+  for (int p = nblk - 1; p >= 0; --p) {
+    const int j0 = p * kWyB, nb = min(kWyB, nrefl - j0);
+    // the block's V entries of this thread's rows (registers), loaded in one batch
+    double vr[kWyB][NPL];
+#pragma unroll
+    for (int i = 0; i < kWyB; ++i) {
+      const double* vi = Wk + (int64_t)(j0 + i) * M;
+#pragma unroll
+      for (int u = 0; u < NPL; ++u) {
+        const int c = tid + NT * u;
+        vr[i][u] = (i < nb && c > j0 + i && c < M) ? __ldg(vi + c) : 0.0;
+      }
+    }
+    // w = V^T z: per-thread partials of all dots, lane-transposed warp sums, 8-warp sum
+    double part[kWyB];
+#pragma unroll
+    for (int i = 0; i < kWyB; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int u = 0; u < NPL; ++u) a = fma(vr[i][u], zr[u], a);
+      part[i] = a;
+    }
+    const double ws = transpose_sum16(part);
+    if (lane < kWyB) red[p & 1][warp][lane] = ws;
+    __syncthreads();
+    if (warp == 0) {
+      double w = 0.0;
+      if (lane < kWyB) {
+#pragma unroll
+        for (int w2 = 0; w2 < kBxW; ++w2) w += red[p & 1][w2][lane];
+      }
+      // w' = T w (T upper triangular): lane r sums T(r, c) w_c for c >= r
+      const double* T = Tg + (int64_t)p * kWyB * kWyB;
+      double tw = 0.0;
+#pragma unroll
+      for (int c = 0; c < kWyB; ++c) {
+        const double wc = __shfl_sync(0xffffffffu, w, c);
+        if (lane < kWyB && c >= lane) tw = fma(__ldg(T + lane * kWyB + c), wc, tw);
+      }
+      if (lane < kWyB) wv[p & 1][lane] = tw;
+    }
+    __syncthreads();
+    // z -= V w'
+#pragma unroll
+    for (int i = 0; i < kWyB; ++i) {
+      const double wi = wv[p & 1][i];
+#pragma unroll
+      for (int u = 0; u < NPL; ++u) zr[u] = fma(-wi, vr[i][u], zr[u]);
+    }
+  }
+  // sign rule: entry of largest |.| positive, ties -> lowest index
+  double best = -1.0, bval = 0.0;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    if (c < M && fabs(zr[u]) > best) { best = fabs(zr[u]); bi = c; bval = zr[u]; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const double ov = __shfl_xor_sync(0xffffffffu, bval, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; bval = ov; }
+  }
+  if (lane == 0) { bestv[warp] = bval; besti[warp] = bi; bestm[warp] = best; }
+  __syncthreads();
+  double gb = bestm[0], gv = bestv[0];
+  int gi = besti[0];
+  for (int w2 = 1; w2 < kBxW; ++w2)
+    if (bestm[w2] > gb || (bestm[w2] == gb && besti[w2] < gi)) { gb = bestm[w2]; gi = besti[w2]; gv = bestv[w2]; }
+  const double sg = gv < 0.0 ? -1.0 : 1.0;
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int c = tid + NT * u;
+    if (c < M) V[(int64_t)jj * M + c] = sg * zr[u];
+  }
+  if (tid == 0) lam_out[jj] = lam[jj];
+}
+
 // Re-orthogonalisation by CholeskyQR, applied twice (CholQR2): S = Z Z^T (k x k), S = R^T R,
 // Z <- R^{-T} Z.  In exact arithmetic this is classical Gram-Schmidt of the vectors in their
 // (descending-eigenvalue) order -- the same result as reorth_kernel -- but parallel over M.
@@ -1205,7 +1369,8 @@ __global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __rest
 
 size_t eig_workspace_doubles(int M, int k) {
   // d, e, tau (3M) + p / LL words (16M) + lam, tnorm (k+1) + Z, Z2, Z3 (3kM) + S, T (2k^2) + flag + A (M*M)
-  return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 18 + (size_t)M * M;
+  return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 18 + (size_t)M * M +
+         ((size_t)(M + kWyB - 1) / kWyB) * kWyB * kWyB;   // + compact-WY T blocks
 }
 
 int eig_path_rows_resident(int M) {
@@ -1371,6 +1536,19 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t rsm = ((size_t)(kBxStages + 1) * M + 2 * kBxW) * sizeof(double);
+  static const int bx_mode = getenv("FKK_BACKXFORM_MODE") ? atoi(getenv("FKK_BACKXFORM_MODE")) : 1;   // A/B only
+  if (bx_mode == 1 && M >= 3 && M <= 32 * kBxW * 4) {   // (NPL = 8 would spill the register-cached V block)
+    const int nrefl = M - 2, nblk = (nrefl + kWyB - 1) / kWyB;
+    double* Tg = A + (size_t)M * M;
+    const size_t tsm = (size_t)kWyB * M * sizeof(double);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(wy_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    wy_t_kernel<<<nblk, 256, tsm, s>>>(A, tau, M, nrefl, Tg);
+    check_launch("eig_wy_t");
+    if (M <= 32 * kBxW * 2) backxform_wy_kernel<2><<<k, 32 * kBxW, 0, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
+    else backxform_wy_kernel<4><<<k, 32 * kBxW, 0, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
+    check_launch("eig_backxform_wy");
+    return;
+  }
   if (M >= 3 && M <= 32 * kBxW * 8 && rsm <= (size_t)maxsm) {
 #define FKK_BX_REG(NPL)                                                                                  \
     {                                                                                                    \
