@@ -1251,36 +1251,53 @@ __global__ void gram_rows_kernel(const double* __restrict__ Z, int M, int k, dou
 __global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ S, int k, double* __restrict__ Tout,
                                                        int* __restrict__ fallback) {
   extern __shared__ __align__(16) double sc[];
-  double* Rm = sc;          // k x k
-  double* Tm = sc + k * k;  // k x k
+  double* Wm = sc;          // k x k working copy (upper triangle), then T
+  double* Rm = sc + k * k;  // k x k: R (upper)
+  double* rinv = Rm + k * k;  // k: 1 / R[c][c]
+  double* sdiag = rinv + k;   // k: the original diagonal (pivot-loss test without a global load per column)
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < k * k; i += nt) { Rm[i] = S[i]; Tm[i] = 0.0; }
+  for (int i = tid; i < k * k; i += nt) { Wm[i] = S[i]; Rm[i] = 0.0; }
+  for (int i = tid; i < k; i += nt) sdiag[i] = S[i * k + i];
   __syncthreads();
-  // right-looking Cholesky on the upper triangle: R[c][c] = sqrt(S[c][c]), R[c][j] /= R[c][c], trailing update
+  // right-looking Cholesky, one barrier per column: row c of R from the working row, and the
+  // trailing update W[i][j] -= W[c][i] W[c][j] / W[c][c] (row c is not written in this phase)
   for (int c = 0; c < k; ++c) {
-    const double dcc = Rm[c * k + c];
-    const double rcc = dcc > 0.0 ? sqrt(dcc) : 0.0;
-    __syncthreads();
+    const double dcc = Wm[c * k + c];
+    const bool ok = dcc > 0.0;
+    const double rcc = ok ? sqrt(dcc) : 0.0;
+    const double ircc = ok ? 1.0 / rcc : 0.0, idcc = ok ? 1.0 / dcc : 0.0;
     // a pivot that lost ~12 digits: the vectors are (numerically) dependent -> robust fallback
-    if (tid == 0 && !(dcc > 1e-8 * S[c * k + c])) atomicOr(fallback, 1);
-    for (int j = c + 1 + tid; j < k; j += nt) Rm[c * k + j] = rcc > 0.0 ? Rm[c * k + j] / rcc : 0.0;
-    __syncthreads();
-    if (tid == 0) Rm[c * k + c] = rcc;
-    for (int e2 = tid; e2 < (k - c - 1) * (k - c - 1); e2 += nt) {
-      const int i = c + 1 + e2 / (k - c - 1), j = c + 1 + e2 % (k - c - 1);
-      if (j >= i) Rm[i * k + j] -= Rm[c * k + i] * Rm[c * k + j];
+    if (tid == 0) {
+      if (!(dcc > 1e-8 * sdiag[c])) atomicOr(fallback, 1);
+      rinv[c] = ok ? ircc : 0.0;
+    }
+    for (int j = c + tid; j < k; j += nt) Rm[c * k + j] = j == c ? rcc : Wm[c * k + j] * ircc;
+    // 2-D thread grid (16 x 16) over the trailing upper triangle: no integer division per element
+    for (int i = c + 1 + (tid >> 4); i < k; i += nt >> 4) {
+      const double wci = Wm[c * k + i] * idcc;
+      for (int j = i + (tid & 15); j < k; j += 16) Wm[i * k + j] -= wci * Wm[c * k + j];
     }
     __syncthreads();
   }
-  // T = R^{-1}: column j of T solves R t = e_j (back substitution), thread per column
-  for (int j = tid; j < k; j += nt) {
-    for (int i = j; i >= 0; --i) {
-      double sacc = i == j ? 1.0 : 0.0;
-      for (int l = i + 1; l <= j; ++l) sacc -= Rm[i * k + l] * Tm[l * k + j];
-      Tm[i * k + j] = Rm[i * k + i] > 0.0 ? sacc / Rm[i * k + i] : 0.0;
-    }
-  }
+  // T = R^{-1} (upper) by right-looking back substitution, one barrier per row: acc starts as I;
+  // at step i (bottom up) row i of acc is final, T[i][j] = acc[i][j] / R[i][i], and every row r < i
+  // takes acc[r][j] -= R[r][i] T[i][j] (parallel over (r, j); row i itself is only read)
+  double* acc = Wm;
+  for (int q = tid; q < k * k; q += nt) acc[q] = (q / k == q % k) ? 1.0 : 0.0;
   __syncthreads();
+  for (int i = k - 1; i >= 0; --i) {
+    const double ri = rinv[i];
+    for (int r = tid >> 4; r <= i; r += nt >> 4) {
+      const double rri = r < i ? Rm[r * k + i] : 0.0;
+      for (int j = i + (tid & 15); j < k; j += 16) {
+        const double tij = acc[i * k + j] * ri;
+        if (r < i) acc[r * k + j] -= rri * tij;
+        else Rm[i * k + j] = tij;   // r == i: park T[i][j] in R's (now dead) row i
+      }
+    }
+    __syncthreads();
+  }
+  double* Tm = Rm;
   for (int i = tid; i < k * k; i += nt) Tout[i] = Tm[i];
 }
 
@@ -1510,7 +1527,7 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   // Z -> Z2 -> Z3; a near-singular Gram switches to the Gram-Schmidt fallback (Z -> Z3)
   double* Zf = Z3;
   if (k <= 128) {
-    const size_t csm = 2 * (size_t)k * k * sizeof(double);
+    const size_t csm = (2 * (size_t)k * k + 2 * k) * sizeof(double);
     FKK_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     FKK_CUDA_CHECK(cudaMemsetAsync(fallback, 0, sizeof(int), s));
     const int npairs = k * (k + 1) / 2;
