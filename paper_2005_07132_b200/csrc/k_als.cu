@@ -16,6 +16,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fkk_internal.h"
@@ -89,15 +90,48 @@ __device__ __forceinline__ int seg_of(int col, int M, int P) {
   return s;
 }
 
-template <typename TY, typename TZ>
-__global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, int64_t n, int M, int P, int T,
+// lane exchange among the NL threads of one spectrum: out = mine of lane src (src clamped; callers
+// ignore out-of-range sources).  NL = 32: shuffles; NL = 64 (two warps): through shared memory.
+template <int NL, int W>
+__device__ __forceinline__ void lane_get2(const double (&mine)[W], int src1, double (&out1)[W], int src2,
+                                          double (&out2)[W], double* xs) {
+  if constexpr (NL == 32) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      out1[i] = __shfl_sync(0xffffffffu, mine[i], src1 & 31);
+      out2[i] = __shfl_sync(0xffffffffu, mine[i], src2 & 31);
+    }
+  } else {
+    __syncthreads();   // the previous exchange's reads are done
+#pragma unroll
+    for (int i = 0; i < W; ++i) xs[i * NL + threadIdx.x] = mine[i];
+    __syncthreads();
+    const int a = min(max(src1, 0), NL - 1), b = min(max(src2, 0), NL - 1);
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      out1[i] = xs[i * NL + a];
+      out2[i] = xs[i * NL + b];
+    }
+  }
+}
+template <int NL>
+__device__ __forceinline__ void spectrum_sync() {
+  if constexpr (NL == 32) __syncwarp();
+  else __syncthreads();
+}
+
+// NL threads (one or two warps) per spectrum, P <= NL segments: two warps halve the dependent chain
+// of every lane (the solver is latency-bound at ~7 spectra per SM, the shared-memory limit)
+template <typename TY, typename TZ, int NL>
+__global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, int64_t n, int M, int P, int T,
                                                       double lam, double p, int iters, TZ* __restrict__ z) {
   extern __shared__ __align__(16) double sh[];
   double* sl1 = sh;                  // [T][32] l1 of the current factorisation
-  double* srd = sl1 + 32 * T;        // [T][32] 1/D
-  double* sg = srd + 32 * T;         // [T][32] g = D^-1 L^-1 f~   (finally: z)
-  TY* sy = reinterpret_cast<TY*>(sg + 32 * T);                          // [T][32] y (input precision)
-  unsigned char* sw = reinterpret_cast<unsigned char*>(sy + 32 * T);   // [T][32] w: 1 -> p, 0 -> 1-p
+  double* srd = sl1 + NL * T;        // [T][NL] 1/D
+  double* sg = srd + NL * T;         // [T][NL] g = D^-1 L^-1 f~   (finally: z)
+  double* xs = sg + NL * T;          // [10][NL] lane-exchange scratch (NL = 64)
+  TY* sy = reinterpret_cast<TY*>(xs + (NL == 64 ? 10 * NL : 0));     // [T][NL] y (input precision)
+  unsigned char* sw = reinterpret_cast<unsigned char*>(sy + NL * T);   // [T][NL] w: 1 -> p, 0 -> 1-p
   const int s = threadIdx.x;
   const bool act = s < P;
   const int b = act ? seg_b(s, M, P) : M, e = act ? seg_b(s + 1, M, P) : M;
@@ -110,16 +144,16 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
 
   for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
     const TY* yr = y + row * (int64_t)M;
-    __syncwarp();
-    for (int col = s; col < M; col += 32) {           // coalesced read, scatter to [t][lane]
+    spectrum_sync<NL>();
+    for (int col = s; col < M; col += NL) {           // coalesced read, scatter to [t][lane]
       const int sc = seg_of(col, M, P);
-      sy[(col - seg_b(sc, M, P)) * 32 + sc] = yr[col];
+      sy[(col - seg_b(sc, M, P)) * NL + sc] = yr[col];
     }
-    __syncwarp();
+    spectrum_sync<NL>();
     double2 xL = make_double2(0.0, 0.0), xR = make_double2(0.0, 0.0);   // separator values (left: S_{s-1})
     for (int it = 0; it <= iters; ++it) {
       const bool dr = it & 1;                 // 0: ascending elimination, 1: descending
-      const int ix0 = dr ? (nn - 1) * 32 + s : s, dix = dr ? -32 : 32;
+      const int ix0 = dr ? (nn - 1) * NL + s : s, dix = dr ? -NL : NL;
       const int i0 = dr ? b + nn - 1 : b, di = dr ? -1 : 1;
       const int na = dr ? e - 2 : b - 1;      // near-adjacent separator row
       const bool hasN = dr ? hasR : hasL, hasF = dr ? hasL : hasR;
@@ -136,8 +170,10 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
         constexpr bool BSUB = decltype(bsub_c)::value, FACT = decltype(fact_c)::value;
         int ix = ix0, i = i0;
         // one row in elimination order; ea/eb = near-spike entries (t < 2), LASTROW: l1 = 0
-        auto step = [&](auto last_c, double ea, double eb) {
-          constexpr bool LASTROW = decltype(last_c)::value;
+        // EDGE: this position may hold one of the rows 0, 1, M-2, M-1 (where D^T D's band differs);
+        // only the peeled positions t = 0, 1, nn-2, nn-1 can, so the main loop runs without the check
+        auto step = [&](auto last_c, auto edge_c, double ea, double eb) {
+          constexpr bool LASTROW = decltype(last_c)::value, EDGE = decltype(edge_c)::value;
           const double yv = (double)sy[ix];
           double wv = 1.0;
           if constexpr (BSUB) {
@@ -151,7 +187,9 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
           }
           if constexpr (FACT) {
             double ld0 = lam6, ld1 = lamm4;
-            if (edge) { ld0 = lam * d0v(i, M); ld1 = lam * d1v(dr ? i - 1 : i, M); }
+            if constexpr (EDGE) {
+              if (edge) { ld0 = lam * d0v(i, M); ld1 = lam * d1v(dr ? i - 1 : i, M); }
+            }
             const double D = (wv + ld0) - L1m1 * L1m1 * Dm1 - lam2 * rDm2;
             const double rd = rcp64n1(D);
             const double l1n = LASTROW ? 0.0 : (ld1 - lam * L1m1) * rd;
@@ -180,12 +218,13 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
           i += di;
         };
         if (nn == 0) return;                      // lanes beyond the P segments
-        step(F_{}, ea0, eb0);                     // t = 0   (nn >= 2 on active lanes)
-        if (nn == 2) { step(T_{}, ea1, 0.0); return; }
-        step(F_{}, ea1, 0.0);                     // t = 1
+        step(F_{}, T_{}, ea0, eb0);               // t = 0   (nn >= 2 on active lanes)
+        if (nn == 2) { step(T_{}, T_{}, ea1, 0.0); return; }
+        step(F_{}, T_{}, ea1, 0.0);               // t = 1
 #pragma unroll 2
-        for (int t = 2; t < nn - 1; ++t) step(F_{}, 0.0, 0.0);
-        step(T_{}, 0.0, 0.0);                     // t = nn - 1
+        for (int t = 2; t < nn - 2; ++t) step(F_{}, F_{}, 0.0, 0.0);
+        if (nn >= 4) step(F_{}, T_{}, 0.0, 0.0);  // t = nn - 2
+        step(T_{}, T_{}, 0.0, 0.0);               // t = nn - 1
       };
       if (it == 0) passA(F_{}, T_{});
       else if (it < iters) passA(T_{}, T_{});
@@ -233,13 +272,21 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
         CfL = make_double2(Cf_fb, Cf_fa);
       }
       // ---------------- reduced block-tridiagonal system on the separators, lane s <-> S_s
-      const M2 nLL = shfl(CLL, 1, false), nLR = shfl(CLR, 1, false);
-      const double2 nCfL = shflv(CfL, 1, false);
+      M2 nLL, nLR;
+      double2 nCfL;
+      {   // from lane s + 1
+        const double mine[10] = {CLL.a, CLL.b, CLL.c, CLL.d, CLR.a, CLR.b, CLR.c, CLR.d, CfL.x, CfL.y};
+        double o[10], o2[10];
+        lane_get2<NL, 10>(mine, s + 1, o, s + 1, o2, xs);
+        nLL = {o[0], o[1], o[2], o[3]};
+        nLR = {o[4], o[5], o[6], o[7]};
+        nCfL = make_double2(o[8], o[9]);
+      }
       M2 Dk = {1.0, 0.0, 0.0, 1.0}, Uk = {0.0, 0.0, 0.0, 0.0};
       double2 rk = make_double2(0.0, 0.0);
       if (hasR) {
         const int i0s = e - 2, i1s = e - 1;
-        const int l0 = (i0s - b) * 32 + s, l1x = (i1s - b) * 32 + s;
+        const int l0 = (i0s - b) * NL + s, l1x = (i1s - b) * NL + s;
         const double w0 = it == 0 ? 1.0 : (sw[l0] ? p : q);
         const double w1 = it == 0 ? 1.0 : (sw[l1x] ? p : q);
         const double off = lam * d1v(i0s, M);
@@ -248,18 +295,33 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
         Uk = {-nLR.a, -nLR.b, -nLR.c, -nLR.d};
         rk = make_double2(w0 * (double)sy[l0] - CfR.x - nCfL.x, w1 * (double)sy[l1x] - CfR.y - nCfL.y);
       }
-      M2 Lk = shfl(Uk, 1, true);
+      M2 Lk;
+      {   // from lane s - 1
+        const double mine[4] = {Uk.a, Uk.b, Uk.c, Uk.d};
+        double o[4], o2[4];
+        lane_get2<NL, 4>(mine, s - 1, o, s - 1, o2, xs);
+        Lk = {o[0], o[1], o[2], o[3]};
+      }
       Lk = {Lk.a, Lk.c, Lk.b, Lk.d};   // transpose
       if (s == 0 || !hasR) Lk = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int h = 1; h < 32; h <<= 1) {
+      for (int h = 1; h < NL; h <<= 1) {
         const M2 Di = inv(Dk);
         const M2 Pm = mul(Di, Lk), Qm = mul(Di, Uk);
         const double2 sv = mulv(Di, rk);
-        const M2 Pdn = shfl(Pm, h, true), Qdn = shfl(Qm, h, true);
-        const double2 sdn = shflv(sv, h, true);
-        const M2 Pup = shfl(Pm, h, false), Qup = shfl(Qm, h, false);
-        const double2 sup = shflv(sv, h, false);
+        M2 Pdn, Qdn, Pup, Qup;
+        double2 sdn, sup;
+        {   // from lanes s - h and s + h
+          const double mine[10] = {Pm.a, Pm.b, Pm.c, Pm.d, Qm.a, Qm.b, Qm.c, Qm.d, sv.x, sv.y};
+          double dn[10], up[10];
+          lane_get2<NL, 10>(mine, s - h, dn, s + h, up, xs);
+          Pdn = {dn[0], dn[1], dn[2], dn[3]};
+          Qdn = {dn[4], dn[5], dn[6], dn[7]};
+          sdn = make_double2(dn[8], dn[9]);
+          Pup = {up[0], up[1], up[2], up[3]};
+          Qup = {up[4], up[5], up[6], up[7]};
+          sup = make_double2(up[8], up[9]);
+        }
         M2 nL = {0.0, 0.0, 0.0, 0.0}, nU = {0.0, 0.0, 0.0, 0.0};
         if (s - h >= 0) {
           const M2 a1 = mul(Lk, Pdn), a2 = mul(Lk, Qdn);
@@ -268,7 +330,7 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
           Dk = {Dk.a - a2.a, Dk.b - a2.b, Dk.c - a2.c, Dk.d - a2.d};
           rk = make_double2(rk.x - a3.x, rk.y - a3.y);
         }
-        if (s + h < 32) {
+        if (s + h < NL) {
           const M2 b1 = mul(Uk, Qup), b2 = mul(Uk, Pup);
           const double2 b3 = mulv(Uk, sup);
           nU = {-b1.a, -b1.b, -b1.c, -b1.d};
@@ -279,10 +341,15 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
         Uk = nU;
       }
       xR = hasR ? mulv(inv(Dk), rk) : make_double2(0.0, 0.0);
-      xL = shflv(xR, 1, true);
+      {   // from lane s - 1
+        const double mine[2] = {xR.x, xR.y};
+        double o[2], o2[2];
+        lane_get2<NL, 2>(mine, s - 1, o, s - 1, o2, xs);
+        xL = make_double2(o[0], o[1]);
+      }
       if (!hasL) xL = make_double2(0.0, 0.0);
       if (hasR) {   // separator values of this solve; weights for the next
-        const int l0 = (e - 2 - b) * 32 + s, l1x = (e - 1 - b) * 32 + s;
+        const int l0 = (e - 2 - b) * NL + s, l1x = (e - 1 - b) * NL + s;
         sg[l0] = xR.x;
         sg[l1x] = xR.y;
         sw[l0] = (double)sy[l0] > xR.x ? 1 : 0;
@@ -330,48 +397,67 @@ __global__ void __launch_bounds__(32) als_part_kernel(const TY* __restrict__ y, 
       }
     }
     // ---------------- write z (interior from the last back-substitution, separators from the last solve)
-    __syncwarp();
+    spectrum_sync<NL>();
     TZ* zr = z + row * (int64_t)M;
-    for (int col = s; col < M; col += 32) {
+    for (int col = s; col < M; col += NL) {
       const int sc = seg_of(col, M, P);
-      zr[col] = (TZ)sg[(col - seg_b(sc, M, P)) * 32 + sc];
+      zr[col] = (TZ)sg[(col - seg_b(sc, M, P)) * NL + sc];
     }
   }
 }
 
 }  // namespace
 
+// lanes per spectrum: 32 (one warp).  The two-warp variant (64 segments, FKK_ALS_LANES=64) halves every
+// lane's dependent chain but adds a PCR level and shared-memory lane exchanges; measured on cfg3 rows it
+// is no faster (13.06 vs 12.95 ms per 131,072 spectra: the extra exchange/separator work eats the gain)
+static int als_lanes(int M) {
+  const char* ev = getenv("FKK_ALS_LANES");
+  const int want = ev ? atoi(ev) : 32;
+  return (want == 64 && M / 4 >= 64) ? 64 : 32;
+}
+
 size_t als_part_smem(int M, int y_f64) {
-  const int P = M / 4 < 32 ? M / 4 : 32;
+  const int NL = als_lanes(M);
+  const int P = M / 4 < NL ? M / 4 : NL;
   if (P < 2) return 0;
   const int T = (M + P - 1) / P;
-  return (size_t)32 * T * (3 * sizeof(double) + (y_f64 ? 8 : 4) + 1);
+  return (size_t)NL * T * (3 * sizeof(double) + (y_f64 ? 8 : 4) + 1) + (NL == 64 ? 10 * (size_t)NL * sizeof(double) : 0);
 }
 
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
                      cudaStream_t s) {
-  const int P = M / 4 < 32 ? M / 4 : 32;
+  const int NL = als_lanes(M);
+  const int P = M / 4 < NL ? M / 4 : NL;
   if (P < 2 || n <= 0) return false;
   const int T = (M + P - 1) / P;
-  const size_t sm = als_part_smem(M, y_f64);
+  const size_t sm = (size_t)NL * T * (3 * sizeof(double) + (y_f64 ? 8 : 4) + 1) +
+                    (NL == 64 ? 10 * (size_t)NL * sizeof(double) : 0);
   int dev = 0, sms = 148, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (sm > (size_t)maxsm) return false;
-#define FKK_ALS_PART(TY, TZ)                                                                          \
+#define FKK_ALS_PART(TY, TZ, L)                                                                       \
   {                                                                                                   \
-    auto kf = als_part_kernel<TY, TZ>;                                                                \
+    auto kf = als_part_kernel<TY, TZ, L>;                                                             \
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
     int per = 1;                                                                                      \
-    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, 32, sm));                  \
+    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, L, sm));                   \
     const int64_t g = std::min<int64_t>(n, (int64_t)sms * std::max(per, 1));                         \
-    kf<<<(unsigned)g, 32, sm, s>>>((const TY*)y, n, M, P, T, lam, p, iters, (TZ*)z);                  \
+    kf<<<(unsigned)g, L, sm, s>>>((const TY*)y, n, M, P, T, lam, p, iters, (TZ*)z);                   \
   }
-  if (y_f64 && z_f64) FKK_ALS_PART(double, double)
-  else if (!y_f64 && !z_f64) FKK_ALS_PART(float, float)
-  else if (!y_f64 && z_f64) FKK_ALS_PART(float, double)
-  else FKK_ALS_PART(double, float)
+#define FKK_ALS_TYPES(L)                                                                              \
+  if (y_f64 && z_f64) FKK_ALS_PART(double, double, L)                                                 \
+  else if (!y_f64 && !z_f64) FKK_ALS_PART(float, float, L)                                            \
+  else if (!y_f64 && z_f64) FKK_ALS_PART(float, double, L)                                            \
+  else FKK_ALS_PART(double, float, L)
+  if (NL == 64) {
+    FKK_ALS_TYPES(64)
+  } else {
+    FKK_ALS_TYPES(32)
+  }
+#undef FKK_ALS_TYPES
 #undef FKK_ALS_PART
   check_launch("als_part");
   return true;

@@ -80,6 +80,19 @@ def test_direct_segment_edge_sizes(torch_cuda, fkk, M):
     assert _rel_inf(K, K_or) <= 1e-5
 
 
+@pytest.mark.parametrize("M", [256, 1000])
+def test_direct_two_warp_als(torch_cuda, fkk, M, monkeypatch):
+    """The opt-in two-warp ALS (64 segments per spectrum, shared-memory lane exchanges, 6 PCR
+    levels): M = 256 gives 4-row segments (2-row interiors)."""
+    monkeypatch.setenv("FKK_ALS_LANES", "64")
+    cfg = CONFIGS["cfg1"].with_(height=4, width=9, n_freq=M)
+    I, Iref, _ = generate(cfg)
+    K_or = O.kk_direct(I, Iref, O.Params())
+    plan = fkk.Plan(M, 4, I.shape[0], in_dtype="f64")
+    K = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
+    assert _rel_inf(K, K_or) <= 1e-5
+
+
 def test_direct_passthrough_and_scale(torch_cuda, fkk):
     rng = np.random.default_rng(1)
     Iref = rng.uniform(0.5, 1.5, 1000).astype(np.float32)

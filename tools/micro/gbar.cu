@@ -75,6 +75,27 @@ __device__ __forceinline__ void split(unsigned* ctr, unsigned* flag, unsigned ep
   }
   __syncthreads();
 }
+// all-poll: every CTA publishes its epoch in its own word; threads 0..P-1 of every CTA poll one
+// word each (packed: 32 words per 128-B line) -- no atomics, one hop
+__device__ __forceinline__ void allpoll(unsigned* fl, unsigned epoch, int stride) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fl + blockIdx.x * stride), "r"(epoch) : "memory");
+  if (threadIdx.x < gridDim.x) {
+    unsigned v;
+    do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + threadIdx.x * stride) : "memory"); } while ((int)(v - epoch) < 0);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void allpoll_relaxed(unsigned* fl, unsigned epoch, int stride) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fl + blockIdx.x * stride), "r"(epoch) : "memory");
+  if (threadIdx.x < gridDim.x) {
+    unsigned v;
+    do { asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + threadIdx.x * stride) : "memory"); } while ((int)(v - epoch) < 0);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  __syncthreads();
+}
 __global__ void kbar(int mode, int iters, int nst, unsigned* ctr, unsigned* fl, double* scratch) {
   unsigned target = 0, ncl = 1, rank = 0;
   if (mode == 2) {
@@ -87,7 +108,10 @@ __global__ void kbar(int mode, int iters, int nst, unsigned* ctr, unsigned* fl, 
     else if (mode == 1) flat_relaxed(ctr, target);
     else if (mode == 2) hier(ctr, target, ncl, rank);
     else if (mode == 3) flags(fl, fl + 148 * 32 + 64, it + 1);
-    else split(ctr, ctr + 64, it + 1, mode == 5);
+    else if (mode == 4 || mode == 5) split(ctr, ctr + 64, it + 1, mode == 5);
+    else if (mode == 6) allpoll(fl, it + 1, 1);
+    else if (mode == 7) allpoll(fl, it + 1, 32);
+    else allpoll_relaxed(fl, it + 1, 1);
   }
 }
 int main() {
@@ -95,7 +119,7 @@ int main() {
   cudaMalloc(&ctr, 4096); cudaMalloc(&fl, 148 * 128 + 4096); cudaMalloc(&scr, 148 * 4096 * 8);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int iters = 2000;
-  for (int mode = 0; mode < 6; ++mode)
+  for (int mode = 0; mode < 9; ++mode)
     for (int cl : {1, 2, 4, 8})
       for (int nst : {0, 512}) {
         if ((mode == 2) != (cl > 1)) continue;
