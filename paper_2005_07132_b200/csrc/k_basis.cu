@@ -97,12 +97,24 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
   for (int e = tid; e < kk; e += nt) B0[e] = C[e] / tr;
   __syncthreads();
   double wgt = 0.5;
+  const int kh = (k + 1) >> 1;   // 2 x 2 output blocks: four independent accumulator chains per thread
   for (int it = 0; it < kRidgeSquarings; ++it) {
-    for (int e = tid; e < kk; e += nt) {
-      const int i = e / k, j = e % k;
-      double s = 0.0;
-      for (int q = 0; q < k; ++q) s = fma(B0[i * k + q], B0[q * k + j], s);
-      B1[e] = s;
+    for (int e = tid; e < kh * kh; e += nt) {
+      const int i = 2 * (e / kh), j = 2 * (e % kh);
+      const bool i1 = i + 1 < k, j1 = j + 1 < k;
+      double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+      for (int q = 0; q < k; ++q) {
+        const double a0 = B0[i * k + q], a1 = i1 ? B0[(i + 1) * k + q] : 0.0;
+        const double b0 = B0[q * k + j], b1 = j1 ? B0[q * k + j + 1] : 0.0;
+        s00 = fma(a0, b0, s00);
+        s01 = fma(a0, b1, s01);
+        s10 = fma(a1, b0, s10);
+        s11 = fma(a1, b1, s11);
+      }
+      B1[i * k + j] = s00;
+      if (j1) B1[i * k + j + 1] = s01;
+      if (i1) B1[(i + 1) * k + j] = s10;
+      if (i1 && j1) B1[(i + 1) * k + j + 1] = s11;
     }
     __syncthreads();
     double tl = 0.0;
@@ -135,43 +147,71 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
   double* L = in_smem ? shm : Lw;   // factor in smem when it fits, copied out at the end
   for (int e = tid; e < kk; e += nt) { const int i = e / k, j = e % k; L[e] = (j <= i) ? C[e] + (i == j ? lam : 0.0) : 0.0; }
   __syncthreads();
-  // right-looking Cholesky, lower triangle
+  // right-looking Cholesky, lower triangle, one barrier per column: every thread reads the pivot,
+  // column j of L is written from the (not yet scaled) column, and the trailing update uses the
+  // unscaled column over the pivot (column j is only read in this phase)
   for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      const double d = L[j * k + j];
-      if (!(d > 0.0)) { atomicOr(flags, 4); L[j * k + j] = 1e-300; }
-      else L[j * k + j] = sqrt(d);
-    }
-    __syncthreads();
-    const double djj = L[j * k + j];
-    for (int i = j + 1 + tid; i < k; i += nt) L[i * k + j] /= djj;
-    __syncthreads();
+    const double d = L[j * k + j];
+    const bool ok = d > 0.0;
+    const double ljj = ok ? sqrt(d) : 1e-300, il = ok ? 1.0 / ljj : 0.0, id = ok ? 1.0 / d : 0.0;
+    if (tid == 0 && !ok) atomicOr(flags, 4);
     const int rem = k - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int i = j + 1 + e / rem, c = j + 1 + e % rem;
-      if (c <= i) L[i * k + c] -= L[i * k + j] * L[c * k + j];
+    // trailing update L[i][c] -= L[i][j] L[c][j] / d for j < c <= i (2-D: rows by tid / 32, cols by lane)
+    for (int i = j + 1 + (tid >> 5); i < k; i += nt >> 5) {
+      const double lij = L[i * k + j] * id;
+      for (int c = j + 1 + lane; c <= i; c += 32) L[i * k + c] -= lij * L[c * k + j];
     }
+    (void)rem;
     __syncthreads();
+    for (int i = j + tid; i < k; i += nt) L[i * k + j] = i == j ? ljj : L[i * k + j] * il;
+    // (column j is written after the barrier above and read by no later phase before the next barrier
+    //  except as L[c][j'] with j' > j)
   }
+  __syncthreads();
   if (in_smem)
     for (int e = tid; e < kk; e += nt) Lw[e] = L[e];
 }
 
+// ncol independent right-hand sides, one per thread; L and the thread block's columns in shared
+// memory ([k][blockDim] layout: a warp's accesses are consecutive), reciprocal diagonal precomputed
 __global__ void ridge_solve_kernel(const double* __restrict__ Lw, int k, const double* __restrict__ R, int ncol,
                                    double* __restrict__ Phi) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncol) return;
-  // forward L y = r, backward L^T x = y; y/x stored in Phi column j
+  extern __shared__ __align__(16) double rs[];
+  double* Ls = rs;               // k x k
+  double* rd = Ls + k * k;       // k
+  double* X = rd + k;            // [k][nt]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < k * k; e += nt) Ls[e] = Lw[e];
+  __syncthreads();
+  for (int i = tid; i < k; i += nt) rd[i] = 1.0 / Ls[i * k + i];
+  const int j = blockIdx.x * nt + tid;
+  const bool act = j < ncol;
+  for (int i = 0; i < k; ++i) X[i * nt + tid] = act ? R[(int64_t)i * ncol + j] : 0.0;
+  __syncthreads();
+  // forward L y = r (two partial sums per row: half the dependent chain)
   for (int i = 0; i < k; ++i) {
-    double s = R[(int64_t)i * ncol + j];
-    for (int q = 0; q < i; ++q) s -= Lw[i * k + q] * Phi[(int64_t)q * ncol + j];
-    Phi[(int64_t)i * ncol + j] = s / Lw[i * k + i];
+    double s0 = X[i * nt + tid], s1 = 0.0;
+    int q = 0;
+    for (; q + 1 < i; q += 2) {
+      s0 = fma(-Ls[i * k + q], X[q * nt + tid], s0);
+      s1 = fma(-Ls[i * k + q + 1], X[(q + 1) * nt + tid], s1);
+    }
+    if (q < i) s0 = fma(-Ls[i * k + q], X[q * nt + tid], s0);
+    X[i * nt + tid] = (s0 + s1) * rd[i];
   }
+  // backward L^T x = y
   for (int i = k - 1; i >= 0; --i) {
-    double s = Phi[(int64_t)i * ncol + j];
-    for (int q = i + 1; q < k; ++q) s -= Lw[q * k + i] * Phi[(int64_t)q * ncol + j];
-    Phi[(int64_t)i * ncol + j] = s / Lw[i * k + i];
+    double s0 = X[i * nt + tid], s1 = 0.0;
+    int q = i + 1;
+    for (; q + 1 < k; q += 2) {
+      s0 = fma(-Ls[q * k + i], X[q * nt + tid], s0);
+      s1 = fma(-Ls[(q + 1) * k + i], X[(q + 1) * nt + tid], s1);
+    }
+    if (q < k) s0 = fma(-Ls[q * k + i], X[q * nt + tid], s0);
+    X[i * nt + tid] = (s0 + s1) * rd[i];
   }
+  if (act)
+    for (int i = 0; i < k; ++i) Phi[(int64_t)i * ncol + j] = X[i * nt + tid];
 }
 
 __global__ void assemble_B_kernel(const double* Vt_f, const double* HPhi, const double* Vsec, const double* Hv,
@@ -228,7 +268,10 @@ void launch_ridge(const double* C, int k, const double* R, int ncol, double ridg
   if (sm) cudaFuncSetAttribute(ridge_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   ridge_factor_kernel<<<1, 1024, sm, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags);
   check_launch("ridge_factor");
-  ridge_solve_kernel<<<(ncol + 127) / 128, 128, 0, s>>>(Lw, k, R, ncol, Phi);
+  const int nts = 32;   // 32 columns per CTA: ncol / 32 CTAs spread over the SMs
+  const size_t ssm = ((size_t)k * k + k + (size_t)k * nts) * sizeof(double);
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(ridge_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  ridge_solve_kernel<<<(ncol + nts - 1) / nts, nts, ssm, s>>>(Lw, k, R, ncol, Phi);
   check_launch("ridge_solve");
 }
 
