@@ -73,17 +73,101 @@ __global__ void dgemm_small_kernel(int m, int n, int kk, const double* __restric
 // anything the ridge weight (reading A11) is sensitive to.
 constexpr int kRidgeSquarings = 24;
 
+// lambda_max estimate of the fPEC ridge (squarings, see ridge_factor_kernel) on ONE cluster of CL CTAs:
+// every CTA keeps B in shared memory, computes its block of rows of B^2 and pushes it (and its partial
+// trace) into the other CTAs' shared memory (st.shared::cluster), one cluster barrier per squaring.  The
+// single-CTA version is FP64-throughput bound on one SM (24 x k^3 FMAs).  Same arithmetic, the traces
+// summed in a different order.
+template <int CL>
+__global__ void __launch_bounds__(256) ridge_lmax_kernel(const double* __restrict__ C, int k, double ridge_rel,
+                                                         double* __restrict__ lam_out) {
+  extern __shared__ __align__(16) double lm[];
+  double* B0 = lm;                    // k x k
+  double* B1 = lm + k * k;            // [2][k x k] (parity: a peer's next push never hits a buffer still read)
+  double* trp = B1 + 2 * k * k;       // [2][CL] partial traces
+  __shared__ double red[8];
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int kk = k * k, rb = (k + CL - 1) / CL, r0 = min(k, (int)rank * rb), r1 = min(k, r0 + rb);
+  double t = 0.0;
+  for (int i = lane; i < k; i += 32) t += C[i * k + i];
+  t = warp_sum(t);                    // every warp holds the full trace
+  const double tr = t;
+  double loglam = log(tr > 0 ? tr : 1e-300);
+  for (int e = tid; e < kk; e += nt) B0[e] = C[e] / tr;
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  double wgt = 0.5;
+  for (int it = 0; it < kRidgeSquarings; ++it) {
+    double* B1p = B1 + (it & 1) * kk;
+    double* trq = trp + (it & 1) * CL;
+    double tl = 0.0;
+    for (int e = tid; e < (r1 - r0) * k; e += nt) {
+      const int i = r0 + e / k, j = e - (e / k) * k;
+      double s0 = 0.0, s1 = 0.0;
+      int q = 0;
+      for (; q + 1 < k; q += 2) {
+        s0 = fma(B0[i * k + q], B0[q * k + j], s0);
+        s1 = fma(B0[i * k + q + 1], B0[(q + 1) * k + j], s1);
+      }
+      if (q < k) s0 = fma(B0[i * k + q], B0[q * k + j], s0);
+      const double v = s0 + s1;
+      if (i == j) tl += v;
+      // own copy + every peer's copy of this entry
+#pragma unroll
+      for (int d = 0; d < CL; ++d) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(B1p + i * k + j)), "r"(d));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+      }
+    }
+    tl = warp_sum(tl);
+    if (lane == 0) red[wid] = tl;
+    __syncthreads();
+    if (tid < CL) {
+      double ps = 0.0;
+      for (int w2 = 0; w2 < nt / 32; ++w2) ps += red[w2];
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(trq + rank)), "r"(tid));
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(ps) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    double c = 0.0;
+    for (int d = 0; d < CL; ++d) c += trq[d];
+    c = c > 0 ? c : 1e-300;
+    loglam += wgt * log(c);
+    wgt *= 0.5;
+    for (int e = tid; e < kk; e += nt) B0[e] = B1p[e] / c;
+    __syncthreads();
+  }
+  double fr = 0.0;
+  for (int e = tid; e < kk; e += nt) fr += B0[e] * B0[e];
+  fr = warp_sum(fr);
+  if (lane == 0) red[wid] = fr;
+  __syncthreads();
+  if (tid == 0 && rank == 0) {
+    double sfr = 0;
+    for (int w2 = 0; w2 < nt / 32; ++w2) sfr += red[w2];
+    const double lmax = exp(loglam + 2.0 * wgt * log(sqrt(sfr > 0 ? sfr : 1e-300)));
+    lam_out[0] = ridge_rel * lmax;
+  }
+  // no CTA leaves while a peer may still push into it (the last pushes precede the last barrier)
+}
+
+template <bool SMEM>   // SMEM: the k x k work matrices in shared memory (typed shared pointers: LDS, not generic loads)
 __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __restrict__ C, int k, double ridge_rel,
                                                             double* __restrict__ Lw, double* __restrict__ work,
-                                                            double* __restrict__ lam_out, int* __restrict__ flags) {
+                                                            double* __restrict__ lam_out, int* __restrict__ flags,
+                                                            int have_lam) {
   extern __shared__ __align__(16) double shm[];
   __shared__ double red[32];
   __shared__ double sh_scal[2];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int kk = k * k;
-  const bool in_smem = k <= 80;
-  double* B0 = in_smem ? shm : work;
-  double* B1 = in_smem ? shm + kk : work + kk;
+  constexpr bool in_smem = SMEM;
+  double* B0 = SMEM ? shm : work;
+  double* B1 = SMEM ? shm + kk : work + kk;
+  if (!have_lam) {
   // trace
   double t = 0.0;
   for (int i = tid; i < k; i += nt) t += C[i * k + i];
@@ -143,6 +227,10 @@ __global__ void __launch_bounds__(1024) ridge_factor_kernel(const double* __rest
     lam_out[0] = sh_scal[0];
   }
   __syncthreads();
+  } else {
+    if (tid == 0) sh_scal[0] = lam_out[0];
+    __syncthreads();
+  }
   const double lam = sh_scal[0];
   double* L = in_smem ? shm : Lw;   // factor in smem when it fits, copied out at the end
   for (int e = tid; e < kk; e += nt) { const int i = e / k, j = e % k; L[e] = (j <= i) ? C[e] + (i == j ? lam : 0.0) : 0.0; }
@@ -265,8 +353,32 @@ void launch_ridge(const double* C, int k, const double* R, int ncol, double ridg
                   double* work, int* flags, cudaStream_t s) {
   double* Lw = work;
   const size_t sm = k <= 80 ? (size_t)2 * k * k * sizeof(double) : 0;
-  if (sm) cudaFuncSetAttribute(ridge_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  ridge_factor_kernel<<<1, 1024, sm, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags);
+  int have_lam = 0;
+  constexpr int CL = 8;
+  const size_t lsm = (3 * (size_t)k * k + 2 * CL) * sizeof(double);
+  if (k >= CL && lsm <= 200 * 1024) {
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(ridge_lmax_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = lsm;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, ridge_lmax_kernel<CL>, C, k, ridge_rel, lam_out));
+    have_lam = 1;
+  }
+  if (sm) {
+    cudaFuncSetAttribute(ridge_factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    ridge_factor_kernel<true><<<1, 1024, sm, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags, have_lam);
+  } else {
+    ridge_factor_kernel<false><<<1, 1024, 0, s>>>(C, k, ridge_rel, Lw, work + (int64_t)k * k, lam_out, flags, have_lam);
+  }
   check_launch("ridge_factor");
   const int nts = 32;   // 32 columns per CTA: ncol / 32 CTAs spread over the SMs
   const size_t ssm = ((size_t)k * k + k + (size_t)k * nts) * sizeof(double);
