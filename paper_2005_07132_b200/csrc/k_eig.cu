@@ -271,22 +271,22 @@ __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], do
 // The pass over one owned row r > j (one warp): pending update row -= v_{j-1}[r] w + w[r] v_{j-1} (if
 // pending) and the dot A^(j)[r,:] v_j over c > j.  Lane 0 handles c = j + 1 first, so row[j+1]
 // (= A^(j)[r][j+1]) is its own write.
-__device__ __forceinline__ double row_pass(double* row, int m0, int M, bool pending, double vr, double wr,
+__device__ __forceinline__ double row_pass(double* row, int roff, int m0, int M, bool pending, double vr, double wr,
                                            const double* vp, const double* wp, const double* v, double* pub) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
   if (pending) {
 #pragma unroll 4
     for (int c = m0 + lane; c < M; c += 32) {
-      const double a = row[c] - (vr * wp[c] + wr * vp[c]);
-      row[c] = a;
+      const double a = row[c - roff] - (vr * wp[c] + wr * vp[c]);
+      row[c - roff] = a;
       if (pub) pub[c] = a;
       acc = fma(a, v[c], acc);
     }
   } else {
 #pragma unroll 4
     for (int c = m0 + lane; c < M; c += 32) {
-      const double a = row[c];
+      const double a = row[c - roff];
       if (pub) pub[c] = a;
       acc = fma(a, v[c], acc);
     }
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
       if (r <= j) continue;
       double* row = rows + (size_t)i * M;
       const bool publish = last && (r == j + 1 || r == M - 1);   // rows for the trailing 2 x 2 flush
-      const double acc = row_pass(row, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
+      const double acc = row_pass(row, 0, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
       // p_r and A^(j)[r][j+1] into the column-parity buffers: a fast CTA's next pass never overwrites
       // what a slow CTA still reads
       if (lane == 0) {
@@ -454,41 +454,46 @@ template <int NPL>
 __global__ void __launch_bounds__(kTsThreads, 1) tridiag_tail_kernel(const double* __restrict__ G, double* __restrict__ Wk,
                                                                    int M, int jend, double* __restrict__ d,
                                                                    double* __restrict__ e, double* __restrict__ tau,
-                                                                   const double* __restrict__ Pg) {
+                                                                   const double* __restrict__ Pg, int dbg) {
   extern __shared__ __align__(16) double sm[];
+  long long tsr[6] = {0, 0, 0, 0, 0, 0};   // dbg >= 3: phase clocks of rank 0 at column M - dcol
+  const int dcol = (dbg >> 8) ? (dbg >> 8) : 100;
+  dbg &= 0xff;
   uint32_t rank, CL;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CL));
   const int mt = M - jend;
   const int R = (mt - (int)rank + (int)CL - 1) / (int)CL;   // owned rows r = jend + rank + i CL
-  double* rows = sm - jend;                                 // row i: rows + i mt, valid for c >= jend
-  double* base = sm + (size_t)((mt + CL - 1) / CL) * mt;    // same layout in every CTA of the cluster
-  double* vbuf0 = base - jend;
-  double* vbuf1 = vbuf0 + mt;
-  double* wp = vbuf1 + mt;
-  double* pb = wp + mt;     // pb + parity * mt: p of the column with that parity (absolute index c)
-  double* cb = pb + 2 * mt; // cb + parity * mt: column j+1 of A^(j) (absolute index c)
-  double* red = base + 7 * mt;
+  double* rows = sm;                                        // row i: rows + i mt, local column c - jend
+  // vectors indexed by the absolute column c (size M each, so no pointer leaves the shared window);
+  // same layout in every CTA of the cluster
+  double* base = sm + (size_t)((mt + CL - 1) / CL) * mt;
+  double* vbuf0 = base;
+  double* vbuf1 = vbuf0 + M;
+  double* wp = vbuf1 + M;
+  double* pb = wp + M;      // pb + parity * M: p of the column with that parity
+  double* cb = pb + 2 * M;  // cb + parity * M: column j+1 of A^(j)
+  double* red = base + 7 * (size_t)M;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int pprev0 = (jend - 1) & 1;
   for (int i = 0; i < R; ++i) {
     const int r = jend + (int)rank + i * (int)CL;
     const double* src = jend > 0 ? Wk + (int64_t)r * M : G + (int64_t)r * M;
-    for (int c = jend + tid; c < M; c += nt) rows[(size_t)i * mt + c] = src[c];
+    for (int c = jend + tid; c < M; c += nt) rows[(size_t)i * mt + (c - jend)] = src[c];
   }
   for (int c = jend + tid; c < M; c += nt) {
     vbuf0[c] = 0.0;
     wp[c] = 0.0;
     vbuf1[c] = jend > 0 ? __ldcg(Wk + (int64_t)(jend - 1) * M + c) : 0.0;
-    pb[pprev0 * mt + c] = jend > 0 ? __ldcg(Pg + pprev0 * M + c) : 0.0;
-    cb[pprev0 * mt + c] = jend > 0 ? __ldcg(Pg + (2 + pprev0) * M + c) : G[c];
+    pb[pprev0 * M + c] = jend > 0 ? __ldcg(Pg + pprev0 * M + c) : 0.0;
+    cb[pprev0 * M + c] = jend > 0 ? __ldcg(Pg + (2 + pprev0) * M + c) : G[c];
   }
   double tprev = jend > 0 ? tau[jend - 1] : 0.0;
   // remote addresses of the p / column buffers in every CTA of the cluster (lane q < CL: CTA q)
   uint32_t rpb = 0, rcb = 0;
   if (lane < (int)CL) {
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpb) : "r"(tc::smem_u32(pb + jend)), "r"(lane));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rcb) : "r"(tc::smem_u32(cb + jend)), "r"(lane));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpb) : "r"(tc::smem_u32(pb)), "r"(lane));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rcb) : "r"(tc::smem_u32(cb)), "r"(lane));
   }
   cluster_sync_all();
   double* v = vbuf0;
@@ -497,21 +502,24 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_tail_kernel(const doubl
     const int pp = (j - 1) & 1, pc = j & 1;
     if (tid < kTsChain) {
       double X[NPL], Pv[NPL];
-      const double* pprev = pb + pp * mt;
-      const double* cprev = cb + pp * mt;
+      const double* pprev = pb + pp * M;
+      const double* cprev = cb + pp * M;
 #pragma unroll
       for (int i = 0; i < NPL; ++i) {
         const int c = j + tid + kTsChain * i;
         Pv[i] = c < M ? pprev[c] : 0.0;
         X[i] = c < M ? cprev[c] : 0.0;
       }
+      if (dbg >= 3 && rank == 0 && tid == 0 && j == M - dcol) tsr[0] = clock64();
       column_chain<NPL>(j, M, Pv, X, pprev[j], vp, wp, v, red, tprev, rank == 0, d, e, tau);
+      if (dbg >= 3 && rank == 0 && tid == 0 && j == M - dcol) tsr[1] = clock64();
     } else if (j > 0) {
       double* rj = Wk + (int64_t)(j - 1) * M;
       const int len = (M - j + CL - 1) / CL, c0 = j + rank * len, c1 = min(M, c0 + len);
       for (int c = c0 + tid - kTsChain; c < c1; c += nt - kTsChain) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
     }
     __syncthreads();
+    if (dbg >= 3 && rank == 0 && tid == 0 && j == M - dcol) tsr[2] = clock64();
     const double t = red[8];
     const int m0 = j + 1;
     const bool last = j + 3 == M;
@@ -520,22 +528,26 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_tail_kernel(const doubl
       if (r <= j) continue;
       double* row = rows + (size_t)i * mt;
       const bool publish = last && (r == j + 1 || r == M - 1);
-      const double acc = row_pass(row, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
-      const double cval = __shfl_sync(0xffffffffu, lane == 0 ? row[m0] : 0.0, 0);
-      if (lane < (int)CL) {
-        const uint32_t off = (uint32_t)((pc * mt + (r - jend)) * 8);
+      const double acc = row_pass(row, jend, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
+      const double cval = __shfl_sync(0xffffffffu, lane == 0 ? row[m0 - jend] : 0.0, 0);
+      if (lane < (int)CL && dbg != 4) {   // dbg 4: timing without the pushes (wrong results)
+        const uint32_t off = (uint32_t)((pc * M + r) * 8);
         asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rpb + off), "d"(t * acc) : "memory");
         asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rcb + off), "d"(cval) : "memory");
       }
     }
+    if (dbg >= 3 && rank == 0 && tid == 0 && j == M - dcol) tsr[3] = clock64();
     cluster_sync_all();
+    if (dbg >= 3 && rank == 0 && tid == 0 && j == M - dcol) tsr[4] = clock64();
     tprev = t;
     double* tmp = vp; vp = v; v = tmp;
   }
   if (rank == 0 && M >= 3) {
-    const double* pcur = pb + ((M - 3) & 1) * mt;
+    const double* pcur = pb + ((M - 3) & 1) * M;
     tail_flush(M, [&](int c) { return pcur[c]; }, vp, wp, tprev, red, Wk, d, e);
   }
+  if (dbg >= 3 && rank == 0 && tid == 0)
+    for (int q = 0; q < 5; ++q) d[q] = (double)tsr[q];
 }
 
 size_t tridiag_rows_smem(int M, int P) {
@@ -543,8 +555,8 @@ size_t tridiag_rows_smem(int M, int P) {
   return ((size_t)R * M + 3 * (size_t)M + 32) * sizeof(double);
 }
 
-size_t tridiag_tail_smem(int mt, int CL) {
-  return ((size_t)((mt + CL - 1) / CL) * mt + 7 * (size_t)mt + 32) * sizeof(double);
+size_t tridiag_tail_smem(int mt, int CL, int Mfull) {
+  return ((size_t)((mt + CL - 1) / CL) * mt + 7 * (size_t)Mfull + 32) * sizeof(double);
 }
 
 // 1/q via the MUFU seed + two Newton steps (full fp64 accuracy for normal q; a Sturm count only
@@ -1453,7 +1465,7 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
       int cap = 200;   // per-column cost of the tail grows with m^2 / CL; below ~200 it beats the grid barrier
       if (const char* ev = getenv("FKK_TRIDIAG_MT")) cap = std::max(3, atoi(ev));   // A/B only
       mt = std::min(M, cap);
-      while (mt > 2 && tridiag_tail_smem(mt, CL) > (size_t)maxsm) --mt;
+      while (mt > 2 && tridiag_tail_smem(mt, CL, M) > (size_t)maxsm) --mt;
     }
     int jend = CL > 0 ? M - mt : M - 2;
     if (jend < 2 && CL > 0) jend = 0;   // whole problem in the tail
@@ -1477,7 +1489,7 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
       count_launch();
     }
     if (jend < M - 2) {
-      const size_t smem = tridiag_tail_smem(M - jend, CL);
+      const size_t smem = tridiag_tail_smem(M - jend, CL, M);
       auto kt = tridiag_tail_kernel<8>;
       FKK_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if (CL > 8) FKK_CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1494,7 +1506,12 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
       cfg.attrs = at;
       cfg.numAttrs = 1;
       const double* Pc = pg;
-      FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kt, Gc, A, Mi, jendi, d, e, tau, Pc));
+      int tdbg = 0;
+      if (const char* ev = getenv("FKK_TRIDIAG_DBG")) {   // timing experiments only: 13 / 14 (+ 256 x column offset)
+        const int v = atoi(ev);
+        tdbg = (v & 0xff) >= 13 ? ((v & ~0xff) | ((v & 0xff) - 10)) : 0;
+      }
+      FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kt, Gc, A, Mi, jendi, d, e, tau, Pc, tdbg));
       count_launch();
     }
   } else {
