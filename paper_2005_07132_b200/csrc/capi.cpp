@@ -100,6 +100,7 @@ struct fkk_basis {
 // Plan
 // ------------------------------------------------------------------------------------------------
 struct fkk_plan {
+  bool a0_raw = false;   // A0 not materialised by the last svd_stage (projection reads the cube)
   fkk_plan_desc d{};
   int M = 0, k = 0, kp = 0, L = 0, log2L = 0, sg_half = 0, in_f64 = 0, pad_zero = 0;
   size_t in_elem = 4;
@@ -288,7 +289,8 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->flags = dalloc<int>(4);
   FKK_CUDA_CHECK(cudaMemset(p->flags, 0, 4 * sizeof(int)));
   FKK_CUDA_CHECK(cudaMallocHost(&p->h_flags, 4 * sizeof(int)));
-  p->inv_ref = dalloc<float>(M);
+  p->inv_ref = dalloc<float>((size_t)(M + 31) / 32 * 32);   // zero tail: the raw-cube projection reads 32-channel stages
+  FKK_CUDA_CHECK(cudaMemset(p->inv_ref, 0, (size_t)(M + 31) / 32 * 32 * sizeof(float)));
   p->ref64 = dalloc<double>(M);
   // twiddles exp(-2 pi i j / L), fp64 on the host
   {
@@ -404,9 +406,12 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   const int M = p->M, k = p->k;
   fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
   const bool pre = p->apre != nullptr;
+  // with the pre-split Gram and the TMA projection, A0 is never materialised: the projection forms it
+  // from the cube in its converter warps (saves writing and re-reading N x M fp32)
+  p->a0_raw = pre && !p->in_f64 && p->d.gemm_impl == FKK_GEMM_3XTF32 && fkk::project_raw_ok(M, p->kp) && !getenv("FKK_A0_STORE");
   if (pre)
     fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->apre_blocks, p->inv_ref,
-                             (float)p->d.ratio_floor, p->A, p->apre, p->flags, s);
+                             (float)p->d.ratio_floor, p->a0_raw ? nullptr : p->A, p->apre, p->flags, s);
   else
     fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
   if (p->d.f_mode == FKK_F_EQ9) {
@@ -482,8 +487,11 @@ void transform_rest(fkk_plan* p, const void* cube, int64_t n_rows, int64_t row0,
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
-    (void)cube;
-    if (tcg)
+    if (tcg && p->a0_raw)
+      fkk::launch_project_tc(static_cast<const float*>(cube) + r0 * (int64_t)M, r1 - r0, M, p->wimg, k, kp,
+                             p->US + r0 * (int64_t)kp, p->ext_val, p->ext_idx, row0 + r0, 1, s, p->inv_ref,
+                             (float)p->d.ratio_floor);
+    else if (tcg)
       fkk::launch_project_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->wimg, k, kp, p->US + r0 * (int64_t)kp, p->ext_val,
                              p->ext_idx, row0 + r0, 1, s);
     else
@@ -822,6 +830,7 @@ fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows,
     const int M = p->M, k = p->k;
     fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
     fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->A, p->flags, s);
+    p->a0_raw = false;   // A0 materialised here
     if (p->d.f_mode == FKK_F_EQ9) {
       FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
       fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);

@@ -109,8 +109,11 @@ size_t project_tc_wimg_floats(int M, int kp);
 int project_tc_num_blocks(int64_t n);
 void launch_build_wimg(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* wimg,
                        cudaStream_t s);
+// the TMA projection can read the raw f32 cube and form A0 itself (log-ratio pass writes no A0)
+bool project_raw_ok(int M, int kp);
 void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int k, int kp, float* US, float* ext_val,
-                       int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s);
+                       int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s, const float* inv_ref = nullptr,
+                       float floor = 0.f);
 // Reconstruction K = exp(US B_amp) e^{i US B_ph} (k_reconstruct.cu); Bi: k x M x 2 (amp, ph);
 // US: n x ldus fp32 (ldus >= k, columns >= k zero).
 void launch_reconstruct_simt(const float* US, int64_t n, int k, int ldus, const float* Bi, int M, void* out,

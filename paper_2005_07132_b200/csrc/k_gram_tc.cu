@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restri
         o.y = 0.5f * logf(fmaxf(v.y * ir.y, floor));
         o.z = 0.5f * logf(fmaxf(v.z * ir.z, floor));
         o.w = 0.5f * logf(fmaxf(v.w * ir.w, floor));
-        *reinterpret_cast<float4*>(A + px * (int64_t)M + col) = o;
+        if (A) *reinterpret_cast<float4*>(A + px * (int64_t)M + col) = o;   // A == nullptr: image only
       }
       x[e] = o;
     }

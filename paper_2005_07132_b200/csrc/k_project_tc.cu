@@ -286,11 +286,12 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
 // W (bulk copies from L2), so the kernel is bounded by HBM rather than by shared-memory bandwidth
 // (the smem-A version moved ~136 KB of smem traffic per 16 KB of A0, this one ~72 KB).
 //   warp 0   : A0 TMA producer (raw ring)        warp 2: W stage producer (W ring)
-//   warp 1   : TMEM alloc, MMA issue            warps 4-7: converters (warp % 4 = TMEM lane quadrant)
+//   warp 1   : TMEM alloc, MMA issue            warps 4-7, 12-15: converters (warp % 4 = TMEM lane
+//                                               quadrant; two warps split the 32 channels of a stage)
 //   warps 8-11: epilogue (as above)
 constexpr int QKC = 32;                       // channels per stage (one 128-B swizzle row)
 constexpr int QA_BYTES = PTM * QKC * 4;       // 16 KB raw tile
-constexpr int QTHREADS = 384;
+constexpr int QTHREADS = 512;
 __host__ __device__ inline int q_w_part(int kp) { return kp * QKC * 4; }     // hi or lo: kp rows x 128 B
 __host__ __device__ inline int q_nw(int kp) { return kp <= 64 ? 6 : 3; }    // W ring slots
 __host__ __device__ inline int q_nraw(int kp) { return (208 * 1024 - q_nw(kp) * 2 * q_w_part(kp)) / QA_BYTES; }
@@ -324,7 +325,8 @@ struct Ring {
 __global__ void __launch_bounds__(QTHREADS, 1)
 project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, const float* __restrict__ wimg, int kp,
                    float* __restrict__ US, float* __restrict__ ext_val, int64_t* __restrict__ ext_idx, int k,
-                   int64_t row_offset, int want_ext, int nbuf, int abase, int NA) {
+                   int64_t row_offset, int want_ext, int nbuf, int abase, int NA, const float* __restrict__ inv_ref,
+                   float floor) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int NR = q_nraw(kp), NW = q_nw(kp);
@@ -348,9 +350,9 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
   const int64_t ntiles = (n + PTM - 1) / PTM;
   const int nst = (M + QKC - 1) / QKC;
   if (tid == 0) {
-    for (int s2 = 0; s2 < NR; ++s2) { tc::mbar_init(&a_full[s2], 1); tc::mbar_init(&a_empty[s2], 4); }
+    for (int s2 = 0; s2 < NR; ++s2) { tc::mbar_init(&a_full[s2], 1); tc::mbar_init(&a_empty[s2], 8); }
     for (int s2 = 0; s2 < NW; ++s2) { tc::mbar_init(&w_full[s2], 1); tc::mbar_init(&w_empty[s2], 1); }
-    for (int s2 = 0; s2 < NA; ++s2) { tc::mbar_init(&t_full[s2], 4); tc::mbar_init(&t_empty[s2], 1); }
+    for (int s2 = 0; s2 < NA; ++s2) { tc::mbar_init(&t_full[s2], 8); tc::mbar_init(&t_empty[s2], 1); }
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 128); }
     tc::fence_mbar_init();
     tma::prefetch_map(&amap);
@@ -399,33 +401,52 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
       }
       __syncwarp();
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ------------------------------------------------------------ converters: smem row -> TMEM hi | lo
+    // two warps per TMEM lane quadrant (warps 4-7: channels 0-15 of the stage, 12-15: channels 16-31)
     const int q = warp & 3, r = q * 32 + lane;            // pixel row = TMEM lane
+    const int hc = warp >= 12 ? 16 : 0;                    // first channel of this warp's half
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ring ra, rt;
     for (int64_t pos = 0; pos < npos; ++pos, ra.next(NR), rt.next(NA)) {
       tc::mbar_wait(&a_full[ra.slot], ra.phase);
       const unsigned char* rowp = ring_a + ra.slot * QA_BYTES + r * 128;
-      float x[32];
+      float x[16];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+      for (int c = 0; c < 4; ++c) {
+        const int cc = (hc >> 2) + c;   // logical 16-B chunk
+        const float4 v = *reinterpret_cast<const float4*>(rowp + ((cc ^ (r & 7)) << 4));
         x[4 * c] = v.x;
         x[4 * c + 1] = v.y;
         x[4 * c + 2] = v.z;
         x[4 * c + 3] = v.w;
       }
-      float hi[32], lo[32];
+      if (inv_ref) {
+        // the tile is the raw cube: A0 = 1/2 ln(max(I / I_ref, floor)) here (hardware log, <= 2 ulp;
+        // channels >= M zero like the A0 image), so the log-ratio pass never writes A0 to HBM
+        const int c0 = (int)(pos % nst) * QKC + hc;
+        // inv_ref is zero-padded to a multiple of 32: broadcast float4 loads, no predication
+        float ir[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) tc::split_fast(x[i], hi[i], lo[i]);
+        for (int u = 0; u < 4; ++u) {
+          const float4 v4 = __ldg(reinterpret_cast<const float4*>(inv_ref + c0) + u);
+          ir[4 * u] = v4.x; ir[4 * u + 1] = v4.y; ir[4 * u + 2] = v4.z; ir[4 * u + 3] = v4.w;
+        }
+        const int nvalid = M - c0;   // channels c0 + i, i < nvalid, are real
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float a0 = 0.5f * __logf(fmaxf(x[i] * ir[i], floor));
+          x[i] = i < nvalid ? a0 : 0.0f;
+        }
+      }
+      float hi[16], lo[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tc::split_fast(x[i], hi[i], lo[i]);
       tc::mbar_wait(&t_empty[rt.slot], rt.phase ^ 1);
       tc::tc_fence_after();
-      const uint32_t ta = tmem_a + lane_off + (uint32_t)(rt.slot * 2 * QKC);
+      const uint32_t ta = tmem_a + lane_off + (uint32_t)(rt.slot * 2 * QKC) + (uint32_t)hc;
       tc::tmem_st16(ta, hi);
-      tc::tmem_st16(ta + 16, hi + 16);
       tc::tmem_st16(ta + QKC, lo);
-      tc::tmem_st16(ta + QKC + 16, lo + 16);
       tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
@@ -434,7 +455,7 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
         tc::mbar_arrive(&t_full[rt.slot]);
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------ epilogue (as project_tc_kernel)
     const int ew = warp - 8;
     uint32_t ph[2] = {0, 0};
@@ -620,6 +641,8 @@ size_t pt_smem(int kp) { return (size_t)p_nstages(kp) * p_stage_bytes(kp) + 2 * 
 
 }  // namespace
 
+bool project_raw_ok(int M, int kp) { return project_use_tma(M, kp); }
+
 size_t project_tc_wimg_floats(int M, int kp) { return (size_t)((M + PKC - 1) / PKC) * pb_stage(kp) / 4; }
 
 int project_tc_num_blocks(int64_t n) { return (int)((n + PTM - 1) / PTM); }
@@ -634,7 +657,9 @@ void launch_build_wimg(const double* V, const double* fscale, const double* csca
 }
 
 void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int k, int kp, float* US, float* ext_val,
-                       int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s) {
+                       int64_t* ext_idx, int64_t row_offset, int want_ext, cudaStream_t s, const float* inv_ref,
+                       float floor) {
+  if (inv_ref && !project_use_tma(M, kp)) throw Status(10, "project_tc: raw-cube input needs the TMA variant");
   if (n <= 0) return;
   if (project_use_tma(M, kp)) {
     if (kp > 128 || kp % 16 || p_set_cols(M, kp) > 512)
@@ -655,7 +680,7 @@ void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int 
       if (atoi(ev) > 0) na = std::min(na, atoi(ev));
     }
     project_tma_kernel<<<grid, QTHREADS, smem, s>>>(amap, n, M, wimg, kp, US, ext_val, ext_idx, k, row_offset, want_ext,
-                                                    nbuf, abase, na);
+                                                    nbuf, abase, na, inv_ref, floor);
     check_launch("project_tma");
     return;
   }
