@@ -181,10 +181,11 @@ def run_ours(args) -> dict:
     # per-kernel-class rooflines of the other hot kernels (same event timing)
     hbm = peaks["hbm_gbs"]
     other = {}
-    # logratio_pre reads the cube and writes A0 (for the projection) plus the tf32 hi/lo MMA image of A0
-    # for the Gram (128-channel blocks x 32-pixel stages of 2 x 16,640 B)
+    # logratio_pre reads the cube and writes the tf32 hi/lo MMA image of A0 for the Gram (128-channel
+    # blocks x 32-pixel stages of 2 x 16,640 B); A0 itself is not stored: the projection reads the cube
+    # again and forms A0 in its converter warps
     image_bytes = 2.0 * ((M + 127) // 128) * ((n_loc + 31) // 32) * 16640
-    for name, nbytes in (("logratio", 8.0 * n_loc * M + image_bytes), ("project", 4.0 * n_loc * M + 4.0 * n_loc * k),
+    for name, nbytes in (("logratio", 4.0 * n_loc * M + image_bytes), ("project", 4.0 * n_loc * M + 4.0 * n_loc * k),
                          ("reconstruct", 8.0 * n_loc * M + 4.0 * n_loc * k)):
         ms = stage_ms.get(name)
         if ms:
