@@ -32,7 +32,7 @@ namespace {
 constexpr int RTM = 128;          // pixels per tile (UMMA M)
 constexpr int RT_PARTS = 4;       // epilogue: 4 warps per TMEM lane group, each a quarter of the chunk
 constexpr int RT_EPI = 128 * RT_PARTS;
-constexpr int RT_THREADS = 128 + RT_EPI + 32;
+constexpr int RT_THREADS = 128 + RT_EPI + 64;   // + MMA warp + B loader warp
 constexpr int A_LBO = 128;        // unpadded (the A tile is stored once per tile; conflicts there are cheap)
 constexpr int B_LBO = 128;
 static_assert(A_LBO == B_LBO, "the MMA loop advances both descriptors by the same K offset");
@@ -223,22 +223,12 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     const uint32_t idesc = tc::make_idesc_tf32(RTM, g.N, false, false);
     const uint32_t sb = tc::smem_u32(bst);
     const uint64_t db00 = tc::make_sdesc(sb, B_LBO, g.b_sbo);
-    uint32_t a_ph[2] = {0, 0}, bf_ph = 0, be_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
+    uint32_t a_ph[2] = {0, 0}, bf_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
     int64_t it = 0;
     int64_t gq = 0;
-    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t total = my_tiles * g.nchunks;
     const int nks = g.kr / 8;
-    auto load_b = [&](int64_t q) {   // chunk sequence position q -> stage q % RT_BST
-      const int s1 = (int)(q % RT_BST);
-      if (q >= RT_BST) { tc::mbar_wait(&b_empty[s1], (be_ph >> s1) & 1); be_ph ^= 1u << s1; }
-      const int ch1 = (int)(q % g.nchunks);
-      if (tc::elect_one())
-        bulk_g2s(sb + s1 * g.b_stage, reinterpret_cast<const unsigned char*>(bimg) + (size_t)ch1 * g.b_stage, g.b_stage,
-                 &b_full[s1]);
-      __syncwarp();
-    };
-    for (int64_t q = 0; q < RT_BST - 1 && q < total; ++q) load_b(q);
+    // (the B chunks come from the loader warp: the MMA warp never waits on its own commits, so the
+    //  tensor pipe gets chunk gq's MMAs while chunk gq-1's are still executing)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int a = (int)(it % nas);
       tc::mbar_wait(&a_full[a], a_ph[a]);
@@ -246,7 +236,6 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
       tc::tc_fence_after();
       const uint32_t tah = tmem_a + (uint32_t)(a * 2 * g.kr), tal = tah + (uint32_t)g.kr;
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
-        if (gq + RT_BST - 1 < total) load_b(gq + RT_BST - 1);   // its stage was used by chunk gq - 1
         const int s = (int)(gq % RT_BST);
         tc::mbar_wait(&b_full[s], (bf_ph >> s) & 1);
         bf_ph ^= 1u << s;
@@ -269,6 +258,21 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
         }
         __syncwarp();
       }
+    }
+  } else if (warp == 5 + RT_EPI / 32) {
+    // ------------------------------------------------------------ B-chunk loader (bulk copies, ring of RT_BST)
+    const uint32_t sb = tc::smem_u32(bst);
+    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total = my_tiles * g.nchunks;
+    uint32_t be_ph = 0;
+    for (int64_t q = 0; q < total; ++q) {
+      const int s1 = (int)(q % RT_BST);
+      if (q >= RT_BST) { tc::mbar_wait(&b_empty[s1], (be_ph >> s1) & 1); be_ph ^= 1u << s1; }
+      const int ch1 = (int)(q % g.nchunks);
+      if (tc::elect_one())
+        bulk_g2s(sb + s1 * g.b_stage, reinterpret_cast<const unsigned char*>(bimg) + (size_t)ch1 * g.b_stage, g.b_stage,
+                 &b_full[s1]);
+      __syncwarp();
     }
   }
   tc::tc_fence_before();
