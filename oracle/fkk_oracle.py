@@ -373,6 +373,21 @@ def ml_train(I, I_ref, k, p: Params = Params()) -> tuple[dict, np.ndarray]:
 # ----------------------------------------------------------------------------------------------
 
 
+def svd_denoise(I: np.ndarray, k: int) -> np.ndarray:
+    """Rank-k SVD denoise of the RAW cube (the conventional workflow's first step, Fig. 1(a),
+    PAPER.md:58, :64 "creating new U, S and V matrices that exclude the non-desired singular values";
+    the conventional SVD acts on raw BCARS spectra, not on the log-ratio):
+    I_k = U_k S_k V_k^T = (I V_k) V_k^T with V_k the top-k eigenvectors of I^T I (reading A26)."""
+    V, _, _ = eig_topk(gram(I), k)
+    return (I @ V) @ V.T
+
+
+def conventional_workflow(I: np.ndarray, I_ref: np.ndarray, k: int, p: Params = Params()) -> np.ndarray:
+    """The paper's comparison baseline (Fig. 1(a)): SVD denoise of the raw
+    cube to rank k, then the per-spectrum KK + PEC + SEC (kk_direct) of every denoised spectrum."""
+    return kk_direct(svd_denoise(I, k), I_ref, p)
+
+
 def rss(K: np.ndarray, truth_im: np.ndarray) -> np.ndarray:
     """Per-pixel sum over omega of (Im K - truth)^2.  Null RSS = rss(0, truth)."""
     return np.sum((np.imag(K) - truth_im) ** 2, axis=1)

@@ -309,3 +309,30 @@ def test_P20_quality_cfg1():
     r = O.rss(out["K"], truth).mean()
     null = O.rss(np.zeros_like(out["K"]), truth).mean()
     assert r < 0.1 * null
+
+
+# ------------------------------------------------------------------ conventional workflow (NEXT row 2)
+def test_P21_svd_denoise_eckart_young_and_full_rank():
+    """svd_denoise against the SVD definition: the truncation error is the tail of the singular values
+    (Eckart-Young, ||I - I_k||_F^2 = sum_{i>k} sigma_i^2 from numpy.linalg.svd), I_k has rank k, full
+    rank reproduces I, and a rank-1 cube is reproduced at k = 1."""
+    rng = np.random.default_rng(5)
+    I = rng.random((40, 24)) + 0.5
+    sig = np.linalg.svd(I, compute_uv=False)
+    for k in (1, 3, 7):
+        Ik = O.svd_denoise(I, k)
+        assert abs(np.sum((I - Ik) ** 2) - np.sum(sig[k:] ** 2)) <= 1e-9 * np.sum(sig ** 2)
+        assert np.linalg.matrix_rank(Ik, tol=1e-9 * sig[0]) == k
+    assert np.max(np.abs(O.svd_denoise(I, 24) - I)) <= 1e-12 * np.max(np.abs(I))
+    r1 = np.outer(rng.random(30) + 0.5, rng.random(24) + 0.5)
+    assert np.max(np.abs(O.svd_denoise(r1, 1) - r1)) <= 1e-12 * np.max(r1)
+
+
+def test_P22_conventional_full_rank_equals_direct():
+    """At full rank the SVD denoise is the identity, so the conventional workflow equals kk_direct."""
+    from synth import CONFIGS, generate
+    cfg = CONFIGS["cfg1"].with_(height=3, width=4, n_freq=64)
+    I, Iref, _ = generate(cfg)
+    K_conv = O.conventional_workflow(I, Iref, 64)
+    K_dir = O.kk_direct(I, Iref)
+    assert np.max(np.abs(K_conv - K_dir)) <= 1e-9 * np.max(np.abs(K_dir))
