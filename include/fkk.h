@@ -12,7 +12,8 @@
  *             fkk_apply_trained_basis -- ML:fKK-EC (Eqs. 24-25), local;
  *             kk_direct_batch    -- conventional per-spectrum KK + PEC + SEC (Eqs. 3-5,
  *                                   PAPER.md:36-55), local;
- *             fkk_svd            -- the truncated SVD alone.
+ *             fkk_svd            -- the truncated SVD alone;
+ *             fkk_conventional   -- SVD-denoise of the raw cube + kk_direct (Fig. 1(a), NEXT 2).
  *
  * Conventions:
  *   - cube layout: row-major N x M, each spectrum contiguous; the frequency axis is uniform and
@@ -131,6 +132,17 @@ fkk_status fkk_apply_trained_basis(fkk_plan_t p, fkk_basis_t b, const void* d_ic
  * phi' = phi - phi_err; K' = e^{a'} e^{i phi'}; K_CARS = K' / SGtrend(Re K').  Local. */
 fkk_status kk_direct_batch(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref,
                            void* d_out);
+
+/* fkk_conventional -- the paper's comparison baseline, Fig. 1(a) (
+ * SURVEY 8(f) NEXT 2; reading A26): rank-k_keep SVD denoise of the RAW cube,
+ * I_k = (I V_k) V_k^T with V_k the top eigenvectors of I^T I (same tensor-core Gram, GPU eigensolver
+ * and projection as fkk_svd), then kk_direct_batch of every denoised spectrum.
+ * k_keep in [1, rank_k].  d_icars: n_rows x M f32 (device), d_out: as kk_direct_batch.  The plan's
+ * N x M workspace holds I_k.  Requires an f32 plan on the 3xTF32 path with world_size 1
+ * (FKK_ERR_NOT_IMPLEMENTED otherwise).  Local, enqueued on the plan stream (one host sync after the
+ * eigensolver). */
+fkk_status fkk_conventional(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, int32_t k_keep,
+                            void* d_out);
 
 /* Host-buffer variants (end-to-end: host->device copies, compute, device->host copies, all on the
  * plan's stream; they synchronise before returning).  h_* may be pageable or pinned. */

@@ -872,6 +872,49 @@ fkk_status kk_direct_batch(fkk_plan_t p, const void* d_icars, int64_t n_rows, co
   });
 }
 
+// Conventional workflow with SVD denoise (Fig. 1(a); reading A26):
+// rank-k_keep SVD of the RAW cube through the same pre-split Gram + GPU eigensolver + TMA projection, the
+// denoised cube I_k = US . V^T by the reconstruction GEMM in linear mode (into the plan's N x M
+// workspace), then the direct KK + PEC + SEC of every denoised spectrum.  Local (single rank).
+fkk_status fkk_conventional(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, int32_t k_keep,
+                            void* d_out) {
+  return guarded(p, [&] {
+    check_cube_args(p, d_icars, n_rows, d_iref, d_out);
+    if (k_keep < 1 || k_keep > p->k) throw Status(FKK_ERR_INVALID_ARG, "k_keep must be in [1, rank_k]");
+    if (p->in_f64 || !p->apre || p->d.gemm_impl != FKK_GEMM_3XTF32 || p->d.world_size != 1 ||
+        !fkk::project_raw_ok(p->M, p->kp))
+      throw Status(FKK_ERR_NOT_IMPLEMENTED,
+                   "conventional workflow: f32 input, tensor-core path (pre-split Gram, TMA projection), one rank");
+    if (n_rows < 1) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be >= 1");
+    p->begin_call();
+    cudaStream_t s = p->stream;
+    const int M = p->M, k = p->k, kp = p->kp;
+    fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
+    // Gram of the raw cube (image with raw = 1) and the eigensolver
+    fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->apre_blocks, p->inv_ref,
+                             (float)p->d.ratio_floor, nullptr, p->apre, p->flags, s, 1);
+    const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, n_rows));
+    fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+    fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, false, s);
+    p->mark("gram");
+    fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, p->flags, s);
+    p->check_flags_sync();
+    p->mark("eig");
+    // US = I V_k (the projection on the raw cube, no log), I_k = US V_k^T (linear reconstruction)
+    fkk::launch_fill(p->f64, 1.0, M, s);
+    fkk::launch_build_wimg(p->V64, p->f64, nullptr, M, k_keep, kp, p->wimg, s);
+    fkk::launch_project_tc(static_cast<const float*>(d_icars), n_rows, M, p->wimg, k_keep, kp, p->US, p->ext_val,
+                           p->ext_idx, 0, 0, s);
+    fkk::launch_bi_linear(p->V64, k_keep, M, p->Bi, s);
+    fkk::launch_build_bimg(p->Bi, k_keep, M, p->bimg, s);
+    fkk::launch_reconstruct_tc(p->US, n_rows, k_keep, kp, p->bimg, M, p->A, 2, s);
+    p->mark("denoise");
+    // conventional KK + PEC + SEC on the denoised cube
+    direct_run(p, p->A, n_rows, d_iref, d_out);
+    p->end_call();
+  });
+}
+
 fkk_status fkk_transform_host(fkk_plan_t p, const void* h_icars, int64_t n_rows, const void* h_iref, void* h_out,
                               fkk_basis_t* basis_out) {
   return guarded(p, [&] {

@@ -42,6 +42,7 @@ void launch_colsum(const void* I, int in_f64, int64_t n, int M, double* colsum, 
 void launch_noise_scale_from_sums(const double* colsum, int M, double inv_n, double alpha, double sg, double* f64,
                                   float* f32, cudaStream_t s);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
+void launch_bi_linear(const double* V, int k, int M, float* Bi, cudaStream_t s);
 void launch_fill_f(float* p, float v, int64_t n, cudaStream_t s);
 void launch_scale_gram(double* G, const double* f, int M, cudaStream_t s);
 void launch_cast_w(const double* V, const double* fscale, const double* cscale, int M, int k, int kp, float* W,
@@ -85,7 +86,7 @@ void launch_gram_tc_reduce(const double* partials, int ntiles, int nsplit, int M
 // nT = number of 128-channel image blocks (>= ceil(M / 128); blocks past M are zero)
 size_t gram_pre_bytes(int64_t n, int nT);
 void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* inv_ref, float floor, float* A,
-                         unsigned char* Apre, int* flags, cudaStream_t s);
+                         unsigned char* Apre, int* flags, cudaStream_t s, int raw = 0);
 // CTA-pair Gram fed by the image (k_gram_pre2.cu): 256 x 256 tiles (gram_tc2_tiles / _splits / _reduce)
 int gram_pre2_image_blocks(int M);
 void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,

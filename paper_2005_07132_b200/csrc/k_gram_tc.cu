@@ -233,7 +233,7 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
 __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restrict__ I, int64_t n, int M,
                                                            const float* __restrict__ inv_ref, float floor,
                                                            float* __restrict__ A, unsigned char* __restrict__ Apre,
-                                                           int64_t nq, int nT, int* __restrict__ flags) {
+                                                           int64_t nq, int nT, int* __restrict__ flags, int raw) {
   // the image block (hi + lo, 2 GOP_BYTES) is assembled in shared memory and leaves with ONE bulk
   // copy (full-line writes); double-buffered; the next item's I loads are issued before this item's
   // arithmetic (register prefetch)
@@ -271,10 +271,14 @@ __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restri
       if (px < n && col < M) {
         const float4 v = x[e];
         bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
-        o.x = 0.5f * logf(fmaxf(v.x * ir.x, floor));     // same arithmetic as logratio_kernel
-        o.y = 0.5f * logf(fmaxf(v.y * ir.y, floor));
-        o.z = 0.5f * logf(fmaxf(v.z * ir.z, floor));
-        o.w = 0.5f * logf(fmaxf(v.w * ir.w, floor));
+        if (raw) {   // image of the raw cube (the conventional workflow's SVD, reading A26)
+          o = v;
+        } else {
+          o.x = 0.5f * logf(fmaxf(v.x * ir.x, floor));     // same arithmetic as logratio_kernel
+          o.y = 0.5f * logf(fmaxf(v.y * ir.y, floor));
+          o.z = 0.5f * logf(fmaxf(v.z * ir.z, floor));
+          o.w = 0.5f * logf(fmaxf(v.w * ir.w, floor));
+        }
         if (A) *reinterpret_cast<float4*>(A + px * (int64_t)M + col) = o;   // A == nullptr: image only
       }
       x[e] = o;
@@ -524,7 +528,7 @@ size_t gram_pre_bytes(int64_t n, int nT) {
 }
 
 void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* inv_ref, float floor, float* A,
-                         unsigned char* Apre, int* flags, cudaStream_t s) {
+                         unsigned char* Apre, int* flags, cudaStream_t s, int raw) {
   if (n <= 0) return;
   const int64_t nq = (n + GKC - 1) / GKC;
   int dev = 0, sms = 148;
@@ -534,7 +538,7 @@ void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* 
   const int grid = (int)std::min<int64_t>(items, (int64_t)sms * 3);
   const int smem = 4 * GOP_BYTES;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(logratio_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  logratio_pre_kernel<<<grid, 256, smem, s>>>(I, n, M, inv_ref, floor, A, Apre, nq, nT, flags);
+  logratio_pre_kernel<<<grid, 256, smem, s>>>(I, n, M, inv_ref, floor, A, Apre, nq, nT, flags, raw);
   check_launch("logratio_pre");
 }
 

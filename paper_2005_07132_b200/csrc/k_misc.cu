@@ -199,6 +199,20 @@ void launch_noise_scale_from_sums(const double* colsum, int M, double inv_n, dou
   check_launch("noise_scale");
 }
 
+// B for the linear reconstruction I_k = US . V^T (conventional SVD denoise, reading A26): amp row i =
+// column i of V (M x k column-major), phase rows zero
+__global__ void bi_linear_kernel(const double* __restrict__ V, int k, int M, float* __restrict__ Bi) {
+  const int64_t total = (int64_t)k * M;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    Bi[2 * e] = (float)V[e];
+    Bi[2 * e + 1] = 0.f;
+  }
+}
+void launch_bi_linear(const double* V, int k, int M, float* Bi, cudaStream_t s) {
+  bi_linear_kernel<<<256, 256, 0, s>>>(V, k, M, Bi);
+  check_launch("bi_linear");
+}
+
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   fill_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(p, v, n);

@@ -91,7 +91,7 @@ __host__ __device__ inline int rt_box_region(const RtGeom& g) { return (RTM * (g
 template <int RT_BST>
 __global__ void __launch_bounds__(RT_THREADS, 1)
 reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, const float* __restrict__ bimg, int M,
-                      const __grid_constant__ CUtensorMap tmap_out, int imag_only) {
+                      const __grid_constant__ CUtensorMap tmap_out, int imag_only) {   // 0 complex, 1 Im, 2 linear real
   extern __shared__ __align__(1024) unsigned char smem[];
   const RtGeom g = rt_geom(k, M);
   // [RT_NBUF][2 halves][box]; the TMA swizzle pattern is a function of the smem address -> 1024-align
@@ -181,6 +181,12 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
 #pragma unroll
           for (int q = 0; q < 8; q += 2) {
             if (q >= cnt) break;
+            if (imag_only == 2) {   // linear real: the amp column itself, US . V^T (reading A26)
+              const int byte = (j0 + q) * 4;
+              const int gsn = (byte >> 4) ^ swz;
+              *reinterpret_cast<float2*>(row + gsn * 16 + (byte & 15)) = make_float2(v[2 * q], v[2 * q + 2]);
+              continue;
+            }
             const float2 z0 = cis_exp(v[2 * q], v[2 * q + 1]);
             const float2 z1 = cis_exp(v[2 * q + 2], v[2 * q + 3]);
             if (imag_only) {

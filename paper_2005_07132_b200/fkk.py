@@ -65,6 +65,7 @@ _SIGS = {
     "fkk_transform": (_i32, [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
     "fkk_apply_trained_basis": (_i32, [_vp, _vp, _vp, _i64, _vp]),
     "kk_direct_batch": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "fkk_conventional": (_i32, [_vp, _vp, _i64, _vp, _i32, _vp]),
     "fkk_transform_host": (_i32, [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
     "fkk_apply_trained_basis_host": (_i32, [_vp, _vp, _vp, _i64, _vp]),
     "kk_direct_batch_host": (_i32, [_vp, _vp, _i64, _vp, _vp]),
@@ -252,6 +253,15 @@ class Plan:
         self._use_current_stream()
         out = self._out(I.shape[0], out)
         _check(self._h, kk_direct_batch_raw(self._h, I, Iref, out))
+        return out
+
+    def conventional(self, I, Iref, k_keep, out=None):
+        """fkk_conventional: rank-k_keep SVD denoise of the raw cube, then the direct KK (Fig. 1(a))."""
+        self._check_cube(I, Iref)
+        self._use_current_stream()
+        out = self._out(I.shape[0], out)
+        _check(self._h, _lib.fkk_conventional(self._h, _dev_ptr(I, "I"), I.shape[0], _dev_ptr(Iref, "I_ref"),
+                                              int(k_keep), _dev_ptr(out, "out")))
         return out
 
     # host-buffer variants (numpy arrays or pinned CPU torch tensors)

@@ -223,6 +223,33 @@ def test_gram_tc_equals_simt_in_fp32_accuracy(torch_cuda, fkk, cfg2):
         assert np.max(np.abs(G[g] - G_or)) / np.max(np.abs(G_or)) <= 2e-6, g
 
 
+# ------------------------------------------------------- conventional workflow (NEXT 2) ----------
+@pytest.mark.parametrize("k_keep", [6, 12])
+def test_conventional_svd_denoise_cfg1(torch_cuda, fkk, cfg1, k_keep):
+    """fkk_conventional (rank-k SVD denoise of the raw cube, then direct KK) against the oracle's
+    conventional_workflow on the same cube: the denoised cube goes through the fp32 tensor-core SVD, so
+    the bar is the factorized path's (1e-3 max-norm relative, Im and Re)."""
+    I, Iref = cfg1
+    I32 = I[:1024].astype(np.float32)   # (the oracle's per-spectrum ALS bounds the size)
+    plan = fkk.Plan(I.shape[1], 12, I32.shape[0], in_dtype="f32")
+    K = plan.conventional(_dev(torch_cuda, I32), _dev(torch_cuda, Iref.astype(np.float32)), k_keep).cpu().numpy()
+    K_or = O.conventional_workflow(I32.astype(np.float64), Iref.astype(np.float32).astype(np.float64), k_keep)
+    err = np.max(np.abs(K - K_or)) / np.max(np.abs(K_or))
+    print(f"conventional cfg1 k={k_keep}: {err:.3e}")
+    assert err <= 1e-3, err
+
+
+def test_conventional_cfg2_sample(torch_cuda, fkk, cfg2):
+    I, Iref = cfg2
+    I = I[:512]
+    plan = fkk.Plan(1000, 40, I.shape[0])
+    K = plan.conventional(_dev(torch_cuda, I), _dev(torch_cuda, Iref), 20).cpu().numpy()
+    K_or = O.conventional_workflow(I.astype(np.float64), Iref.astype(np.float64), 20)
+    err = np.max(np.abs(K - K_or)) / np.max(np.abs(K_or))
+    print(f"conventional cfg2 k=20: {err:.3e}")
+    assert err <= 1e-3, err
+
+
 # ------------------------------------------------------------------------- ML reuse --------------
 def test_ml_apply_matches_oracle_and_self_consistent(torch_cuda, fkk):
     cfg = CONFIGS["cfg5_train"].with_(height=64, width=64)
