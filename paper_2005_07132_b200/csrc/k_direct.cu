@@ -55,21 +55,69 @@ direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __
   const int pl = (L - M) >> 1;
   const float invL = 1.0f / (float)L;
   int bad = 0;
+  // f32 rows with M % 4 == 0 (M <= 4 x 4 x blockDim): the next pair's rows are loaded as float4 into
+  // registers while this pair's FFTs run (the row loads' latency was the kernel's largest stall)
+  constexpr int kPF = 2;   // float4 per thread and row (M <= 2048; larger M takes the scalar loop)
+  const bool vec = sizeof(TIn) == 4 && (M & 3) == 0 && M <= 4 * kPF * (int)blockDim.x;
+  float4 nx0[kPF], nx1[kPF];
+  auto prefetch = [&](int64_t pr) {
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) { nx0[u] = make_float4(0.f, 0.f, 0.f, 0.f); nx1[u] = nx0[u]; }
+    if (pr >= npairs) return;
+    const int64_t r0 = 2 * pr, r1 = r0 + 1;
+    const float4* p0 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(I) + r0 * (int64_t)M);
+    const float4* p1 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(I) + r1 * (int64_t)M);
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
+      const int q = threadIdx.x + u * blockDim.x;
+      if (4 * q < M) {
+        nx0[u] = __ldcs(p0 + q);
+        if (r1 < n) nx1[u] = __ldcs(p1 + q);
+      }
+    }
+  };
+  if (vec) prefetch(blockIdx.x);
   for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
     const int64_t r0 = 2 * pr, r1 = r0 + 1;
     const TIn* i0 = I + r0 * (int64_t)M;
     const TIn* i1 = I + r1 * (int64_t)M;
     const bool has1 = r1 < n;
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-      TIn v0 = i0[j];
-      bad |= !finite_elem(v0);
-      a0[j] = log_ratio_elem<TIn>(v0, inv_ref[j], ref64[j], floor);
-      if (has1) {
-        TIn v1 = i1[j];
-        bad |= !finite_elem(v1);
-        a1[j] = log_ratio_elem<TIn>(v1, inv_ref[j], ref64[j], floor);
-      } else {
-        a1[j] = 0.f;
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < kPF; ++u) {
+        const int q = threadIdx.x + u * blockDim.x;
+        if (4 * q < M) {
+          const float4 ir = *reinterpret_cast<const float4*>(inv_ref + 4 * q);
+          const float4 v0 = nx0[u], v1 = nx1[u];
+          bad |= !isfinite(v0.x) | !isfinite(v0.y) | !isfinite(v0.z) | !isfinite(v0.w);
+          a0[4 * q] = 0.5f * logf(fmaxf(v0.x * ir.x, floor));
+          a0[4 * q + 1] = 0.5f * logf(fmaxf(v0.y * ir.y, floor));
+          a0[4 * q + 2] = 0.5f * logf(fmaxf(v0.z * ir.z, floor));
+          a0[4 * q + 3] = 0.5f * logf(fmaxf(v0.w * ir.w, floor));
+          if (has1) {
+            bad |= !isfinite(v1.x) | !isfinite(v1.y) | !isfinite(v1.z) | !isfinite(v1.w);
+            a1[4 * q] = 0.5f * logf(fmaxf(v1.x * ir.x, floor));
+            a1[4 * q + 1] = 0.5f * logf(fmaxf(v1.y * ir.y, floor));
+            a1[4 * q + 2] = 0.5f * logf(fmaxf(v1.z * ir.z, floor));
+            a1[4 * q + 3] = 0.5f * logf(fmaxf(v1.w * ir.w, floor));
+          } else {
+            a1[4 * q] = a1[4 * q + 1] = a1[4 * q + 2] = a1[4 * q + 3] = 0.f;
+          }
+        }
+      }
+      prefetch(pr + gridDim.x);
+    } else {
+      for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        TIn v0 = i0[j];
+        bad |= !finite_elem(v0);
+        a0[j] = log_ratio_elem<TIn>(v0, inv_ref[j], ref64[j], floor);
+        if (has1) {
+          TIn v1 = i1[j];
+          bad |= !finite_elem(v1);
+          a1[j] = log_ratio_elem<TIn>(v1, inv_ref[j], ref64[j], floor);
+        } else {
+          a1[j] = 0.f;
+        }
       }
     }
     __syncthreads();
