@@ -318,6 +318,9 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   float* a0 = reinterpret_cast<float*>(x + L);
   float* a1 = a0 + M;
   float2* kb = reinterpret_cast<float2*>(a1 + M);
+  float* pd0 = reinterpret_cast<float*>(kb + M);   // phi - phi_err of row r0 / r1 (read with the other rows)
+  float* pd1 = pd0 + M;
+  float* pe_s = reinterpret_cast<float*>(kb);
   for (int j = threadIdx.x; j < (L >> 1); j += blockDim.x) { float2 t = tw_g[j]; tw[j].x = t.x; tw[j].y = t.y; }
   const int64_t npairs = (n + 1) >> 1;
   const int pl = (L - M) >> 1;
@@ -328,22 +331,32 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
     const bool has1 = r1 < n;
     const float* e0 = phierr + r0 * (int64_t)M;
     const float* e1 = has1 ? phierr + r1 * (int64_t)M : e0;
+    // every row this pair needs (I, phi, phi_err of both spectra) loaded in one batch per element
+#pragma unroll 4
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
-      a0[j] = log_ratio_elem<TIn>(I[r0 * (int64_t)M + j], inv_ref[j], ref64[j], floor);
-      a1[j] = has1 ? log_ratio_elem<TIn>(I[r1 * (int64_t)M + j], inv_ref[j], ref64[j], floor) : 0.f;
+      const TIn v0 = I[r0 * (int64_t)M + j];
+      const TIn v1 = has1 ? I[r1 * (int64_t)M + j] : (TIn)0;
+      const float f0 = phi[r0 * (int64_t)M + j], g0 = e0[j];
+      const float f1 = has1 ? phi[r1 * (int64_t)M + j] : 0.f, g1 = has1 ? e1[j] : 0.f;
+      a0[j] = log_ratio_elem<TIn>(v0, inv_ref[j], ref64[j], floor);
+      a1[j] = has1 ? log_ratio_elem<TIn>(v1, inv_ref[j], ref64[j], floor) : 0.f;
+      pd0[j] = f0 - g0;
+      pd1[j] = f1 - g1;
+      pe_s[j] = g0;          // phi_err rows for the padded transform (kb's space, dead until the r loop)
+      pe_s[M + j] = g1;
     }
-    pad_pair<float, float>(x, e0, e1, M, L, pad_zero);   // (syncs)
+    __syncthreads();
+    pad_pair<float, float>(x, pe_s, pe_s + M, M, L, pad_zero);   // (syncs)
     hilbert_pair_stockham<float, MAXB>(x, tw, L, log2L);
     for (int r = 0; r < 2; ++r) {
       if (r == 1 && !has1) break;
       const int64_t row = r0 + r;
-      const float* ph = phi + row * (int64_t)M;
-      const float* pe = phierr + row * (int64_t)M;
+      const float* pdr = r == 0 ? pd0 : pd1;
       const float* aa = r == 0 ? a0 : a1;
       for (int j = threadIdx.x; j < M; j += blockDim.x) {
         const float hpe = (r == 0 ? x[pl + j].x : x[pl + j].y) * invL;
         const float ap = aa[j] + hpe;              // a' = a + H{phi_err}
-        const float pp = ph[j] - pe[j];            // phi' = phi - phi_err
+        const float pp = pdr[j];                   // phi' = phi - phi_err
         float sn, cs;
         sincosf(pp, &sn, &cs);
         const float mag = expf(ap);
@@ -452,7 +465,7 @@ void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, dou
 
 size_t direct_finish_smem(int M, int L) {
   return (size_t)(4 * (M + 1) + 96 + 64) * sizeof(double) + (size_t)(L / 2 + L) * sizeof(float2) +
-         2 * (size_t)M * sizeof(float) + (size_t)M * sizeof(float2) + 64;
+         4 * (size_t)M * sizeof(float) + (size_t)M * sizeof(float2) + 64;
 }
 
 void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
