@@ -239,6 +239,19 @@ def test_conventional_svd_denoise_cfg1(torch_cuda, fkk, cfg1, k_keep):
     assert err <= 1e-3, err
 
 
+@pytest.mark.parametrize("rows,k_keep", [(1, 1), (33, 3), (200, 12)])
+def test_conventional_ragged_small(torch_cuda, fkk, cfg1, rows, k_keep):
+    """Ragged / tiny cubes through the conventional workflow (one Gram split, partial tiles)."""
+    I, Iref = cfg1
+    I32 = I[:rows].astype(np.float32)
+    R32 = Iref.astype(np.float32)
+    plan = fkk.Plan(I.shape[1], 12, rows, in_dtype="f32")
+    K = plan.conventional(_dev(torch_cuda, I32), _dev(torch_cuda, R32), k_keep).cpu().numpy()
+    K_or = O.conventional_workflow(I32.astype(np.float64), R32.astype(np.float64), k_keep)
+    err = np.max(np.abs(K - K_or)) / np.max(np.abs(K_or))
+    assert err <= 1e-3, err
+
+
 def test_conventional_cfg2_sample(torch_cuda, fkk, cfg2):
     I, Iref = cfg2
     I = I[:512]
