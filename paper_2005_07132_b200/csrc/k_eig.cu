@@ -214,7 +214,7 @@ __device__ __forceinline__ double chain_sum(double v, double* buf) {
 //   t_j = 2 / v.v -> red[8];  d[j], e[j], tau[j] by the writer.
 // Only the two 128-thread sums synchronise.  pj = p_{j-1}[j], vj = v_{j-1}[j] are read by every thread
 // before any wp write.
-template <int NPL>
+template <int NPL, bool SIGNAL_W = false>
 __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], double (&X)[NPL], double pj,
                                              const double* vp, double* wp, double* v, double* red, double tprev,
                                              bool writer, double* d, double* e, double* tau) {
@@ -238,6 +238,9 @@ __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], do
       X[i] -= vj * w + wj * V[i];
       if (c < M) wp[c] = w;
     }
+    // w is complete: the pass warps may apply the pending update to their rows while this chain
+    // finishes the reflector (named barrier 2: 128 arrivals here + the 384 pass threads' bar.sync)
+    if constexpr (SIGNAL_W) asm volatile("bar.arrive 2, %0;" ::"r"(kTsThreads) : "memory");
   }
   double s2 = 0.0;
 #pragma unroll
@@ -381,13 +384,27 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
         pj = __ldcg(pprev + j);
       }
       stamp(j, 1);
-      column_chain<NPL>(j, M, Pv, X, pj, vp, wp, v, red, tprev, cta == 0, d, e, tau);
+      column_chain<NPL, true>(j, M, Pv, X, pj, vp, wp, v, red, tprev, cta == 0, d, e, tau);
       stamp(j, 2);
-    } else if (j > 0 && dbg != 5) {   // dbg 5: timing without the reflector stores (wrong results)
-      // reflector v_{j-1} -> dead row j-1, a 1/P slice per CTA
-      double* rj = Wk + (int64_t)(j - 1) * M;
-      const int len = (M - j + P - 1) / P, c0 = j + cta * len, c1 = min(M, c0 + len);
-      for (int c = c0 + tid - kTsChain; c < c1; c += nt - kTsChain) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+    } else if (j > 0) {
+      if (dbg != 5) {   // dbg 5: timing without the reflector stores (wrong results)
+        // reflector v_{j-1} -> dead row j-1, a 1/P slice per CTA
+        double* rj = Wk + (int64_t)(j - 1) * M;
+        const int len = (M - j + P - 1) / P, c0 = j + cta * len, c1 = min(M, c0 + len);
+        for (int c = c0 + tid - kTsChain; c < c1; c += nt - kTsChain) rj[c] = tprev != 0.0 ? vp[c] : 0.0;
+      }
+      // pending rank-2 update of the owned rows r > j as soon as w is known (overlaps the chain's
+      // second half): row -= v_{j-1}[r] w + w[r] v_{j-1} over c > j; the pass then only reads
+      asm volatile("bar.sync 2, %0;" ::"r"(kTsThreads) : "memory");
+      const int m0u = j + 1;
+      for (int i = warp - kTsChain / 32; i < R; i += nw - kTsChain / 32) {
+        const int r = cta + i * P;
+        if (r <= j || tprev == 0.0) continue;
+        double* row = rows + (size_t)i * M;
+        const double vr = vp[r], wr = wp[r];
+#pragma unroll 4
+        for (int c = m0u + lane; c < M; c += 32) row[c] -= vr * wp[c] + wr * vp[c];
+      }
     }
     __syncthreads();
     const double t = red[8];
@@ -395,12 +412,14 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
     // ---- pass over the owned rows r > j: pending update (eager, smem), p_r = t A^(j)[r,:] v_j
     const int m0 = j + 1;
     const bool last = j + 3 == M;
-    for (int i = warp; i < (dbg == 1 ? 0 : R); i += nw) {   // one warp per owned row; dbg 1: timing without the pass
+    // one non-chain warp per owned row (the same warp that applied its pending update above); dbg 1:
+    // timing without the pass
+    for (int i = warp - kTsChain / 32; i < (dbg == 1 || warp < kTsChain / 32 ? 0 : R); i += nw - kTsChain / 32) {
       const int r = cta + i * P;
       if (r <= j) continue;
       double* row = rows + (size_t)i * M;
       const bool publish = last && (r == j + 1 || r == M - 1);   // rows for the trailing 2 x 2 flush
-      const double acc = row_pass(row, 0, m0, M, j > 0, vp[r], wp[r], vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
+      const double acc = row_pass(row, 0, m0, M, false, 0.0, 0.0, vp, wp, v, publish ? Wk + (int64_t)r * M : nullptr);
       // p_r and A^(j)[r][j+1] into the column-parity buffers: a fast CTA's next pass never overwrites
       // what a slow CTA still reads
       if (lane == 0) {
