@@ -271,6 +271,27 @@ __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], do
   }
 }
 
+// row[c] -= vr w[c] + wr v_{j-1}[c] for c >= m0 (one warp): the loads of four iterations are issued
+// before their stores -- the compiler otherwise keeps every load behind the previous row store (the
+// arrays may alias), a ~100-cycle dependent chain per iteration (tools/micro/rowpass.cu)
+__device__ __forceinline__ void row_update(double* row, int m0, int M, double vr, double wr, const double* vp,
+                                           const double* wp) {
+  const int lane = threadIdx.x & 31;
+  int c = m0 + lane;
+  for (; c + 96 < M; c += 128) {
+    double a[4], ww[4], pp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = row[c + 32 * u];
+      ww[u] = wp[c + 32 * u];
+      pp[u] = vp[c + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) row[c + 32 * u] = a[u] - (vr * ww[u] + wr * pp[u]);
+  }
+  for (; c < M; c += 32) row[c] -= vr * wp[c] + wr * vp[c];
+}
+
 // The pass over one owned row r > j (one warp): pending update row -= v_{j-1}[r] w + w[r] v_{j-1} (if
 // pending) and the dot A^(j)[r,:] v_j over c > j.  Lane 0 handles c = j + 1 first, so row[j+1]
 // (= A^(j)[r][j+1]) is its own write.
@@ -402,8 +423,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) tridiag_rows_kernel(const doubl
         if (r <= j || tprev == 0.0) continue;
         double* row = rows + (size_t)i * M;
         const double vr = vp[r], wr = wp[r];
-#pragma unroll 4
-        for (int c = m0u + lane; c < M; c += 32) row[c] -= vr * wp[c] + wr * vp[c];
+        row_update(row, m0u, M, vr, wr, vp, wp);
       }
     }
     __syncthreads();
