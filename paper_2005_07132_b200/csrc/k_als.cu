@@ -169,17 +169,32 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
       auto passA = [&](auto bsub_c, auto fact_c) {
         constexpr bool BSUB = decltype(bsub_c)::value, FACT = decltype(fact_c)::value;
         int ix = ix0, i = i0;
+        // the next row's shared-memory operands are loaded at the top of each step, before this row's
+        // stores: the compiler otherwise orders every load behind the previous row's stores (the
+        // arrays may alias) and the smem latency joins the dependent chain (tools/micro/rowpass.cu)
+        const int ixmax = (T - 1) * NL + s;
+        double cy = 0.0, cg = 0.0, cl1 = 0.0, crd = 0.0;
+        if (nn > 0) {
+          cy = (double)sy[ix];
+          if constexpr (BSUB) { cg = sg[ix]; cl1 = sl1[ix]; crd = srd[ix]; }
+        }
         // one row in elimination order; ea/eb = near-spike entries (t < 2), LASTROW: l1 = 0
         // EDGE: this position may hold one of the rows 0, 1, M-2, M-1 (where D^T D's band differs);
         // only the peeled positions t = 0, 1, nn-2, nn-1 can, so the main loop runs without the check
         auto step = [&](auto last_c, auto edge_c, double ea, double eb) {
           constexpr bool LASTROW = decltype(last_c)::value, EDGE = decltype(edge_c)::value;
-          const double yv = (double)sy[ix];
+          const double yv = cy;
+          const double g_old = cg, l1_old = cl1, rd_old = crd;
+          {
+            const int ixn = min(max(ix + dix, s), ixmax);   // (clamped: past-the-segment rows are unused)
+            cy = (double)sy[ixn];
+            if constexpr (BSUB) { cg = sg[ixn]; cl1 = sl1[ixn]; crd = srd[ixn]; }
+          }
           double wv = 1.0;
           if constexpr (BSUB) {
             // previous order: this row's l1 / l2 couple to the rows visited just before (z1, z2;
             // both zero at the first rows, where the stored l1 is zero too)
-            const double zv = sg[ix] - sl1[ix] * z1 - lam * srd[ix] * z2;
+            const double zv = g_old - l1_old * z1 - lam * rd_old * z2;
             z2 = z1;
             z1 = zv;
             wv = yv > zv ? p : q;
@@ -367,15 +382,25 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
           constexpr bool FIRST = decltype(first_c)::value;
           double g1 = 0.0, g2 = 0.0, l1prev = 0.0, rdm1 = 0.0, rdm2 = 0.0;
           int ix = ix0;
+          const int ixmaxB = (T - 1) * NL + s;
+          // next row's operands loaded before this row's store (see pass A)
+          unsigned char nw_ = 0;
+          double ny = 0.0, nrd = 0.0, nl1 = 0.0;
+          if (nn > 0) { nw_ = sw[ix]; ny = (double)sy[ix]; nrd = srd[ix]; nl1 = sl1[ix]; }
           auto stepB = [&](double corr) {
-            const double wv = FIRST ? 1.0 : (sw[ix] ? p : q);
-            const double f = wv * (double)sy[ix] - corr;
-            const double rd = srd[ix];
+            const double wv = FIRST ? 1.0 : (nw_ ? p : q);
+            const double f = wv * ny - corr;
+            const double rd = nrd;
+            const double l1c = nl1;
+            {
+              const int ixn = min(max(ix + dix, s), ixmaxB);
+              nw_ = sw[ixn]; ny = (double)sy[ixn]; nrd = srd[ixn]; nl1 = sl1[ixn];
+            }
             const double g = f - l1prev * g1 - lam * rdm2 * g2;
             sg[ix] = g * rd;
             g2 = g1;
             g1 = g;
-            l1prev = sl1[ix];
+            l1prev = l1c;
             rdm2 = rdm1;
             rdm1 = rd;
             ix += dix;
