@@ -300,8 +300,27 @@ __device__ __forceinline__ double row_pass(double* row, int roff, int m0, int M,
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
   if (pending) {
-#pragma unroll 4
-    for (int c = m0 + lane; c < M; c += 32) {
+    // groups of four iterations with every load before the group's stores (see row_update)
+    int c = m0 + lane;
+    for (; c + 96 < M; c += 128) {
+      double a[4], ww[4], pp[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = row[c + 32 * u - roff];
+        ww[u] = wp[c + 32 * u];
+        pp[u] = vp[c + 32 * u];
+        vv[u] = v[c + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] -= vr * ww[u] + wr * pp[u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        row[c + 32 * u - roff] = a[u];
+        if (pub) pub[c + 32 * u] = a[u];
+        acc = fma(a[u], vv[u], acc);
+      }
+    }
+    for (; c < M; c += 32) {
       const double a = row[c - roff] - (vr * wp[c] + wr * vp[c]);
       row[c - roff] = a;
       if (pub) pub[c] = a;
