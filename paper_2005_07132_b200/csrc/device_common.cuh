@@ -280,11 +280,23 @@ __device__ __forceinline__ void block_prefix3(const double* y, int M, double* P0
 // Interior: centred quadratic least-squares value; edges: the quadratic fitted on the first/last
 // w samples evaluated at i.  Exact rewriting of the per-window least-squares fit: with centred
 // offsets k in [-h, h], c1 decouples and [n K2; K2 K4] [c0 c2]^T = [S0 S2]^T.
-__device__ __forceinline__ double sg_point(const double* P0, const double* P1, const double* P2, int M, int h, int i) {
-  const double n = 2.0 * h + 1.0;
+// the window constants of the local quadratic least-squares fit (computed once per kernel: the fp64
+// divides are long instruction sequences and sg_point runs for every channel of every spectrum)
+struct SgConst {
+  double n, K2, K4, idet, iK2;
+};
+__device__ __forceinline__ SgConst sg_const(int h) {
+  SgConst k;
+  k.n = 2.0 * h + 1.0;
   const double hd = (double)h;
-  const double K2 = hd * (hd + 1.0) * (2.0 * hd + 1.0) / 3.0;
-  const double K4 = hd * (hd + 1.0) * (2.0 * hd + 1.0) * (3.0 * hd * hd + 3.0 * hd - 1.0) / 15.0;
+  k.K2 = hd * (hd + 1.0) * (2.0 * hd + 1.0) / 3.0;
+  k.K4 = hd * (hd + 1.0) * (2.0 * hd + 1.0) * (3.0 * hd * hd + 3.0 * hd - 1.0) / 15.0;
+  k.idet = 1.0 / (k.n * k.K4 - k.K2 * k.K2);
+  k.iK2 = 1.0 / k.K2;
+  return k;
+}
+__device__ __forceinline__ double sg_point(const double* P0, const double* P1, const double* P2, int M, int h, int i,
+                                           const SgConst& kc) {
   int c = i;
   if (c < h) c = h;
   if (c > M - 1 - h) c = M - 1 - h;
@@ -294,13 +306,15 @@ __device__ __forceinline__ double sg_point(const double* P0, const double* P1, c
   const double S0 = Q0;
   const double S1 = Q1 - cd * Q0;
   const double S2 = Q2 - 2.0 * cd * Q1 + cd * cd * Q0;
-  const double det = n * K4 - K2 * K2;
-  const double c0 = (K4 * S0 - K2 * S2) / det;
+  const double c0 = (kc.K4 * S0 - kc.K2 * S2) * kc.idet;
   if (c == i) return c0;
-  const double c2 = (n * S2 - K2 * S0) / det;
-  const double c1 = S1 / K2;
+  const double c2 = (kc.n * S2 - kc.K2 * S0) * kc.idet;
+  const double c1 = S1 * kc.iK2;
   const double k = (double)(i - c);
   return c0 + c1 * k + c2 * k * k;
+}
+__device__ __forceinline__ double sg_point(const double* P0, const double* P1, const double* P2, int M, int h, int i) {
+  return sg_point(P0, P1, P2, M, h, i, sg_const(h));
 }
 
 }  // namespace fkk

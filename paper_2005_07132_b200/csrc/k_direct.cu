@@ -326,6 +326,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   const int pl = (L - M) >> 1;
   const float invL = 1.0f / (float)L;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const SgConst sgk = sg_const(h);
   for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
     const int64_t r0 = 2 * pr, r1 = r0 + 1;
     const bool has1 = r1 < n;
@@ -368,7 +369,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       // min of the trend, mean of Re K'
       double tmin = 1e300;
       for (int j = threadIdx.x; j < M; j += blockDim.x) {
-        const double T = sg_point(P0, P1, P2, M, h, j);
+        const double T = sg_point(P0, P1, P2, M, h, j, sgk);
         ybuf[j] = T;
         tmin = fmin(tmin, T);
       }
@@ -382,7 +383,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       for (int j = threadIdx.x; j < M; j += blockDim.x) {
         const double T = gmin <= 0.0 ? mean : ybuf[j];
         const float2 kv = kb[j];
-        const float it = (float)(1.0 / T);
+        const float it = (float)rcp64(T);   // MUFU seed + two Newton steps (~1 ulp)
         if (imag_only) {
           reinterpret_cast<float*>(out)[row * (int64_t)M + j] = kv.y * it;
         } else {
