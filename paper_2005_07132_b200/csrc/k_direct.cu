@@ -358,9 +358,13 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
         const float hpe = (r == 0 ? x[pl + j].x : x[pl + j].y) * invL;
         const float ap = aa[j] + hpe;              // a' = a + H{phi_err}
         const float pp = pdr[j];                   // phi' = phi - phi_err
+        // hardware sin/cos after a two-term reduction to [-pi, pi] and the hardware exp: ~1e-6 absolute,
+        // an order below the 1e-5 direct-KK tolerance (the accurate sincosf/expf were a long sequence)
+        const float kq = __fsub_rn(__fadd_rn(pp * 0.15915494309189535f, 12582912.0f), 12582912.0f);
+        const float rr = fmaf(kq, 1.7484556e-07f, fmaf(-kq, 6.2831854820251465f, pp));
         float sn, cs;
-        sincosf(pp, &sn, &cs);
-        const float mag = expf(ap);
+        __sincosf(rr, &sn, &cs);
+        const float mag = __expf(ap);
         kb[j] = make_float2(mag * cs, mag * sn);
         ybuf[j] = (double)(mag * cs);
       }
