@@ -20,7 +20,7 @@ __device__ __forceinline__ float log_ratio_elem(const TIn v, const float inv_ref
     return (float)(0.5 * log(fmax(r, (double)floor)));
   } else {
     float r = (float)v * inv_ref;
-    return 0.5f * logf(fmaxf(r, floor));
+    return 0.5f * __logf(fmaxf(r, floor));   // hardware log (<= 2 ulp; the direct path only)
   }
 }
 
@@ -90,16 +90,16 @@ direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __
           const float4 ir = *reinterpret_cast<const float4*>(inv_ref + 4 * q);
           const float4 v0 = nx0[u], v1 = nx1[u];
           bad |= !isfinite(v0.x) | !isfinite(v0.y) | !isfinite(v0.z) | !isfinite(v0.w);
-          a0[4 * q] = 0.5f * logf(fmaxf(v0.x * ir.x, floor));
-          a0[4 * q + 1] = 0.5f * logf(fmaxf(v0.y * ir.y, floor));
-          a0[4 * q + 2] = 0.5f * logf(fmaxf(v0.z * ir.z, floor));
-          a0[4 * q + 3] = 0.5f * logf(fmaxf(v0.w * ir.w, floor));
+          a0[4 * q] = 0.5f * __logf(fmaxf(v0.x * ir.x, floor));
+          a0[4 * q + 1] = 0.5f * __logf(fmaxf(v0.y * ir.y, floor));
+          a0[4 * q + 2] = 0.5f * __logf(fmaxf(v0.z * ir.z, floor));
+          a0[4 * q + 3] = 0.5f * __logf(fmaxf(v0.w * ir.w, floor));
           if (has1) {
             bad |= !isfinite(v1.x) | !isfinite(v1.y) | !isfinite(v1.z) | !isfinite(v1.w);
-            a1[4 * q] = 0.5f * logf(fmaxf(v1.x * ir.x, floor));
-            a1[4 * q + 1] = 0.5f * logf(fmaxf(v1.y * ir.y, floor));
-            a1[4 * q + 2] = 0.5f * logf(fmaxf(v1.z * ir.z, floor));
-            a1[4 * q + 3] = 0.5f * logf(fmaxf(v1.w * ir.w, floor));
+            a1[4 * q] = 0.5f * __logf(fmaxf(v1.x * ir.x, floor));
+            a1[4 * q + 1] = 0.5f * __logf(fmaxf(v1.y * ir.y, floor));
+            a1[4 * q + 2] = 0.5f * __logf(fmaxf(v1.z * ir.z, floor));
+            a1[4 * q + 3] = 0.5f * __logf(fmaxf(v1.w * ir.w, floor));
           } else {
             a1[4 * q] = a1[4 * q + 1] = a1[4 * q + 2] = a1[4 * q + 3] = 0.f;
           }
