@@ -214,6 +214,26 @@ __device__ __forceinline__ double chain_sum(double v, double* buf) {
 //   t_j = 2 / v.v -> red[8];  d[j], e[j], tau[j] by the writer.
 // Only the two 128-thread sums synchronise.  pj = p_{j-1}[j], vj = v_{j-1}[j] are read by every thread
 // before any wp write.
+// sqrt and 1/x for the column chain's critical path: MUFU seeds + Newton steps (~1 ulp; the IEEE
+// sequences were ~150 cycles of the per-column latency)
+__device__ __forceinline__ double chain_sqrt(double x) {
+  if (!(x > 0.0)) return 0.0;
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  const double s0 = x * r;
+  return fma(0.5 * r, fma(-s0, s0, x), s0);
+}
+__device__ __forceinline__ double chain_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int NPL, bool SIGNAL_W = false>
 __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], double (&X)[NPL], double pj,
                                              const double* vp, double* wp, double* v, double* red, double tprev,
@@ -255,11 +275,11 @@ __device__ __forceinline__ void column_chain(int j, int M, double (&Pv)[NPL], do
   if (ct == 0) red[13] = X[0];   // x[j]
   const double nrm2 = chain_sum(s2, red + 4);
   const double x0 = red[12];
-  const double nrm = sqrt(nrm2);
+  const double nrm = chain_sqrt(nrm2);
   const double alpha = x0 >= 0.0 ? -nrm : nrm;
   const double v0 = x0 - alpha;
   const double vtv = nrm2 - x0 * x0 + v0 * v0;
-  const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 / vtv;
+  const double t = (nrm == 0.0 || vtv == 0.0) ? 0.0 : 2.0 * chain_rcp(vtv);
   if (ct == 1) v[j + 1] = v0;
   if (ct == 0) {
     red[8] = t;
