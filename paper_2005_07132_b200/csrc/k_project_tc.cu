@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
 project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, const float* __restrict__ wimg, int kp,
                    float* __restrict__ US, float* __restrict__ ext_val, int64_t* __restrict__ ext_idx, int k,
                    int64_t row_offset, int want_ext, int nbuf, int abase, int NA, const float* __restrict__ inv_ref,
-                   float floor) {
+                   float floor, int ir_smem) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int NR = q_nraw(kp), NW = q_nw(kp);
@@ -345,6 +345,9 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
   float* red_v = reinterpret_cast<float*>(acc_empty + 2);      // [4 warps][2][128 cols]
   int* red_i = reinterpret_cast<int*>(red_v + 4 * 2 * 128);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_i + 4 * 2 * 128);
+  // inv_ref staged in shared memory (raw-cube mode, when it fits): the converters' per-stage L1 loads
+  // of it were their largest stall
+  float* sir = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~(uintptr_t)15);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (n + PTM - 1) / PTM;
@@ -358,6 +361,8 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
     tma::prefetch_map(&amap);
   }
   const int nseg = p_nseg(M), setc = p_set_cols(M, kp);
+  if (ir_smem)
+    for (int c = tid; c < ((M + 31) & ~31); c += blockDim.x) sir[c] = inv_ref[c];
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
@@ -429,7 +434,8 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
         float ir[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 v4 = __ldg(reinterpret_cast<const float4*>(inv_ref + c0) + u);
+          const float4 v4 = ir_smem ? reinterpret_cast<const float4*>(sir + c0)[u]
+                                    : __ldg(reinterpret_cast<const float4*>(inv_ref + c0) + u);
           ir[4 * u] = v4.x; ir[4 * u + 1] = v4.y; ir[4 * u + 2] = v4.z; ir[4 * u + 3] = v4.w;
         }
         const int nvalid = M - c0;   // channels c0 + i, i < nvalid, are real
@@ -664,7 +670,10 @@ void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int 
   if (project_use_tma(M, kp)) {
     if (kp > 128 || kp % 16 || p_set_cols(M, kp) > 512)
       throw Status(10, "project_tc: unsupported rank padding / channel count");
-    const size_t smem = qt_smem(kp);
+    size_t smem = qt_smem(kp);
+    const size_t irbytes = (size_t)((M + 31) & ~31) * sizeof(float) + 32;
+    const int ir_smem = (inv_ref && smem + irbytes <= 227 * 1024) ? 1 : 0;
+    if (ir_smem) smem += irbytes;
     FKK_CUDA_CHECK(cudaFuncSetAttribute(project_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -680,7 +689,7 @@ void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int 
       if (atoi(ev) > 0) na = std::min(na, atoi(ev));
     }
     project_tma_kernel<<<grid, QTHREADS, smem, s>>>(amap, n, M, wimg, kp, US, ext_val, ext_idx, k, row_offset, want_ext,
-                                                    nbuf, abase, na, inv_ref, floor);
+                                                    nbuf, abase, na, inv_ref, floor, ir_smem);
     check_launch("project_tma");
     return;
   }
