@@ -178,8 +178,17 @@ __device__ __forceinline__ void stockham_pass(cplx<T>* x, const cplx<T>* tw, int
       const int k = j % Ns;
       if (Ns > 1) {
         const int step = (L / (Ns * R)) * k;
+        {
+          // w^r from one table load and r-1 complex products (~r x 6e-8 relative): the other table
+          // loads were half of the pass's shared-memory reads
+          const cplx<T> w1 = tw_at(tw, step, L, INV);
+          cplx<T> wr = w1;
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], tw_at(tw, r * step, L, INV));
+          for (int r = 1; r < R; ++r) {
+            v[u][r] = cmul(v[u][r], wr);
+            wr = cmul(wr, w1);
+          }
+        }
       }
       dft_small<T, R, INV>(v[u]);
     }
