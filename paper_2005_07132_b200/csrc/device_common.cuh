@@ -198,10 +198,19 @@ __device__ __forceinline__ void stockham_pass(cplx<T>* x, const cplx<T>* tw, int
   for (int u = 0; u < NBT; ++u) {
     const int j = jj[u];
     if (j < nb) {
-      const int k = j % Ns;
-      const int base = (j / Ns) * Ns * R + k;
+      if (sizeof(T) == 4 && Ns == 1 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        // first pass: this thread's R outputs are contiguous (x[j R + r]) -> 16-B stores (the 8-B
+        // stores at a 64-B lane stride were 16-way bank conflicted)
+        float4* dst = reinterpret_cast<float4*>(x + j * R);
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[base + r * Ns] = v[u][r];
+        for (int r = 0; r < R; r += 2)
+          dst[r / 2] = make_float4((float)v[u][r].x, (float)v[u][r].y, (float)v[u][r + 1].x, (float)v[u][r + 1].y);
+      } else {
+        const int k = j % Ns;
+        const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[base + r * Ns] = v[u][r];
+      }
     }
   }
   __syncthreads();
