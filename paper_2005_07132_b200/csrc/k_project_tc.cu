@@ -413,38 +413,54 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
     const int hc = warp >= 12 ? 16 : 0;                    // first channel of this warp's half
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ring ra, rt;
+    // explicit shared-space loads (the swizzled row and inv_ref): the generic pointers above compile
+    // to generic LD.E, whose latency was the converters' largest stall
+    const uint32_t ring_a_s = tc::smem_u32(ring_a) + (uint32_t)(r * 128);
+    const uint32_t sir_s = tc::smem_u32(sir);
+    const float kHalfLn2 = 0.34657359027997264f;
+    int st = 0;
     for (int64_t pos = 0; pos < npos; ++pos, ra.next(NR), rt.next(NA)) {
       tc::mbar_wait(&a_full[ra.slot], ra.phase);
-      const unsigned char* rowp = ring_a + ra.slot * QA_BYTES + r * 128;
+      const uint32_t rows = ring_a_s + (uint32_t)(ra.slot * QA_BYTES);
       float x[16];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int cc = (hc >> 2) + c;   // logical 16-B chunk
-        const float4 v = *reinterpret_cast<const float4*>(rowp + ((cc ^ (r & 7)) << 4));
-        x[4 * c] = v.x;
-        x[4 * c + 1] = v.y;
-        x[4 * c + 2] = v.z;
-        x[4 * c + 3] = v.w;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x[4 * c]), "=f"(x[4 * c + 1]), "=f"(x[4 * c + 2]), "=f"(x[4 * c + 3])
+                     : "r"(rows + (uint32_t)((cc ^ (r & 7)) << 4)));
       }
       if (inv_ref) {
-        // the tile is the raw cube: A0 = 1/2 ln(max(I / I_ref, floor)) here (hardware log, <= 2 ulp;
-        // channels >= M zero like the A0 image), so the log-ratio pass never writes A0 to HBM
-        const int c0 = (int)(pos % nst) * QKC + hc;
+        // the tile is the raw cube: A0 = 1/2 ln(max(I / I_ref, floor)) here (hardware log2, flush to
+        // zero: the argument is >= floor > 0; channels >= M zero like the A0 image), so the log-ratio
+        // pass never writes A0 to HBM
+        const int c0 = st * QKC + hc;
         // inv_ref is zero-padded to a multiple of 32: broadcast float4 loads, no predication
         float ir[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 v4 = ir_smem ? reinterpret_cast<const float4*>(sir + c0)[u]
-                                    : __ldg(reinterpret_cast<const float4*>(inv_ref + c0) + u);
-          ir[4 * u] = v4.x; ir[4 * u + 1] = v4.y; ir[4 * u + 2] = v4.z; ir[4 * u + 3] = v4.w;
+          if (ir_smem) {
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(ir[4 * u]), "=f"(ir[4 * u + 1]), "=f"(ir[4 * u + 2]), "=f"(ir[4 * u + 3])
+                         : "r"(sir_s + (uint32_t)((c0 + 4 * u) * 4)));
+          } else {
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(inv_ref + c0) + u);
+            ir[4 * u] = v4.x; ir[4 * u + 1] = v4.y; ir[4 * u + 2] = v4.z; ir[4 * u + 3] = v4.w;
+          }
         }
-        const int nvalid = M - c0;   // channels c0 + i, i < nvalid, are real
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a0 = 0.5f * __logf(fmaxf(x[i] * ir[i], floor));
-          x[i] = i < nvalid ? a0 : 0.0f;
+          float l2;
+          asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(fmaxf(x[i] * ir[i], floor)));
+          x[i] = kHalfLn2 * l2;
+        }
+        const int nvalid = M - c0;   // channels c0 + i, i < nvalid, are real
+        if (nvalid < 16) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) x[i] = i < nvalid ? x[i] : 0.0f;
         }
       }
+      if (++st == nst) st = 0;
       float hi[16], lo[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) tc::split_fast(x[i], hi[i], lo[i]);
