@@ -169,17 +169,18 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
         if (want_ext) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            float vmax = valid ? v[q] : -INFINITY, vmin = valid ? v[q] : INFINITY;
-            int imax = valid ? row : 0x7fffffff, imin = imax;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, vmax, o);
-              const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
-              if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
-              const float nv = __shfl_xor_sync(0xffffffffu, vmin, o);
-              const int ni = __shfl_xor_sync(0xffffffffu, imin, o);
-              if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
-            }
+            // warp max/min with the smallest row among ties, by redux.sync on order-preserving
+            // integer keys (+0 canonicalises -0, which compares equal to it)
+            const uint32_t u = __float_as_uint(v[q] + 0.0f);
+            const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+            const uint32_t kM = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
+            const uint32_t km = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
+            const int imax = (int)__reduce_min_sync(0xffffffffu, (valid && key == kM) ? (uint32_t)row : 0x7fffffffu);
+            const int imin = (int)__reduce_min_sync(0xffffffffu, (valid && key == km) ? (uint32_t)row : 0x7fffffffu);
+            const float vmax = imax == 0x7fffffff ? -INFINITY
+                                                  : __uint_as_float((kM & 0x80000000u) ? (kM & 0x7fffffffu) : ~kM);
+            const float vmin = imin == 0x7fffffff ? INFINITY
+                                                  : __uint_as_float((km & 0x80000000u) ? (km & 0x7fffffffu) : ~km);
             if (lane == 0) {
               red_v[(ew * 2 + 0) * 128 + c0 + q] = vmax;
               red_i[(ew * 2 + 0) * 128 + c0 + q] = imax;
@@ -507,17 +508,18 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
         if (want_ext) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            float vmax = valid ? v[q] : -INFINITY, vmin = valid ? v[q] : INFINITY;
-            int imax = valid ? row : 0x7fffffff, imin = imax;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, vmax, o);
-              const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
-              if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
-              const float nv = __shfl_xor_sync(0xffffffffu, vmin, o);
-              const int ni = __shfl_xor_sync(0xffffffffu, imin, o);
-              if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
-            }
+            // warp max/min with the smallest row among ties, by redux.sync on order-preserving
+            // integer keys (+0 canonicalises -0, which compares equal to it)
+            const uint32_t u = __float_as_uint(v[q] + 0.0f);
+            const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+            const uint32_t kM = __reduce_max_sync(0xffffffffu, valid ? key : 0u);
+            const uint32_t km = __reduce_min_sync(0xffffffffu, valid ? key : 0xffffffffu);
+            const int imax = (int)__reduce_min_sync(0xffffffffu, (valid && key == kM) ? (uint32_t)row : 0x7fffffffu);
+            const int imin = (int)__reduce_min_sync(0xffffffffu, (valid && key == km) ? (uint32_t)row : 0x7fffffffu);
+            const float vmax = imax == 0x7fffffff ? -INFINITY
+                                                  : __uint_as_float((kM & 0x80000000u) ? (kM & 0x7fffffffu) : ~kM);
+            const float vmin = imin == 0x7fffffff ? INFINITY
+                                                  : __uint_as_float((km & 0x80000000u) ? (km & 0x7fffffffu) : ~km);
             if (lane == 0) {
               red_v[(ew * 2 + 0) * 128 + c0 + q] = vmax;
               red_i[(ew * 2 + 0) * 128 + c0 + q] = imax;
