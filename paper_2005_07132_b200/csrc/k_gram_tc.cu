@@ -230,6 +230,12 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
 // needs no producer threads: one loader lane bulk-copies (cp.async.bulk, mbarrier tx) 2 or 4 blocks
 // per stage, so the A0 stream has no register lookahead limit and no transposes on the Gram's SMs.
 // Pixels >= n and channels >= M are zero in the image; split boundaries are stage aligned.
+__device__ __forceinline__ float half_ln(float x) {
+  float l2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(x));
+  return 0.34657359027997264f * l2;   // ln 2 / 2
+}
+
 __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restrict__ I, int64_t n, int M,
                                                            const float* __restrict__ inv_ref, float floor,
                                                            float* __restrict__ A, unsigned char* __restrict__ Apre,
@@ -274,10 +280,12 @@ __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restri
         if (raw) {   // image of the raw cube (the conventional workflow's SVD, reading A26)
           o = v;
         } else {
-          o.x = 0.5f * logf(fmaxf(v.x * ir.x, floor));     // same arithmetic as logratio_kernel
-          o.y = 0.5f * logf(fmaxf(v.y * ir.y, floor));
-          o.z = 0.5f * logf(fmaxf(v.z * ir.z, floor));
-          o.w = 0.5f * logf(fmaxf(v.w * ir.w, floor));
+          // hardware log2 (<= 2 ulp, as the projection's raw-cube converters: reading A25); the
+          // argument is >= floor > 0, so flush-to-zero never applies
+          o.x = half_ln(fmaxf(v.x * ir.x, floor));
+          o.y = half_ln(fmaxf(v.y * ir.y, floor));
+          o.z = half_ln(fmaxf(v.z * ir.z, floor));
+          o.w = half_ln(fmaxf(v.w * ir.w, floor));
         }
         if (A) *reinterpret_cast<float4*>(A + px * (int64_t)M + col) = o;   // A == nullptr: image only
       }
