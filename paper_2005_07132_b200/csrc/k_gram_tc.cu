@@ -236,7 +236,7 @@ __device__ __forceinline__ float half_ln(float x) {
   return 0.34657359027997264f * l2;   // ln 2 / 2
 }
 
-__global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restrict__ I, int64_t n, int M,
+__global__ void __launch_bounds__(256, 4) logratio_pre_kernel(const float* __restrict__ I, int64_t n, int M,
                                                            const float* __restrict__ inv_ref, float floor,
                                                            float* __restrict__ A, unsigned char* __restrict__ Apre,
                                                            int64_t nq, int nT, int* __restrict__ flags, int raw) {
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restri
     }
   };
   load(blockIdx.x);
-  int buf = 0;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, buf ^= 1) {
+  const int buf = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t q = it / nT;
     const int cb = (int)(it - q * nT);
     const int col = cb * GT + 4 * c4;
@@ -291,8 +291,9 @@ __global__ void __launch_bounds__(256) logratio_pre_kernel(const float* __restri
       }
       x[e] = o;
     }
-    // buffer `buf` was last read by the bulk store issued two items ago
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    // the single buffer was last read by the bulk store issued one item ago (its smem reads finish
+    // while this item's loads and logs run); one buffer -> 33 KB per CTA, 4 CTAs per SM
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncthreads();
     unsigned char* hi = simg + buf * 2 * GOP_BYTES;
 #pragma unroll
@@ -543,8 +544,8 @@ void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = nq * nT;
-  const int grid = (int)std::min<int64_t>(items, (int64_t)sms * 3);
-  const int smem = 4 * GOP_BYTES;
+  const int grid = (int)std::min<int64_t>(items, (int64_t)sms * 4);
+  const int smem = 2 * GOP_BYTES;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(logratio_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   logratio_pre_kernel<<<grid, 256, smem, s>>>(I, n, M, inv_ref, floor, A, Apre, nq, nT, flags, raw);
   check_launch("logratio_pre");
