@@ -1612,7 +1612,9 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   }
   FKK_CUDA_CHECK(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(2 * (size_t)M * sizeof(double))));
-  bisect_kernel<<<k, 128, 2 * (size_t)M * sizeof(double), s>>>(d, e, M, k, lam, tnorm);
+  int bth = 128;
+  if (const char* ev = getenv("FKK_BISECT_THREADS")) bth = std::max(32, std::min(1024, atoi(ev)) / 32 * 32);   // A/B
+  bisect_kernel<<<k, bth, 2 * (size_t)M * sizeof(double), s>>>(d, e, M, k, lam, tnorm);
   check_launch("eig_bisect");
   const size_t ism = (size_t)5 * M * sizeof(double) + (size_t)M + 16;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(inviter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ism));
