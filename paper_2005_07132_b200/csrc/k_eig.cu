@@ -1237,19 +1237,33 @@ __global__ void __launch_bounds__(32 * kBxW) backxform_wy_kernel(const double* _
     zr[u] = c < M ? Z[(int64_t)jj * M + c] : 0.0;
   }
   const int nblk = (nrefl + kWyB - 1) / kWyB;
-  for (int p = nblk - 1; p >= 0; --p) {
-    const int j0 = p * kWyB, nb = min(kWyB, nrefl - j0);
-    // the block's V entries of this thread's rows (registers), loaded in one batch
-    double vr[kWyB][NPL];
+  // the next block's V entries of this thread's rows are prefetched into shared memory by cp.async
+  // (zero-filled outside the reflector) while this block computes: the per-block L2 latency of the
+  // 16 rows was the kernel's critical path.  Each thread reads back only its own slots.
+  extern __shared__ double vnext[];   // [kWyB][NPL][NT]
+  auto prefetch = [&](int pb) {
+    const int pj0 = pb * kWyB, pnb = min(kWyB, nrefl - pj0);
 #pragma unroll
-    for (int i = 0; i < kWyB; ++i) {
-      const double* vi = Wk + (int64_t)(j0 + i) * M;
+    for (int i = 0; i < kWyB; ++i)
 #pragma unroll
       for (int u = 0; u < NPL; ++u) {
         const int c = tid + NT * u;
-        vr[i][u] = (i < nb && c > j0 + i && c < M) ? __ldg(vi + c) : 0.0;
+        const bool ok = i < pnb && c > pj0 + i && c < M;
+        const double* src = ok ? Wk + (int64_t)(pj0 + i) * M + c : Wk;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&vnext[(i * NPL + u) * NT + tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
       }
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch(nblk - 1);
+  for (int p = nblk - 1; p >= 0; --p) {
+    double vr[kWyB][NPL];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < kWyB; ++i)
+#pragma unroll
+      for (int u = 0; u < NPL; ++u) vr[i][u] = vnext[(i * NPL + u) * NT + tid];
+    if (p > 0) prefetch(p - 1);
     // w = V^T z: per-thread partials of all dots, lane-transposed warp sums, 8-warp sum
     double part[kWyB];
 #pragma unroll
@@ -1658,8 +1672,11 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     FKK_CUDA_CHECK(cudaFuncSetAttribute(wy_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     wy_t_kernel<<<nblk, 256, tsm, s>>>(A, tau, M, nrefl, Tg);
     check_launch("eig_wy_t");
-    if (M <= 32 * kBxW * 2) backxform_wy_kernel<2><<<k, 32 * kBxW, 0, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
-    else backxform_wy_kernel<4><<<k, 32 * kBxW, 0, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
+    const int npl = M <= 32 * kBxW * 2 ? 2 : 4;
+    const int wsm = kWyB * npl * 32 * kBxW * (int)sizeof(double);   // the prefetched block
+    auto kb = npl == 2 ? backxform_wy_kernel<2> : backxform_wy_kernel<4>;
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm));
+    kb<<<k, 32 * kBxW, wsm, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
     check_launch("eig_backxform_wy");
     return;
   }
