@@ -143,8 +143,8 @@ struct fkk_plan {
   int2* gtc_tiles = nullptr;
   int* gtc_tile_of = nullptr;
   int gtc_ntiles = 0, gtc_nTj = 0, gtc_nsplit = 0;
-  // Gram variants (3xTF32): 0 = 1-CTA 128x128 fed by the pre-split A0 image (default), 1 = CTA pairs
-  // 256x256 fed by the image (same speed at cfg3), 2 = 1-CTA with in-kernel producers (fp64 input /
+  // Gram variants (3xTF32): 0 = 1-CTA 128x128 fed by the pre-split A0 image, 1 = CTA pairs 256x256
+  // fed by the image (default when ceil(M/128) is even), 2 = 1-CTA with in-kernel producers (fp64 input /
   // loopback shards), 3 = CTA pairs with in-kernel producers (measurement only).  FKK_GRAM_MODE overrides.
   int gram_mode = 0;
   bool gtc_pair = false;
@@ -310,7 +310,9 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   if (d->gemm_impl == FKK_GEMM_3XTF32) {
     std::vector<int2> tl;
     std::vector<int> tof;
-    int mode = 0;
+    // CTA pairs (256 x 256 tiles) when they add no channel padding over 128 x 128 tiles: after the
+    // batched fp64 flush they are faster (3.50 vs 3.61 ms at cfg3)
+    int mode = ((M + 127) / 128) % 2 == 0 ? 1 : 0;
     if (const char* ev = getenv("FKK_GRAM_MODE")) mode = atoi(ev) & 3;
     if ((mode == 0 || mode == 1) && (d->in_dtype || d->loopback_shards > 1)) mode = 2;   // image needs fp32, 1 shard
     p->gram_mode = mode;
@@ -401,6 +403,21 @@ void check_cube_args(fkk_plan* p, const void* cube, int64_t n_rows, const void* 
 }
 
 // F0..F4: log-ratio, Gram (all-reduced), eig -> V64 (device), s (host).
+// Gram from the pre-split image (modes 0 / 1): fp64 partials per (tile, split), reduced into G
+// (accumulated onto G when `accumulate`)
+static void gram_from_image(fkk_plan* p, int64_t n_rows, int64_t nr, bool accumulate, cudaStream_t s) {
+  const int M = p->M;
+  if (p->gtc_pair) {
+    const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
+    fkk::launch_gram_pre2(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+    fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, accumulate, s);
+  } else {
+    const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
+    fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+    fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, accumulate, s);
+  }
+}
+
 void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_iref, int64_t n_global) {
   cudaStream_t s = p->stream;
   const int M = p->M, k = p->k;
@@ -431,14 +448,8 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
     if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
       const int64_t nr = std::max<int64_t>(r1 - r0, 1);
-      if (pre && p->gtc_pair) {
-        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
-        fkk::launch_gram_pre2(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
-        fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
-      } else if (pre) {
-        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
-        fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
-        fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
+      if (pre) {
+        gram_from_image(p, n_rows, nr, sh > 0, s);
       } else if (p->gtc_pair) {
         const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
         fkk::launch_gram_tc2(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
@@ -893,9 +904,7 @@ fkk_status fkk_conventional(fkk_plan_t p, const void* d_icars, int64_t n_rows, c
     // Gram of the raw cube (image with raw = 1) and the eigensolver
     fkk::launch_logratio_pre(static_cast<const float*>(d_icars), n_rows, M, p->apre_blocks, p->inv_ref,
                              (float)p->d.ratio_floor, nullptr, p->apre, p->flags, s, 1);
-    const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, n_rows));
-    fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
-    fkk::launch_gram_tc_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, false, s);
+    gram_from_image(p, n_rows, n_rows, false, s);
     p->mark("gram");
     fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, p->flags, s);
     p->check_flags_sync();

@@ -8,8 +8,9 @@
 // engine writes 66 KB per 32-pixel stage (43 B/clk): ~105 B/clk of the 128 B/clk smem bandwidth,
 // against 128 B/clk for the MMA reads alone in the 1-CTA 128 x 128 kernel.
 //
-// STATUS: parity-green, opt-in (FKK_GRAM_MODE=1): measured 3.89 ms at cfg3, the same as the 1-CTA
-// image-fed kernel (3.88 ms; tensor pipe 65% vs 60% active), so the simpler 1-CTA kernel is the default.
+// STATUS: parity-green; the default when ceil(M/128) is even (no extra channel padding).  Measured at
+// cfg3: 3.50 ms vs 3.61 ms for the 1-CTA image-fed kernel, once the fp64 flush of the register sums
+// was batched (before: 3.89 vs 3.88 ms, both MMA warps waiting on the epilogue ~18% of the time).
 //
 // Accuracy: hi*hi and the cross terms share one TMEM accumulator per
 // buffer (256 columns, double-buffered = the 512 TMEM columns), drained every 64 pixels (24
@@ -165,11 +166,17 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
       if (lane == 0) arrive_on_relaxed(&acc_empty[b], 0);   // TMEM drained: orders no memory
       const bool last = pidx == nper - 1;
       if (last || ((pidx + 1) * PERIOD) % FLUSH == 0) {
+        // fp64 flush in batches of 16 (one L2 round trip per batch, as gram_pre_kernel)
 #pragma unroll
-        for (int q = 0; q < 128; ++q) {
-          double* p = part + (int64_t)(128 * chalf + q) * T2 + i;
-          *p = (first ? 0.0 : *p) + (double)S[q];
-          S[q] = 0.f;
+        for (int q0 = 0; q0 < 128; q0 += 16) {
+          double old[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) old[u] = first ? 0.0 : part[(int64_t)(128 * chalf + q0 + u) * T2 + i];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            part[(int64_t)(128 * chalf + q0 + u) * T2 + i] = old[u] + (double)S[q0 + u];
+            S[q0 + u] = 0.f;
+          }
         }
         first = false;
       }

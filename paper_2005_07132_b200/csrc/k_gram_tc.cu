@@ -162,11 +162,19 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
       tc::mbar_arrive(&acc_empty[b]);
       const bool last = pidx == nper - 1;
       if (last || ((pidx + 1) * GPERIOD) % GFLUSH == 0) {
+        // fp64 flush in batches of 16: the batch's loads are issued together (one L2 round trip per
+        // batch; load/store interleaving per entry serialised 64 round trips, which stalled the MMA
+        // warp on acc_empty for ~18% of the kernel)
 #pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          double* p = part + (int64_t)(64 * chalf + q) * GT + i;
-          *p = (first ? 0.0 : *p) + (double)S[q];
-          S[q] = 0.f;
+        for (int q0 = 0; q0 < 64; q0 += 16) {
+          double old[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) old[u] = first ? 0.0 : part[(int64_t)(64 * chalf + q0 + u) * GT + i];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            part[(int64_t)(64 * chalf + q0 + u) * GT + i] = old[u] + (double)S[q0 + u];
+            S[q0 + u] = 0.f;
+          }
         }
         first = false;
       }
@@ -336,7 +344,7 @@ constexpr int GPTHREADS = 320;   // warps 0-7 epilogue, 8 MMA issue, 9 bulk load
 
 __global__ void __launch_bounds__(GPTHREADS, 1)
 gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, const int2* __restrict__ tiles,
-                int ntiles, double* __restrict__ partials) {
+                int ntiles, double* __restrict__ partials, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + GSTAGES * GSTAGE_BYTES);
   uint64_t* full = bars;                  // [GSTAGES]  bulk copies (tx) -> MMA
@@ -395,11 +403,19 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
       tc::mbar_arrive(&acc_empty[b]);
       const bool last = pidx == nper - 1;
       if (last || ((pidx + 1) * GPERIOD) % GFLUSH == 0) {
+        // fp64 flush in batches of 16: the batch's loads are issued together (one L2 round trip per
+        // batch; load/store interleaving per entry serialised 64 round trips, which stalled the MMA
+        // warp on acc_empty for ~18% of the kernel)
 #pragma unroll
-        for (int q = 0; q < 64; ++q) {
-          double* p = part + (int64_t)(64 * chalf + q) * GT + i;
-          *p = (first ? 0.0 : *p) + (double)S[q];
-          S[q] = 0.f;
+        for (int q0 = 0; q0 < 64; q0 += 16) {
+          double old[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) old[u] = first ? 0.0 : part[(int64_t)(64 * chalf + q0 + u) * GT + i];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            part[(int64_t)(64 * chalf + q0 + u) * GT + i] = old[u] + (double)S[q0 + u];
+            S[q0 + u] = 0.f;
+          }
         }
         first = false;
       }
@@ -413,10 +429,14 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
     uint32_t phase = 0;
     uint32_t eph[2] = {0, 0};
     const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), GLBO, GSBO);
+    unsigned long long w_full = 0, w_acc = 0;   // dbg: cycles waiting for operands / for the epilogue
+    const unsigned long long t_start = clock64();
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
       if (pidx >= 2) {
+        const unsigned long long c0 = dbg ? clock64() : 0;
         tc::mbar_wait(&acc_empty[b], eph[b]);
+        if (dbg) w_acc += clock64() - c0;
         eph[b] ^= 1;
         tc::tc_fence_after();
       }
@@ -424,7 +444,9 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
       const int64_t q0 = qb + pidx * SPP, q1 = (qe < q0 + SPP) ? qe : (q0 + SPP);
       uint32_t acc = 0;
       for (int64_t q = q0; q < q1; ++q) {
+        const unsigned long long c0 = dbg ? clock64() : 0;
         tc::mbar_wait(&full[stage], phase);
+        if (dbg) w_full += clock64() - c0;
         tc::tc_fence_after();
         const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * GSTAGE_BYTES)), dal = tc::sdesc_add(dah, GOP_BYTES);
         const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, 2 * GOP_BYTES);
@@ -446,6 +468,12 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
       }
       if (tc::elect_one()) tc::mma_commit(&acc_full[b]);
       __syncwarp();
+    }
+    if (dbg && lane == 0) {
+      dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
+      dbg[blockIdx.x * 4 + 1] = w_full;
+      dbg[blockIdx.x * 4 + 2] = w_acc;
+      dbg[blockIdx.x * 4 + 3] = (unsigned long long)diag;
     }
   } else if (lane == 0) {
     // ------------------------------------------------------------ bulk loader (warp 9, one lane)
@@ -555,8 +583,31 @@ void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, 
                      double* partials, cudaStream_t s) {
   const int64_t nq = (n + GKC - 1) / GKC;
   FKK_CUDA_CHECK(cudaFuncSetAttribute(gram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM));
-  gram_pre_kernel<<<ntiles * nsplit, GPTHREADS, GSMEM, s>>>(Apre, n, nq, d_tiles, ntiles, partials);
+  // FKK_GRAM_DBG (debug only): per-CTA MMA-warp cycle split (total, waiting for operands, waiting
+  // for the epilogue) of each launch, printed to stderr; synchronises the stream
+  static const bool gdbg = getenv("FKK_GRAM_DBG") != nullptr;
+  unsigned long long* dbg = nullptr;
+  const int nblk = ntiles * nsplit;
+  if (gdbg) FKK_CUDA_CHECK(cudaMalloc(&dbg, (size_t)nblk * 4 * sizeof(unsigned long long)));
+  gram_pre_kernel<<<nblk, GPTHREADS, GSMEM, s>>>(Apre, n, nq, d_tiles, ntiles, partials, dbg);
   check_launch("gram_pre");
+  if (gdbg) {
+    std::vector<unsigned long long> h((size_t)nblk * 4);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(dbg);
+    double tot[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    int cnt[2] = {0, 0};
+    for (int b = 0; b < nblk; ++b) {
+      const int dg = (int)h[b * 4 + 3];
+      for (int q = 0; q < 3; ++q) tot[dg][q] += (double)h[b * 4 + q];
+      cnt[dg]++;
+    }
+    for (int dg = 0; dg < 2; ++dg)
+      if (cnt[dg])
+        fprintf(stderr, "gram_pre dbg %s: %d CTAs, mean cycles total %.0f, wait operands %.0f, wait epilogue %.0f\n",
+                dg ? "diag" : "offdiag", cnt[dg], tot[dg][0] / cnt[dg], tot[dg][1] / cnt[dg], tot[dg][2] / cnt[dg]);
+  }
 }
 
 }  // namespace fkk
