@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "fkk_internal.h"
@@ -98,7 +100,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uin
 
 __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char* __restrict__ Apre, int64_t nq,
                                                             const int2* __restrict__ tiles, int ntiles,
-                                                            double* __restrict__ partials) {
+                                                            double* __restrict__ partials,
+                                                            unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTG * STB);
   uint64_t* full = bars;                    // [NSTG] local: this CTA's bulk copies (tx)
@@ -191,10 +194,14 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
       uint32_t phase = 0;
       uint32_t eph[2] = {0, 0};
       const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), LBO, SBO);
+      unsigned long long w_full = 0, w_peer = 0, w_acc = 0;   // dbg cycle split
+      const unsigned long long t_start = clock64();
       for (int64_t pidx = 0; pidx < nper; ++pidx) {
         const int b = (int)(pidx & 1);
         if (pidx >= 2) {
+          const unsigned long long c0 = dbg ? clock64() : 0;
           wait_cluster(&acc_empty[b], eph[b]);
+          if (dbg) w_acc += clock64() - c0;
           eph[b] ^= 1;
           tc::tc_fence_after();
         }
@@ -202,8 +209,11 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
         const int64_t q0 = qb + pidx * SPP, q1 = (qe < q0 + SPP) ? qe : (q0 + SPP);
         uint32_t acc = 0;
         for (int64_t q = q0; q < q1; ++q) {
+          const unsigned long long c0 = dbg ? clock64() : 0;
           tc::mbar_wait(&full[stage], phase);
+          const unsigned long long c1 = dbg ? clock64() : 0;
           wait_cluster(&pfull[stage], phase);
+          if (dbg) { w_full += c1 - c0; w_peer += clock64() - c1; }
           tc::tc_fence_after();
           const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * STB)), dal = tc::sdesc_add(dah, OPB);
           const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, HALF);
@@ -225,6 +235,12 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
         }
         if (tc::elect_one()) commit2(&acc_full[b]);
         __syncwarp();
+      }
+      if (dbg && lane == 0) {
+        dbg[pair * 4 + 0] = clock64() - t_start;
+        dbg[pair * 4 + 1] = w_full;
+        dbg[pair * 4 + 2] = w_peer;
+        dbg[pair * 4 + 3] = w_acc;
       }
     }
   } else if (warp == 9) {
@@ -286,8 +302,24 @@ void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gram_pre2_kernel, Apre, nq, d_tiles, ntiles, partials));
+  // FKK_GRAM_DBG (debug only): leader MMA-warp cycle split per pair, printed to stderr; synchronises
+  static const bool gdbg = getenv("FKK_GRAM_DBG") != nullptr;
+  unsigned long long* dbg = nullptr;
+  const int npair = ntiles * nsplit;
+  if (gdbg) FKK_CUDA_CHECK(cudaMalloc(&dbg, (size_t)npair * 4 * sizeof(unsigned long long)));
+  FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gram_pre2_kernel, Apre, nq, d_tiles, ntiles, partials, dbg));
   check_launch("gram_pre2");
+  if (gdbg) {
+    std::vector<unsigned long long> h((size_t)npair * 4);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(dbg);
+    double tot[4] = {0, 0, 0, 0};
+    for (int b = 0; b < npair; ++b)
+      for (int q = 0; q < 4; ++q) tot[q] += (double)h[b * 4 + q] / npair;
+    fprintf(stderr, "gram_pre2 dbg: %d pairs, mean cycles total %.0f, wait own stage %.0f, wait peer %.0f, wait epilogue %.0f\n",
+            npair, tot[0], tot[1], tot[2], tot[3]);
+  }
 }
 
 }  // namespace fkk
