@@ -75,7 +75,7 @@ typedef struct {
   int32_t rank_k;            /* k: 1 <= k <= min(M, 128, N_global) retained singular triplets */
   int32_t fft_len;           /* L: 0 -> 2*nextpow2(M); else a power of two >= M, <= 8192 */
   int32_t pad_mode;          /* fkk_pad_mode, default FKK_PAD_REFLECT (reading A3) */
-  double ratio_floor;        /* clamp of I/I_ref before ln, default 1e-6 (reading A16) */
+  double ratio_floor;        /* clamp of I/I_ref before ln, default 1e-6 (reading A16); must be >= FLT_MIN */
   int32_t f_mode;            /* fkk_f_mode: f(omega) of Eq. 9 or f == 1 (default) */
   double f_alpha, f_sigma_g; /* Eq. 9 Poisson multiplier and Gaussian sigma */
   double als_lambda;         /* ALS smoothness, default 1e4 */

@@ -252,7 +252,9 @@ void validate_desc(const fkk_plan_desc* d) {
       throw Status(FKK_ERR_INVALID_ARG, "fft_len must be a power of two in [M, 8192]");
   }
   if (d->pad_mode != FKK_PAD_REFLECT && d->pad_mode != FKK_PAD_ZERO) throw Status(FKK_ERR_INVALID_ARG, "bad pad_mode");
-  if (!(d->ratio_floor > 0)) throw Status(FKK_ERR_INVALID_ARG, "ratio_floor must be > 0");
+  // >= FLT_MIN: the kernels take the log of max(I / I_ref, floor) in fp32 with flush-to-zero hardware lg2
+  if (!(d->ratio_floor >= 1.1754943508222875e-38))
+    throw Status(FKK_ERR_INVALID_ARG, "ratio_floor must be >= FLT_MIN (1.18e-38)");
   if (d->f_mode != FKK_F_ONE && d->f_mode != FKK_F_EQ9) throw Status(FKK_ERR_INVALID_ARG, "bad f_mode");
   if (!(d->als_lambda > 0) || !(d->als_p > 0 && d->als_p < 0.5) || d->als_iters < 1)
     throw Status(FKK_ERR_INVALID_ARG, "ALS needs lambda > 0, 0 < p < 0.5, iters >= 1");

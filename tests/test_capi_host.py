@@ -36,6 +36,9 @@ def test_plan_create_rejects_bad_desc_without_gpu():
     with pytest.raises(fkk.FkkError) as e:
         fkk.Plan(n_freq=64, rank_k=100, max_rows=10)      # k > M
     assert e.value.name == "FKK_ERR_INVALID_ARG"
+    with pytest.raises(fkk.FkkError) as e:
+        fkk.Plan(n_freq=64, rank_k=4, max_rows=10, ratio_floor=1e-40)   # below FLT_MIN (fp32 log clamp)
+    assert e.value.name == "FKK_ERR_INVALID_ARG"
 
 
 @pytest.mark.parametrize("M,k", [(40, 7), (256, 30), (512, 12)])
