@@ -223,6 +223,25 @@ def test_gram_tc_equals_simt_in_fp32_accuracy(torch_cuda, fkk, cfg2):
         assert np.max(np.abs(G[g] - G_or)) / np.max(np.abs(G_or)) <= 2e-6, g
 
 
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_image_gram_variants(torch_cuda, fkk, cfg2, mode, monkeypatch):
+    """Both pre-split-image Gram kernels (0: 1-CTA 128x128 tiles, 1: CTA pairs 256x256, the default at
+    M = 1000) against the fp64 oracle Gram, at a pixel count that leaves ragged stages and splits."""
+    monkeypatch.setenv("FKK_GRAM_MODE", mode)
+    I, Iref = cfg2
+    I = I[:30001]
+    plan = fkk.Plan(1000, 40, I.shape[0])
+    plan.svd(_dev(torch_cuda, I), _dev(torch_cuda, Iref))
+    G_or = O.gram(O.log_ratio(I, Iref, O.Params()))
+    assert np.max(np.abs(plan.stage("G") - G_or)) / np.max(np.abs(G_or)) <= 2e-6
+
+
+def test_factorized_odd_channel_blocks(torch_cuda, fkk, cfg2):
+    """M = 640 (five 128-channel blocks: the 1-CTA image Gram is the default there) end to end."""
+    I, Iref = cfg2
+    _factorized_check(torch_cuda, fkk, np.ascontiguousarray(I[:20000, :640]), np.ascontiguousarray(Iref[:640]), 40)
+
+
 # ------------------------------------------------------- conventional workflow (NEXT 2) ----------
 @pytest.mark.parametrize("k_keep", [6, 12])
 def test_conventional_svd_denoise_cfg1(torch_cuda, fkk, cfg1, k_keep):
