@@ -704,7 +704,10 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   constexpr int NCH = 2;
   const int NPT = blockDim.x * NCH;   // points per round over the whole CTA
   for (int round = 0; round < 64; ++round) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    // absolute tolerance 2 eps ||T|| (LAPACK dstebz's default abstol scale): inverse iteration needs
+    // lambda to O(eps ||T||), and every consumer compares eigenvalues normwise (sigma_i against
+    // sigma_1); a relative-to-lambda stop spent ~3 extra rounds on the plateau eigenvalues
+    if (hi - lo <= 2.0 * eps * tn + pivmin) break;
     const double w = (hi - lo) / (double)(NPT + 1);
     double x[NCH], p1[NCH], p2[NCH];
     int cnt[NCH];
