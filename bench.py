@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one gram_tc launch (profiles/)
-GRAM_TRAFFIC = {"cfg3": 7.30e9}   # ncu --set full, gram_pre2_kernel at cfg3: dram read 6.84 GB + write 0.46 GB
+GRAM_TRAFFIC = {"cfg3": 6.95e9}   # ncu --set full, gram_pre2_kernel at cfg3: dram read 6.71 GB + write 0.24 GB
 
 METRIC = "spectra/s for full fKK-EC (and direct KK) at 1/2/4/8 B200; % HBM/TC roofline"
 
