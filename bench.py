@@ -30,8 +30,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one gram_tc launch (profiles/)
-GRAM_TRAFFIC = {"cfg3": 6.95e9}   # ncu --set full, gram_pre2_kernel at cfg3: dram read 6.71 GB + write 0.24 GB
+# ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernels, extracted
+# from a committed capture by tools/ncu_traffic.py (profiles/*_traffic.json); labelled with its source
+def _traffic():
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return {}, None
+    try:
+        return json.load(open(files[-1])), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return {}, None
+
 
 METRIC = "spectra/s for full fKK-EC (and direct KK) at 1/2/4/8 B200; % HBM/TC roofline"
 
@@ -165,27 +175,32 @@ def run_ours(args) -> dict:
 
     # roofline of the Gram (F2, tcgen05 3xTF32): algorithmic flops N*M^2 (the syrk: M(M+1)/2 unique
     # products x 2 flops, rounded to M^2) per pass; 3xTF32 issues three TF32 products per fp32-equivalent
-    # product, so its fp32-equivalent peak is the TF32 peak / 3
+    # product, so its fp32-equivalent peak is the TF32 peak / 3.  The denominator is
+    # the BURST bf16 figure (scaled by the guide's nominal TF32/BF16 ratio) unless this run's clock record
+    # shows the power cap, in which case it is the sustained one (B200_PROFILING.md).
     peaks, src = _peaks()
+    clocks = clk.summary()
+    capped = "sw_power_cap" in clocks.get("reasons", [])
+    traffic, traffic_src = _traffic()
     gram_ms = stage_ms.get("gram", float("nan"))
     gram_flops = float(n_loc) * M * M
-    # the Gram runs inside a long step (the tensor load lowers the SM clock: ncu saw 1.66 GHz during it),
-    # so its peak is the SUSTAINED bf16 figure (B200_PROFILING.md); the burst fraction is kept beside it
-    bf16_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    peak_3x = bf16_sus * (1.1 / 2.25) / 3.0                     # guide's nominal TF32/BF16 ratio, 3 products
-    peak_3x_burst = peaks["bf16_tflops"] * (1.1 / 2.25) / 3.0
+    bf16 = peaks["bf16_tflops_sustained"] if capped else peaks["bf16_tflops"]
+    peak_3x = bf16 * (1.1 / 2.25) / 3.0
     achieved = gram_flops / (gram_ms / 1e3) / 1e12
     pair = ((M + 127) // 128) % 2 == 0
-    roofline = {"kernel": ("gram_pre2 (F2, tcgen05.mma cta_group::2 kind::tf32 256x256 tiles" if pair else
-                           "gram_pre (F2, tcgen05.mma kind::tf32 128x128 tiles") + ", 3xTF32 from the pre-split A0 image)",
-                "bound": "tensor", "achieved": achieved,
-                "peak": peak_3x, "unit": "TFLOP/s", "frac": achieved / peak_3x,
-                "traffic": GRAM_TRAFFIC.get(args.workload) if pair else None,
-                "peak_burst": peak_3x_burst, "frac_burst": achieved / peak_3x_burst,
-                "peak_source": f"{src} sustained bf16 {bf16_sus:.0f} TF/s x 1.1/2.25 (TF32) / 3 (3xTF32 products) "
-                               f"(burst {peaks['bf16_tflops']:.0f}); algorithmic flops = N*M^2 per pass; timed with CUDA "
-                               f"events on the plan stream (the Gram kernel + its fp64 split reduction)"}
-    # per-kernel-class rooflines of the other hot kernels (same event timing)
+    gname = "gram_pre2" if pair else "gram_pre"
+    tr = traffic.get(args.workload, {}).get(gname)
+    roofline = {"kernel": (f"{gname} (F2, tcgen05.mma {'cta_group::2 ' if pair else ''}kind::tf32 "
+                           f"{'256x256' if pair else '128x128'} tiles, 3xTF32 from the pre-split A0 image)"),
+                "bound": "tensor", "achieved": achieved, "peak": peak_3x, "unit": "TFLOP/s", "frac": achieved / peak_3x,
+                "traffic": tr,
+                "traffic_source": (f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch, {traffic_src}"
+                                   if tr else "not captured for this workload"),
+                "peak_source": (f"{src} {'sustained' if capped else 'burst'} bf16 {bf16:.0f} TF/s x 1.1/2.25 (nominal "
+                                f"TF32/BF16) / 3 (3xTF32 products); {'sw_power_cap seen' if capped else 'no power cap seen'} "
+                                f"during the timed region; algorithmic flops = N*M^2 per pass; CUDA events on the plan "
+                                f"stream (the Gram kernel + its fp64 split reduction)")}
+    # per-kernel rooflines of the other hot kernels (same event timing)
     hbm = peaks["hbm_gbs"]
     other = {}
     # logratio_pre reads the cube and writes the tf32 hi/lo MMA image of A0 for the Gram (128-channel
@@ -197,22 +212,51 @@ def run_ours(args) -> dict:
         ms = stage_ms.get(name)
         if ms:
             gbs = nbytes / (ms / 1e3) / 1e9
-            other[name] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm}
+            other[name] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                           "bytes_per_pass": nbytes}
     roofline["others"] = other
 
     # ---------------- direct KK (same image) ----------------
     plan.direct(I, Iref, out)
+    plan.als_solves()
     _barrier(world)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     nd = max(1, min(args.steps, 3))
+    dstage: dict = {}
     e0.record(stream)
     for _ in range(nd):
         plan.direct(I, Iref, out)
+        for kk, v in plan.stage_times().items():
+            dstage[kk] = dstage.get(kk, 0.0) + v / nd
     e1.record(stream)
     _barrier(world)
     td = _max_over_ranks(e0.elapsed_time(e1) / nd, world)
-    direct_stage = plan.stage_times()
+    solves = plan.als_solves() / (nd * n_loc)
+    # rooflines of the direct path: ALS against the FP64 pipe (algorithmic flops
+    # = 25 M per solve: the serial pentadiagonal LDL^T + forward + back substitution, times the solves
+    # actually needed); the two Hilbert kernels against FP32 (5 L log2 L flops per complex transform,
+    # two transforms per spectrum pair and Hilbert) and HBM (bytes they must move)
+    fp64_peak = 37.2e12    # measured DFMA throughput (tools/micro/lat.cu): 148 SM x 64 x 2 x 1.965 GHz
+    fp32_peak = 148 * 128 * 2 * 1.965e9
+    L = 2 * (1 << (M - 1).bit_length())
+    hil_fl = 5.0 * L * np.log2(L)              # per spectrum (two-for-one) and Hilbert round trip
+    dr = {}
+    if dstage.get("als"):
+        fl = 25.0 * M * solves * n_loc
+        a = fl / (dstage["als"] / 1e3)
+        dr["als"] = {"bound": "fp64", "achieved": a / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                     "frac": a / fp64_peak, "solves_per_spectrum": solves,
+                     "flops_per_spectrum": 25.0 * M * solves}
+    for nm, fl_s, by_s in (("kk_phase", hil_fl, 8.0 * M), ("pec_sec", hil_fl + 40.0 * M, 20.0 * M)):
+        ms = dstage.get(nm)
+        if ms:
+            a_fl = fl_s * n_loc / (ms / 1e3)
+            a_by = by_s * n_loc / (ms / 1e3)
+            dr[nm] = {"bound": "fp32 (FFT)", "achieved": a_fl / 1e12, "peak": fp32_peak / 1e12, "unit": "TFLOP/s",
+                      "frac": a_fl / fp32_peak, "hbm_gbs": a_by / 1e9, "hbm_frac": a_by / (hbm * 1e9)}
+    direct_kk = {"value": N / (td / 1e3), "unit": "spectra/s", "ms_per_pass": td, "stage_ms": dstage,
+                 "als_solves_per_spectrum": solves, "roofline": dr}
 
     # ---------------- conventional workflow (Fig. 1(a): SVD denoise of the raw cube + direct KK) ----------
     conv = None
@@ -240,7 +284,7 @@ def run_ours(args) -> dict:
         Ia_h, _, _ = generate_rows(ap, a0, a1)
         Ia = torch.from_numpy(Ia_h).cuda()
         batch = 50000
-        papply = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local)
+        papply = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local, timing=True)
         oa = torch.empty((batch, ap.n_freq), dtype=torch.complex64, device="cuda")
         for b0 in range(0, min(a1 - a0, batch), batch):
             papply.apply(basis, Ia[b0:b0 + batch], oa[: min(batch, a1 - a0 - b0)])
@@ -254,8 +298,13 @@ def run_ours(args) -> dict:
         e1.record(stream)
         _barrier(world)
         tm = _max_over_ranks(e0.elapsed_time(e1), world)
+        nbytes = 12.0 * (a1 - a0) * ap.n_freq           # read the cube (4 B) + write complex64 K (8 B) per element
+        gbs = nbytes / (tm / 1e3) / 1e9
         ml = {"value": ap.n_pixels / (tm / 1e3), "unit": "spectra/s", "ms_per_pass": tm,
-              "batches": nb, "ms_per_batch": tm / max(nb, 1), "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches"}
+              "batches": nb, "ms_per_batch": tm / max(nb, 1), "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches",
+              "stage_ms_last_batch": papply.stage_times(),
+              "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                           "bytes_per_pass": nbytes}}
         del Ia, papply
 
     # ---------------- end to end through the host-buffer C-ABI ----------------
@@ -283,32 +332,38 @@ def run_ours(args) -> dict:
         "config": {"workload": f"{args.workload}: fKK-EC transform of {N:,} x {M} (k={k}), fp32 cube, complex64 out",
                    "n_spectra": N, "n_freq": M, "rank_k": k, "parallelism": f"pixel shards x{world}",
                    "l2": "inputs larger than L2 (cube 2.81 GB, output 5.62 GB)"},
-        "roofline": roofline, "stage_ms": stage_ms, "clocks": clk.summary(),
+        "roofline": roofline, "stage_ms": stage_ms, "clocks": clocks,
         "gpu_launches": int(launches),
-        "direct_kk": {"value": N / (td / 1e3), "unit": "spectra/s", "ms_per_pass": td, "stage_ms": direct_stage},
+        "direct_kk": direct_kk,
         "ml_apply": ml, "e2e": e2e, "conventional": conv,
     }
     return res
 
 
-def cpu_baseline(args, kind="oracle") -> dict:
-    """The fp64 oracle as it stands, on the host cores, on a bounded sample of the same workload."""
+def cpu_baseline(args, kind="oracle", repeats: int = 3) -> dict:
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample of the same workload:
+    mean +- std of `repeats` runs (the paper's protocol)."""
     from oracle import fkk_oracle as O
     from synth import CONFIGS, generate_rows
     cfg = CONFIGS[args.workload]
     n_s = args.cpu_sample
     I, Iref, _ = generate_rows(cfg, 0, n_s)
-    t0 = time.perf_counter()
-    O.fkk_ec(I, Iref, cfg.rank_k, O.Params())
-    dt = time.perf_counter() - t0
+    ts = []
+    for _ in range(max(1, repeats)):
+        t0 = time.perf_counter()
+        O.fkk_ec(I, Iref, cfg.rank_k, O.Params())
+        ts.append(time.perf_counter() - t0)
+    dt = statistics.mean(ts)
     nd = args.cpu_direct_sample
     t1 = time.perf_counter()
     O.kk_direct(I[:nd], Iref, O.Params())
     dd = time.perf_counter() - t1
     cores = len(os.sched_getaffinity(0))
     return {"value": n_s / dt, "unit": "spectra/s", "cores": cores, "kind": kind,
-            "sample": f"fKK-EC oracle (fp64 NumPy, BLAS threads = {cores}) on the first {n_s:,} spectra of {args.workload} "
-                      f"({dt:.1f} s); direct-KK oracle on {nd:,} spectra: {nd / dd:.1f} spectra/s",
+            "std": statistics.stdev([n_s / t for t in ts]) if len(ts) > 1 else 0.0, "repeats": len(ts),
+            "sample": f"fKK-EC oracle (fp64 NumPy, BLAS threads = {cores}) on the first {n_s:,} spectra of {args.workload}, "
+                      f"mean of {len(ts)} runs ({dt:.1f} s each; the fixed eig/basis cost is amortised over the sample only); "
+                      f"direct-KK oracle on {nd:,} spectra: {nd / dd:.1f} spectra/s",
             "direct_kk_value": nd / dd}
 
 
@@ -321,7 +376,7 @@ def run_reference(args) -> dict:
     for _ in range(args.warmup if args.warmup < 1 else 1):
         pass
     for _ in range(max(1, args.steps)):
-        cb = cpu_baseline(args, kind="oracle")
+        cb = cpu_baseline(args, kind="oracle", repeats=1)
         vals.append(cb["value"])
     v = statistics.median(vals)
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "spectra/s", "n_gpus": world,

@@ -152,6 +152,14 @@ fkk_status fkk_apply_trained_basis_host(fkk_plan_t p, fkk_basis_t b, const void*
                                         int64_t n_rows, void* h_out);
 fkk_status kk_direct_batch_host(fkk_plan_t p, const void* h_icars, int64_t n_rows,
                                 const void* h_iref, void* h_out);
+/* ML:fKK-EC apply of a host-resident cube streamed in batches
+ * of `batch` spectra (<= max_rows): per batch a host->device copy, the apply (as
+ * fkk_apply_trained_basis) and a device->host copy, pipelined over three streams with two device
+ * buffer pairs (allocated on the first call and kept by the plan).  h_icars / h_out should be pinned
+ * (cudaHostAlloc) for the copies to overlap.  h_batch_ms (nullable, ceil(n_rows / batch) floats):
+ * each batch's end-to-end latency (H2D start to D2H end, CUDA events).  Synchronises before returning. */
+fkk_status fkk_apply_trained_basis_stream(fkk_plan_t p, fkk_basis_t b, const void* h_icars, int64_t n_rows,
+                                          int64_t batch, void* h_out, float* h_batch_ms);
 
 fkk_status fkk_basis_destroy(fkk_basis_t b);
 /* Basis metadata: M, k, L.  Any pointer may be NULL. */
@@ -182,6 +190,10 @@ fkk_status fkk_enable_timing(fkk_plan_t p, int32_t on);
 int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap);
 /* Number of kernel launches issued by the last call (the bench reports it). */
 int64_t fkk_last_launch_count(fkk_plan_t p);
+/* Diagnostic: ALS solves summed over the spectra of the direct-path calls since the last query
+ * (the ALS stops once a solve changes no weight, PAPER.md:45 / reading A6; iters per spectrum =
+ * this / spectra).  Synchronises the plan stream and resets the counter; -1 on a CUDA error. */
+int64_t fkk_debug_als_solves(fkk_plan_t p);
 
 /* Test hook (tensor-core plumbing self-test): one tcgen05.mma kind::tf32 of A (128 x 8, row-major
  * fp32, device) times B^T (B: N x 8, N in {16, 32, ..., 256}) into D (128 x N fp32, device) with the

@@ -115,6 +115,7 @@ struct fkk_plan {
   float* inv_ref = nullptr;
   double* ref64 = nullptr;
   float2* tw32 = nullptr;
+  int* pmap = nullptr;
   double2* tw64 = nullptr;
   float* A = nullptr;
   double* gram_part = nullptr;
@@ -133,7 +134,7 @@ struct fkk_plan {
   int64_t* q_dev = nullptr;
   double *X = nullptr, *Vt_f = nullptr, *Hv = nullptr, *P = nullptr, *Phi_err = nullptr, *XtX = nullptr,
          *XtPhi = nullptr, *Phi_pec = nullptr, *HPhi = nullptr, *tmp = nullptr, *Vsec = nullptr, *ridge_work = nullptr,
-         *lam = nullptr, *basis_als_state = nullptr;
+         *lam = nullptr;
   float* Bi = nullptr;
   float* bimg = nullptr;
   float* wimg = nullptr;
@@ -154,13 +155,17 @@ struct fkk_plan {
   // direct path (lazy)
   int64_t direct_batch = 0;
   float *phi = nullptr, *phierr = nullptr;
-  double* als_state = nullptr;
+  int* als_solves = nullptr;   // ALS solves summed over the spectra of the direct calls (diagnostic)
   // host-buffer variants (lazy)
   void* d_in_cube = nullptr;
   size_t d_in_cube_bytes = 0;
   void* d_out_cube = nullptr;
   size_t d_out_cube_bytes = 0;
   void* d_ref_buf = nullptr;
+  // streamed ML apply (lazy): two input and two output batch buffers, copy-in / copy-out streams
+  void* stream_bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t stream_in_bytes = 0, stream_out_bytes = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
   // last-call host state
   std::vector<double> h_s;
   std::vector<int64_t> h_q;
@@ -175,12 +180,15 @@ struct fkk_plan {
 
   ~fkk_plan() {
     if (stream) cudaStreamSynchronize(stream);
-    void* ptrs[] = {flags, inv_ref, ref64, tw32, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
+    void* ptrs[] = {flags, inv_ref, ref64, tw32, pmap, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, basis_als_state, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_state, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
+    for (void* b : stream_bufs) if (b) cudaFree(b);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     for (auto& m : marks) cudaEventDestroy(m.second);
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -216,8 +224,13 @@ struct fkk_plan {
     }
   }
 
-  // deferred device errors: reads the pinned flag word after the stream drained
-  void check_flags_sync() {
+  // deferred device errors: reads the pinned flag word after the stream drained.  In the collective
+  // calls (`collective`, every rank at the same point) the word is first max-reduced over the ranks, so
+  // a non-finite value in one rank's shard makes EVERY rank throw the same error instead of leaving
+  // the others blocked in the next collective.
+  void check_flags_sync(bool collective = false);
+  void check_flags_sync_impl(bool collective) {
+    if (collective && comm) nccl_allreduce_flags();
     FKK_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, stream));
     FKK_CUDA_CHECK(cudaStreamSynchronize(stream));
     const int f = *h_flags;
@@ -230,15 +243,23 @@ struct fkk_plan {
     }
   }
 
+  void nccl_allreduce_flags();
+
   void ensure_direct() {
     if (phi) return;
     direct_batch = std::min<int64_t>(std::max<int64_t>(d.max_rows, 2), 131072);
     direct_batch = ((direct_batch + 31) / 32) * 32;
     phi = dalloc<float>((size_t)direct_batch * M);
     phierr = dalloc<float>((size_t)direct_batch * M);
-    als_state = dalloc<double>((size_t)3 * M * direct_batch);
+    als_solves = dalloc<int>(1);
+    FKK_CUDA_CHECK(cudaMemset(als_solves, 0, sizeof(int)));
   }
 };
+
+void fkk_plan::nccl_allreduce_flags() {
+  nccl_check(g_nccl.AllReduce(flags, flags, 1, ncclInt32, ncclMax, comm, stream), "AllReduce(flags)");
+}
+void fkk_plan::check_flags_sync(bool collective) { check_flags_sync_impl(collective); }
 
 namespace {
 
@@ -294,19 +315,35 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->inv_ref = dalloc<float>((size_t)(M + 31) / 32 * 32);   // zero tail: the raw-cube projection reads 32-channel stages
   FKK_CUDA_CHECK(cudaMemset(p->inv_ref, 0, (size_t)(M + 31) / 32 * 32 * sizeof(float)));
   p->ref64 = dalloc<double>(M);
-  // twiddles exp(-2 pi i j / L), fp64 on the host
+  // twiddles exp(-2 pi i j / L), fp64 on the host (fp32 copy: full period for the direct path's
+  // radix-16 passes; fp64: half period for the basis transforms) and the padding map of the direct
+  // path (source channel of each padded sample; reading A3)
   {
-    std::vector<float2> t32(p->L / 2);
+    std::vector<float2> t32(p->L);
     std::vector<double2> t64(p->L / 2);
-    for (int j = 0; j < p->L / 2; ++j) {
+    for (int j = 0; j < p->L; ++j) {
       const double a = -2.0 * M_PI * (double)j / (double)p->L;
-      t64[j] = make_double2(std::cos(a), std::sin(a));
       t32[j] = make_float2((float)std::cos(a), (float)std::sin(a));
+      if (j < p->L / 2) t64[j] = make_double2(std::cos(a), std::sin(a));
     }
-    p->tw32 = dalloc<float2>(p->L / 2);
+    p->tw32 = dalloc<float2>(p->L);
     p->tw64 = dalloc<double2>(p->L / 2);
     FKK_CUDA_CHECK(cudaMemcpy(p->tw32, t32.data(), t32.size() * sizeof(float2), cudaMemcpyHostToDevice));
     FKK_CUDA_CHECK(cudaMemcpy(p->tw64, t64.data(), t64.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    std::vector<int> pm(p->L);
+    const int pl = (p->L - M) / 2, period = 2 * (M - 1);
+    for (int i = 0; i < p->L; ++i) {
+      const int t = i - pl;
+      if (t >= 0 && t < M) pm[i] = t;
+      else if (p->pad_zero) pm[i] = -1;
+      else {   // even reflection without repeating the edge sample, period 2(M-1) (numpy 'reflect')
+        int r = t % period;
+        if (r < 0) r += period;
+        pm[i] = r < M ? r : period - r;
+      }
+    }
+    p->pmap = dalloc<int>(p->L);
+    FKK_CUDA_CHECK(cudaMemcpy(p->pmap, pm.data(), pm.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
   p->A = dalloc<float>((size_t)n * M);
   if (d->gemm_impl == FKK_GEMM_3XTF32) {
@@ -364,7 +401,6 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->Vsec = dalloc<double>((size_t)k * M);
   p->ridge_work = dalloc<double>((size_t)3 * k * k);
   p->lam = dalloc<double>(1);
-  p->basis_als_state = dalloc<double>((size_t)3 * M * (((nqc + 31) / 32) * 32));
   p->Bi = dalloc<float>((size_t)k * M * 2);
   p->bimg = dalloc<float>(fkk::reconstruct_tc_bimg_floats(k, M));
   p->wimg = dalloc<float>(fkk::project_tc_wimg_floats(M, kp));
@@ -475,7 +511,7 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   fkk::launch_eig_topk(p->G, M, k, p->eig_work, p->V64, p->lam_d, p->flags, s);
   std::vector<double> hl(k);
   FKK_CUDA_CHECK(cudaMemcpyAsync(hl.data(), p->lam_d, k * sizeof(double), cudaMemcpyDeviceToHost, s));
-  p->check_flags_sync();
+  p->check_flags_sync(true);
   p->h_s.assign(k, 0.0);
   for (int i = 0; i < k; ++i) {
     if (!std::isfinite(hl[i])) throw Status(FKK_ERR_NUMERICAL, "eigensolver produced a non-finite eigenvalue");
@@ -571,8 +607,7 @@ void transform_rest(fkk_plan* p, const void* cube, int64_t n_rows, int64_t row0,
   fkk::launch_vt_over_f(p->V64, p->f64, M, k, p->Vt_f, s);
   fkk::launch_hilbert_rows_f64(p->Vt_f, k, M, M, p->Hv, p->L, p->pad_zero, p->tw64, s);          // Eq. 11
   fkk::launch_dgemm_small(nq, M, k, p->X, k, 0, p->Hv, M, 0, p->P, M, 0.0, s);                    // Eq. 16 argument
-  fkk::launch_als_rows(p->P, 1, nq, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->basis_als_state,
-                       p->Phi_err, 1, s);                                                         // D{.}
+  fkk::launch_als_rows(p->P, 1, nq, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->Phi_err, 1, s);                                                         // D{.}
   fkk::launch_dgemm_small(k, k, nq, p->X, k, 1, p->X, k, 0, p->XtX, k, 0.0, s);                   // X^T X
   fkk::launch_dgemm_small(k, M, nq, p->X, k, 1, p->Phi_err, M, 0, p->XtPhi, M, 0.0, s);           // X^T Phi_err
   fkk::launch_ridge(p->XtX, k, p->XtPhi, M, p->d.ridge_rel, p->Phi_pec, p->lam, p->ridge_work, p->flags, s);  // Eq. 17
@@ -656,7 +691,7 @@ fkk_status guarded(fkk_plan* p, F&& f) {
 void direct_run(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_iref, void* d_out) {
   cudaStream_t s = p->stream;
   const int M = p->M;
-  if (fkk::direct_finish_smem(M, p->L) > 227 * 1024) throw Status(FKK_ERR_NOT_IMPLEMENTED, "direct path: M/L too large for one CTA");
+  if (p->L > 4096) throw Status(FKK_ERR_NOT_IMPLEMENTED, "direct path: FFT length above 4096 (M <= 2048)");
   p->ensure_direct();
   fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
   const size_t oel = p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8;
@@ -664,13 +699,13 @@ void direct_run(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_
     const int64_t nb = std::min<int64_t>(p->direct_batch, n_rows - b0);
     const char* in = static_cast<const char*>(d_icars) + (size_t)b0 * M * p->in_elem;
     char* out = static_cast<char*>(d_out) + (size_t)b0 * M * oel;
-    fkk::launch_direct_phase(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->pad_zero,
-                             p->tw32, p->phi, p->flags, s);
+    fkk::launch_direct_phase(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->tw32,
+                             p->pmap, p->phi, p->flags, s);
     p->mark("kk_phase");
-    fkk::launch_als_rows(p->phi, 0, nb, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->als_state, p->phierr, 0, s);
+    fkk::launch_als_rows(p->phi, 0, nb, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->phierr, 0, s, p->als_solves);
     p->mark("als");
-    fkk::launch_direct_finish(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->pad_zero,
-                              p->tw32, p->phi, p->phierr, p->sg_half, out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
+    fkk::launch_direct_finish(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->tw32,
+                              p->pmap, p->phi, p->phierr, p->sg_half, out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
     p->mark("pec_sec");
   }
 }
@@ -680,14 +715,24 @@ void apply_run(fkk_plan* p, fkk_basis* b, const void* d_icars, int64_t n_rows, v
     throw Status(FKK_ERR_INCOMPATIBLE_BASIS, "trained basis M/L/pad/k incompatible with the plan");
   cudaStream_t s = p->stream;
   const int M = p->M;
-  fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, b->inv_ref, b->ref64, (float)b->ratio_floor, p->A, p->flags, s);
-  p->mark("logratio");
-  if (p->d.gemm_impl == FKK_GEMM_3XTF32)
-    fkk::launch_project_tc(p->A, n_rows, M, b->wimg, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, 0, s);
-  else
-    fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
-  p->mark("project");
-  if (p->d.gemm_impl == FKK_GEMM_3XTF32) {
+  const bool tcg = p->d.gemm_impl == FKK_GEMM_3XTF32;
+  if (tcg && !p->in_f64 && fkk::project_raw_ok(M, b->kp)) {
+    // F12 as two streaming kernels: the projection forms A0 = 1/2 ln(max(I/I_ref, floor)) from the raw
+    // cube in its converter warps (no A0 round trip through HBM), US_new = A0 W (W = D_f V diag(s^2 /
+    // (s^2 + lam_ml)), Eq. 25), then the reconstruction with the trained B (Eq. 23)
+    fkk::launch_project_tc(static_cast<const float*>(d_icars), n_rows, M, b->wimg, b->k, b->kp, p->US, p->ext_val,
+                           p->ext_idx, 0, 0, s, b->inv_ref, (float)b->ratio_floor);
+    p->mark("project");
+  } else {
+    fkk::launch_logratio(d_icars, p->in_f64, n_rows, M, b->inv_ref, b->ref64, (float)b->ratio_floor, p->A, p->flags, s);
+    p->mark("logratio");
+    if (tcg)
+      fkk::launch_project_tc(p->A, n_rows, M, b->wimg, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, 0, s);
+    else
+      fkk::launch_project_simt(p->A, n_rows, M, b->W, b->k, b->kp, p->US, p->ext_val, p->ext_idx, 0, s);
+    p->mark("project");
+  }
+  if (tcg) {
     if (!b->bimg_valid) { fkk::launch_build_bimg(b->Bi, b->k, M, b->bimg, s); b->bimg_valid = true; }
     fkk::launch_reconstruct_tc(p->US, n_rows, b->k, b->kp, b->bimg, M, d_out, p->d.out_layout == FKK_OUT_IMAG_F32, s);
   } else {
@@ -825,7 +870,7 @@ fkk_status fkk_transform(fkk_plan_t p, const void* d_icars, int64_t n_rows, cons
     p->last_global_rows = ng;
     svd_stage(p, d_icars, n_rows, d_iref, ng);
     transform_rest(p, d_icars, n_rows, row0, nullptr, 0, d_out);
-    p->check_flags_sync();
+    p->check_flags_sync(true);
     if (basis_out) *basis_out = export_basis(p);
     p->end_call();
   });
@@ -861,7 +906,7 @@ fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows,
     FKK_CUDA_CHECK(cudaStreamSynchronize(s));
     p->h_s.assign(h_s, h_s + k);
     transform_rest(p, d_icars, n_rows, row0, h_q, nq, d_out);
-    p->check_flags_sync();
+    p->check_flags_sync(true);
     p->end_call();
   });
 }
@@ -979,6 +1024,73 @@ fkk_status fkk_apply_trained_basis_host(fkk_plan_t p, fkk_basis_t b, const void*
   });
 }
 
+// ML apply of a host-resident cube streamed in batches: batch i's host->device copy,
+// apply (projection + reconstruction on the plan stream) and device->host copy run on three streams
+// with two device buffer pairs, so the copies of neighbouring batches overlap the compute.
+// h_batch_ms (nullable): per-batch end-to-end latency, first H2D start to last D2H end.
+fkk_status fkk_apply_trained_basis_stream(fkk_plan_t p, fkk_basis_t b, const void* h_icars, int64_t n_rows,
+                                          int64_t batch, void* h_out, float* h_batch_ms) {
+  return guarded(p, [&] {
+    if (!b || !h_icars || !h_out) throw Status(FKK_ERR_INVALID_ARG, "NULL argument");
+    if (batch < 1 || batch > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "batch must be in [1, max_rows]");
+    if (n_rows < 0) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be >= 0");
+    const int M = p->M;
+    const size_t oel = p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8;
+    const size_t in_b = (size_t)batch * M * p->in_elem, out_b = (size_t)batch * M * oel;
+    if (!p->stream_bufs[0]) {
+      for (int i = 0; i < 2; ++i) {
+        p->stream_bufs[i] = dalloc<char>(in_b);
+        p->stream_bufs[2 + i] = dalloc<char>(out_b);
+      }
+      p->stream_in_bytes = in_b;
+      p->stream_out_bytes = out_b;
+      FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+      FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    }
+    if (p->stream_in_bytes < in_b || p->stream_out_bytes < out_b)
+      throw Status(FKK_ERR_INVALID_ARG, "batch larger than the first streaming call's batch");
+    p->begin_call();
+    const int64_t nb = (n_rows + batch - 1) / batch;
+    std::vector<cudaEvent_t> ev(4 * std::max<int64_t>(nb, 1));
+    for (auto& e : ev) FKK_CUDA_CHECK(cudaEventCreate(&e));
+    // ev[4i]: H2D start, ev[4i+1]: H2D done, ev[4i+2]: apply done, ev[4i+3]: D2H done
+    try {
+      for (int64_t i = 0; i < nb; ++i) {
+        const int64_t r0 = i * batch, rows = std::min(batch, n_rows - r0);
+        const int slot = (int)(i & 1);
+        if (i >= 2) {   // the slot's previous batch: its apply read the input, its D2H read the output
+          FKK_CUDA_CHECK(cudaStreamWaitEvent(p->s_in, ev[4 * (i - 2) + 2], 0));
+        }
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i], p->s_in));
+        FKK_CUDA_CHECK(cudaMemcpyAsync(p->stream_bufs[slot], static_cast<const char*>(h_icars) + (size_t)r0 * M * p->in_elem,
+                                       (size_t)rows * M * p->in_elem, cudaMemcpyHostToDevice, p->s_in));
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 1], p->s_in));
+        FKK_CUDA_CHECK(cudaStreamWaitEvent(p->stream, ev[4 * i + 1], 0));
+        if (i >= 2) FKK_CUDA_CHECK(cudaStreamWaitEvent(p->stream, ev[4 * (i - 2) + 3], 0));
+        apply_run(p, b, p->stream_bufs[slot], rows, p->stream_bufs[2 + slot]);
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 2], p->stream));
+        FKK_CUDA_CHECK(cudaStreamWaitEvent(p->s_out, ev[4 * i + 2], 0));
+        FKK_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(h_out) + (size_t)r0 * M * oel, p->stream_bufs[2 + slot],
+                                       (size_t)rows * M * oel, cudaMemcpyDeviceToHost, p->s_out));
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 3], p->s_out));
+      }
+      FKK_CUDA_CHECK(cudaStreamSynchronize(p->s_out));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+      if (h_batch_ms)
+        for (int64_t i = 0; i < nb; ++i) FKK_CUDA_CHECK(cudaEventElapsedTime(h_batch_ms + i, ev[4 * i], ev[4 * i + 3]));
+    } catch (...) {
+      cudaStreamSynchronize(p->s_in);
+      cudaStreamSynchronize(p->s_out);
+      cudaStreamSynchronize(p->stream);
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    p->check_flags_sync();
+    p->end_call();
+  });
+}
+
 fkk_status fkk_basis_destroy(fkk_basis_t b) {
   delete b;
   return FKK_OK;
@@ -1060,6 +1172,15 @@ int32_t fkk_stage_times(fkk_plan_t p, const char** names, float* ms, int32_t cap
 }
 
 int64_t fkk_last_launch_count(fkk_plan_t p) { return p ? p->launches : 0; }
+
+int64_t fkk_debug_als_solves(fkk_plan_t p) {
+  if (!p || !p->als_solves) return 0;
+  int v = 0;
+  if (cudaStreamSynchronize(p->stream) != cudaSuccess) return -1;
+  if (cudaMemcpy(&v, p->als_solves, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  cudaMemset(p->als_solves, 0, sizeof(int));
+  return v;
+}
 
 fkk_status fkk_debug_tc_mma(int32_t mode, const float* d_A, const float* d_B, float* d_D, int32_t N) {
   if (!d_A || !d_B || !d_D || N < 16 || N > 256 || N % 16) return FKK_ERR_INVALID_ARG;

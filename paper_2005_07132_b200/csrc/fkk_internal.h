@@ -53,19 +53,21 @@ void launch_extremes_reduce(const float* ext_val, const int64_t* ext_idx, int nb
 void launch_add_f64(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
 
 // ---- direct path (k_direct.cu)
+// tw: exp(-2 pi i t / L) for t < L (fp32 from fp64); pmap: L padding-map entries (source channel
+// of padded sample i, -1 for a zero pad; reading A3)
 void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
-                         float floor, int L, int pad_zero, const float2* tw, float* phi, int* flags, cudaStream_t s);
+                         float floor, int L, const float2* tw, const int* pmap, float* phi, int* flags, cudaStream_t s);
 // ALS on rows of y (fp32 or fp64, row-major n x M) -> z (fp32 or fp64); state: 3*M*nb doubles, nb = 32*ceil(n/32)
-void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, double* state,
-                     void* z, int z_f64, cudaStream_t s);
+void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
+                     cudaStream_t s, int* solves = nullptr);
 void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
-                          float floor, int L, int pad_zero, const float2* tw, const float* phi, const float* phierr,
+                          float floor, int L, const float2* tw, const int* pmap, const float* phi, const float* phierr,
                           int sg_half, void* out, int out_imag_only, cudaStream_t s);
 size_t direct_finish_smem(int M, int L);
 // warp-partitioned fp64 ALS (k_als.cu), state in shared memory; false if M is out of its range
 size_t als_part_smem(int M, int y_f64);
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s);
+                     cudaStream_t s, int* solves = nullptr);
 
 // ---- factorized path
 // Gram partials (k_gram.cu): 128 x 128 tiles of the upper triangle, nsplit row segments each.

@@ -1,17 +1,22 @@
-// Asymmetric-least-squares baseline D{.} (reading A6/A7): exactly `iters` solves of
-// (W + lam D^T D) z = W y, w^0 = 1, then w_i = p if y_i > z_i else 1 - p -- all in fp64.
+// Asymmetric-least-squares baseline D{.} (readings A6/A7): `iters` solves of
+// (W + lam D^T D) z = W y, w^0 = 1, then w_i = p if y_i > z_i else 1 - p -- all in fp64.  The loop
+// stops early once a solve leaves every weight unchanged: the next system would be identical, so its
+// solution is the current one (the fp64 oracle always runs all `iters` solves).
 //
-// Warp-partitioned solver: ONE warp per spectrum, the M rows split into P <= 32 contiguous
-// segments (lane s owns rows [b_s, b_{s+1})).  The last two rows of every segment but the last are
-// separators; each lane eliminates the interior of its segment (LDL^T of a pentadiagonal block),
-// accumulating the Schur complement of its interior onto the two adjacent separators
-// (C = Y^T D^-1 Y with Y = L^-1 [A_IS, f_I]: forward substitution only, no back-substitution
-// needed).  The separators form a block-tridiagonal system with 2 x 2 blocks, solved by parallel
-// cyclic reduction across the lanes (5 shuffle rounds).  Pass B forward-substitutes the corrected
-// interior right-hand side; the next iteration's pass A back-substitutes it while it factorises the
-// next system in the opposite direction (the elimination direction alternates).  Per-row state
-// (l1, 1/D, g) lives in shared memory in a [row-in-segment][lane] layout (conflict-free), so the
-// 10 solves never touch HBM: the spectrum is read once and the baseline written once.
+// Warp-partitioned solver: ONE warp per spectrum, the M rows split into P <= 32 contiguous segments
+// (lane s owns rows [b_s, b_{s+1})).  The last two rows of every segment but the last are separators;
+// each lane eliminates the interior of its segment (LDL^T of a pentadiagonal block) while
+// forward-substituting the right-hand side and the two near spike columns, accumulating the Schur
+// complement C = Y^T D^-1 Y of its interior onto the adjacent separators.  The separators form a
+// block-tridiagonal system with 2 x 2 blocks, solved by parallel cyclic reduction across the lanes (5
+// shuffle rounds).  Pass B forward-substitutes the corrected interior right-hand side; the next
+// solve's pass A back-substitutes it while it factorises the next system in the opposite direction.
+//
+// On-chip layout (one warp = one spectrum, everything in shared memory or registers):
+//   row block t (t = row - b_s, the row inside the segment) = { l1[32], 1/D[32], g[32] (fp64),
+//   y[32] (input precision) }, lane s at column s: every access of a row is one base pointer plus
+//   compile-time field offsets, and consecutive rows are one fixed stride apart.
+//   weights: one bit per row in a per-lane register mask (bit t = 1 <-> w = p).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -25,6 +30,8 @@ namespace fkk {
 
 namespace {
 
+constexpr int NL = 32;   // lanes (segments) per spectrum
+
 __device__ __forceinline__ double rcp64a(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -33,9 +40,8 @@ __device__ __forceinline__ double rcp64a(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
-// one Newton step on the MUFU seed (~2^-44 relative): the LDL^T pivots of the ALS recurrence --
-// a 1e-13 relative perturbation of the factorisation, far below the 1e-5 direct-KK tolerance
-// (the second step was on the recurrence's critical path)
+// one Newton step on the MUFU seed (~2^-44 relative): the LDL^T pivots of the ALS recurrence -- a
+// 1e-13 relative perturbation of the factorisation, far below the 1e-5 direct-KK tolerance
 __device__ __forceinline__ double rcp64n1(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -43,7 +49,7 @@ __device__ __forceinline__ double rcp64n1(double x) {
   return fma(r, e, r);
 }
 
-// band of lam D^T D (second differences): diagonal d0, first off-diagonal d1 (coupling i, i+1)
+// band of D^T D (second differences): diagonal d0, first off-diagonal d1 (coupling i, i+1)
 __device__ __forceinline__ double d0v(int i, int M) {
   return (i == 0 || i == M - 1) ? 1.0 : ((i == 1 || i == M - 2) ? 5.0 : 6.0);
 }
@@ -66,20 +72,14 @@ __device__ __forceinline__ M2 inv(const M2& x) {
 __device__ __forceinline__ double2 mulv(const M2& x, double2 v) {
   return make_double2(x.a * v.x + x.b * v.y, x.c * v.x + x.d * v.y);
 }
-__device__ __forceinline__ M2 shfl(const M2& x, int delta, bool up) {
-  M2 r;
-  if (up) {
-    r.a = __shfl_up_sync(0xffffffffu, x.a, delta); r.b = __shfl_up_sync(0xffffffffu, x.b, delta);
-    r.c = __shfl_up_sync(0xffffffffu, x.c, delta); r.d = __shfl_up_sync(0xffffffffu, x.d, delta);
-  } else {
-    r.a = __shfl_down_sync(0xffffffffu, x.a, delta); r.b = __shfl_down_sync(0xffffffffu, x.b, delta);
-    r.c = __shfl_down_sync(0xffffffffu, x.c, delta); r.d = __shfl_down_sync(0xffffffffu, x.d, delta);
+
+template <int W>
+__device__ __forceinline__ void lane_get2(const double (&mine)[W], int src1, double (&out1)[W], int src2, double (&out2)[W]) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    out1[i] = __shfl_sync(0xffffffffu, mine[i], src1 & 31);
+    out2[i] = __shfl_sync(0xffffffffu, mine[i], src2 & 31);
   }
-  return r;
-}
-__device__ __forceinline__ double2 shflv(double2 v, int delta, bool up) {
-  if (up) return make_double2(__shfl_up_sync(0xffffffffu, v.x, delta), __shfl_up_sync(0xffffffffu, v.y, delta));
-  return make_double2(__shfl_down_sync(0xffffffffu, v.x, delta), __shfl_down_sync(0xffffffffu, v.y, delta));
 }
 
 // segment of lane s: rows [seg_b(s), seg_b(s+1))
@@ -90,48 +90,60 @@ __device__ __forceinline__ int seg_of(int col, int M, int P) {
   return s;
 }
 
-// lane exchange among the NL threads of one spectrum: out = mine of lane src (src clamped; callers
-// ignore out-of-range sources).  NL = 32: shuffles; NL = 64 (two warps): through shared memory.
-template <int NL, int W>
-__device__ __forceinline__ void lane_get2(const double (&mine)[W], int src1, double (&out1)[W], int src2,
-                                          double (&out2)[W], double* xs) {
-  if constexpr (NL == 32) {
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-      out1[i] = __shfl_sync(0xffffffffu, mine[i], src1 & 31);
-      out2[i] = __shfl_sync(0xffffffffu, mine[i], src2 & 31);
-    }
-  } else {
-    __syncthreads();   // the previous exchange's reads are done
-#pragma unroll
-    for (int i = 0; i < W; ++i) xs[i * NL + threadIdx.x] = mine[i];
-    __syncthreads();
-    const int a = min(max(src1, 0), NL - 1), b = min(max(src2, 0), NL - 1);
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-      out1[i] = xs[i * NL + a];
-      out2[i] = xs[i * NL + b];
-    }
-  }
+// interior weights of a segment: one bit per interior row (bit r <-> segment row r; 1 <-> w = p) in
+// a 64-bit (T <= 64) or 128-bit register.  A pass visits the rows in elimination order (ascending or
+// descending); it reads and rebuilds the mask through "position order" words (bit t <-> t-th row
+// visited), one shift per row, and converts with a bit reversal once per pass.
+template <typename MT> struct MaskBits { static constexpr int N = 8 * (int)sizeof(MT); };
+__device__ __forceinline__ unsigned long long mask_rev(unsigned long long m) { return __brevll(m); }
+__device__ __forceinline__ unsigned __int128 mask_rev(unsigned __int128 m) {
+  return ((unsigned __int128)__brevll((unsigned long long)m) << 64) | __brevll((unsigned long long)(m >> 64));
 }
-template <int NL>
-__device__ __forceinline__ void spectrum_sync() {
-  if constexpr (NL == 32) __syncwarp();
-  else __syncthreads();
+template <typename MT>   // row-order mask -> position-order cursor (bit 0 = first row visited)
+__device__ __forceinline__ MT mask_cursor(MT m, int nn, bool desc) {
+  return desc ? (MT)(mask_rev(m) >> (MaskBits<MT>::N - nn)) : m;
+}
+template <typename MT>
+__device__ __forceinline__ bool mask_take(MT& c) {
+  const bool v = (bool)(c & (MT)1);
+  c >>= 1;
+  return v;
+}
+template <typename MT>   // append the visited row's bit at the top (position t ends at bit N - nn + t)
+__device__ __forceinline__ void mask_push(MT& m, bool v) {
+  m = (MT)(m >> 1) | ((MT)v << (MaskBits<MT>::N - 1));
+}
+template <typename MT>   // pushed word -> row-order mask
+__device__ __forceinline__ MT mask_final(MT m, int nn, bool desc) {
+  return desc ? mask_rev(m) : (MT)(m >> (MaskBits<MT>::N - nn));
 }
 
-// NL threads (one or two warps) per spectrum, P <= NL segments: two warps halve the dependent chain
-// of every lane (the solver is latency-bound at ~7 spectra per SM, the shared-memory limit)
-template <typename TY, typename TZ, int NL>
-__global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, int64_t n, int M, int P, int T,
-                                                      double lam, double p, int iters, TZ* __restrict__ z) {
-  extern __shared__ __align__(16) double sh[];
-  double* sl1 = sh;                  // [T][32] l1 of the current factorisation
-  double* srd = sl1 + NL * T;        // [T][NL] 1/D
-  double* sg = srd + NL * T;         // [T][NL] g = D^-1 L^-1 f~   (finally: z)
-  double* xs = sg + NL * T;          // [10][NL] lane-exchange scratch (NL = 64)
-  TY* sy = reinterpret_cast<TY*>(xs + (NL == 64 ? 10 * NL : 0));     // [T][NL] y (input precision)
-  unsigned char* sw = reinterpret_cast<unsigned char*>(sy + NL * T);   // [T][NL] w: 1 -> p, 0 -> 1-p
+// row block of the shared-memory state: l1 | 1/D | g (fp64 x 32 lanes) | y (TY x 32 lanes)
+template <typename TY>
+struct RowLayout {
+  static constexpr int OFF_L1 = 0;
+  static constexpr int OFF_RD = 8 * NL;
+  static constexpr int OFF_G = 16 * NL;
+  static constexpr int OFF_Y = 24 * NL;
+  // + 8 B: consecutive rows start 2 banks apart, so the coalesced-load scatter of y (32 consecutive
+  // channels = 32 consecutive rows of one segment) is 2-way instead of 32-way bank conflicted
+  static constexpr int BYTES = 24 * NL + (int)sizeof(TY) * NL + 8;
+};
+
+template <typename TY>
+__device__ __forceinline__ double ld_y(const unsigned char* rowp, int s) {
+  return (double)*reinterpret_cast<const TY*>(rowp + RowLayout<TY>::OFF_Y + s * (int)sizeof(TY));
+}
+__device__ __forceinline__ double& fld(unsigned char* rowp, int off, int s) {
+  return *reinterpret_cast<double*>(rowp + off + 8 * s);
+}
+
+template <typename TY, typename TZ, typename MT>
+__global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, int64_t n, int M, int P, int T, double lam,
+                                                     double p, int iters, TZ* __restrict__ z, int* __restrict__ solves) {
+  extern __shared__ __align__(16) unsigned char shm[];
+  using RL = RowLayout<TY>;
+  constexpr int RS = RL::BYTES;
   const int s = threadIdx.x;
   const bool act = s < P;
   const int b = act ? seg_b(s, M, P) : M, e = act ? seg_b(s + 1, M, P) : M;
@@ -141,54 +153,59 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
   const bool edge = act && (b <= 1 || b + nn >= M - 1);
   const double q = 1.0 - p;
   const double lam2 = lam * lam, lam6 = 6.0 * lam, lamm4 = -4.0 * lam;
+  int solves_local = 0;
 
   for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
     const TY* yr = y + row * (int64_t)M;
-    spectrum_sync<NL>();
+    __syncwarp();
     for (int col = s; col < M; col += NL) {           // coalesced read, scatter to [t][lane]
       const int sc = seg_of(col, M, P);
-      sy[(col - seg_b(sc, M, P)) * NL + sc] = yr[col];
+      *reinterpret_cast<TY*>(shm + (col - seg_b(sc, M, P)) * RS + RL::OFF_Y + sc * (int)sizeof(TY)) = yr[col];
     }
-    spectrum_sync<NL>();
-    double2 xL = make_double2(0.0, 0.0), xR = make_double2(0.0, 0.0);   // separator values (left: S_{s-1})
-    for (int it = 0; it <= iters; ++it) {
+    __syncwarp();
+    MT im = 0;                 // interior weights (bit 1 <-> p); w^0 = 1 is handled by it == 0
+    bool ws0 = false, ws1 = false;   // separator weights (rows e-2, e-1)
+    bool sep_flip = true;      // a separator weight changed in the previous solve
+    double2 xL = make_double2(0.0, 0.0), xR = make_double2(0.0, 0.0);
+    int it = 0;
+    for (;; ++it) {
       const bool dr = it & 1;                 // 0: ascending elimination, 1: descending
-      const int ix0 = dr ? (nn - 1) * NL + s : s, dix = dr ? -NL : NL;
       const int i0 = dr ? b + nn - 1 : b, di = dr ? -1 : 1;
+      const int r0 = dr ? nn - 1 : 0;         // segment row of the first eliminated row
+      const int dstep = dr ? -RS : RS;
       const int na = dr ? e - 2 : b - 1;      // near-adjacent separator row
       const bool hasN = dr ? hasR : hasL, hasF = dr ? hasL : hasR;
+      const bool bsub = it > 0, fact = it < iters;
       // ---------------- pass A: back-substitution of the previous system (it > 0) and factorisation
       //                  + forward substitution of the next (it < iters), in elimination order
       double z1 = 0.0, z2 = 0.0;
       double Dm1 = 0.0, rDm1 = 0.0, rDm2 = 0.0, L1m1 = 0.0, L1m2 = 0.0;
       double gf1 = 0.0, gf2 = 0.0, ga1 = 0.0, ga2 = 0.0, gb1 = 0.0, gb2 = 0.0;
       double Caa = 0.0, Cab = 0.0, Cbb = 0.0, Cfa = 0.0, Cfb = 0.0;
+      bool iflip = false;
       const double ea0 = hasN ? cpl(i0, na, M, lam) : 0.0, eb0 = hasN ? lam : 0.0, ea1 = hasN ? lam : 0.0;
       using T_ = std::true_type;
       using F_ = std::false_type;
       auto passA = [&](auto bsub_c, auto fact_c) {
         constexpr bool BSUB = decltype(bsub_c)::value, FACT = decltype(fact_c)::value;
-        int ix = ix0, i = i0;
-        // the next row's shared-memory operands are loaded at the top of each step, before this row's
-        // stores: the compiler otherwise orders every load behind the previous row's stores (the
-        // arrays may alias) and the smem latency joins the dependent chain (tools/micro/rowpass.cu)
-        const int ixmax = (T - 1) * NL + s;
-        double cy = 0.0, cg = 0.0, cl1 = 0.0, crd = 0.0;
-        if (nn > 0) {
-          cy = (double)sy[ix];
-          if constexpr (BSUB) { cg = sg[ix]; cl1 = sl1[ix]; crd = srd[ix]; }
-        }
-        // one row in elimination order; ea/eb = near-spike entries (t < 2), LASTROW: l1 = 0
-        // EDGE: this position may hold one of the rows 0, 1, M-2, M-1 (where D^T D's band differs);
-        // only the peeled positions t = 0, 1, nn-2, nn-1 can, so the main loop runs without the check
+        if (nn == 0) return;                      // lanes beyond the P segments
+        unsigned char* rp = shm + r0 * RS;
+        int i = i0;
+        // the next row's operands are loaded at the top of each step, before this row's stores
+        double cy = ld_y<TY>(rp, s), cg = 0.0, cl1 = 0.0, crd = 0.0;
+        if constexpr (BSUB) { cg = fld(rp, RL::OFF_G, s); cl1 = fld(rp, RL::OFF_L1, s); crd = fld(rp, RL::OFF_RD, s); }
+        MT new_m = 0;
+        // one row in elimination order; ea/eb = near-spike entries (t < 2); LASTROW: l1 = 0 and no
+        // prefetch; EDGE: this position may hold one of the rows 0, 1, M-2, M-1
         auto step = [&](auto last_c, auto edge_c, double ea, double eb) {
           constexpr bool LASTROW = decltype(last_c)::value, EDGE = decltype(edge_c)::value;
           const double yv = cy;
           const double g_old = cg, l1_old = cl1, rd_old = crd;
-          {
-            const int ixn = min(max(ix + dix, s), ixmax);   // (clamped: past-the-segment rows are unused)
-            cy = (double)sy[ixn];
-            if constexpr (BSUB) { cg = sg[ixn]; cl1 = sl1[ixn]; crd = srd[ixn]; }
+          unsigned char* const cur = rp;
+          if constexpr (!LASTROW) {
+            rp += dstep;
+            cy = ld_y<TY>(rp, s);
+            if constexpr (BSUB) { cg = fld(rp, RL::OFF_G, s); cl1 = fld(rp, RL::OFF_L1, s); crd = fld(rp, RL::OFF_RD, s); }
           }
           double wv = 1.0;
           if constexpr (BSUB) {
@@ -197,8 +214,10 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
             const double zv = g_old - l1_old * z1 - lam * rd_old * z2;
             z2 = z1;
             z1 = zv;
-            wv = yv > zv ? p : q;
-            if constexpr (!FACT) sg[ix] = zv;
+            const bool wp = yv > zv;
+            mask_push<MT>(new_m, wp);
+            wv = wp ? p : q;
+            fld(cur, RL::OFF_G, s) = zv;          // kept: the output if this solve is the last
           }
           if constexpr (FACT) {
             double ld0 = lam6, ld1 = lamm4;
@@ -217,9 +236,8 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
             Cbb = fma(gb, ub, Cbb);
             Cfa = fma(gf, ua, Cfa);
             Cfb = fma(gf, ub, Cfb);
-            sl1[ix] = l1n;
-            srd[ix] = rd;
-            sw[ix] = wv == p ? 1 : 0;
+            fld(cur, RL::OFF_L1, s) = l1n;
+            fld(cur, RL::OFF_RD, s) = rd;
             Dm1 = D;
             rDm2 = rDm1;
             rDm1 = rd;
@@ -229,21 +247,31 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
             ga2 = ga1; ga1 = ga;
             gb2 = gb1; gb1 = gb;
           }
-          ix += dix;
           i += di;
         };
-        if (nn == 0) return;                      // lanes beyond the P segments
         step(F_{}, T_{}, ea0, eb0);               // t = 0   (nn >= 2 on active lanes)
-        if (nn == 2) { step(T_{}, T_{}, ea1, 0.0); return; }
-        step(F_{}, T_{}, ea1, 0.0);               // t = 1
+        if (nn == 2) {
+          step(T_{}, T_{}, ea1, 0.0);
+        } else {
+          step(F_{}, T_{}, ea1, 0.0);               // t = 1
 #pragma unroll 2
-        for (int t = 2; t < nn - 2; ++t) step(F_{}, F_{}, 0.0, 0.0);
-        if (nn >= 4) step(F_{}, T_{}, 0.0, 0.0);  // t = nn - 2
-        step(T_{}, T_{}, 0.0, 0.0);               // t = nn - 1
+          for (int t = 2; t < nn - 2; ++t) step(F_{}, F_{}, 0.0, 0.0);
+          if (nn >= 4) step(F_{}, T_{}, 0.0, 0.0);  // t = nn - 2
+          step(T_{}, T_{}, 0.0, 0.0);               // t = nn - 1
+        }
+        if constexpr (BSUB) {
+          const MT nm = mask_final<MT>(new_m, nn, dr);
+          iflip = nm != im;
+          im = nm;
+        }
       };
       if (it == 0) passA(F_{}, T_{});
-      else if (it < iters) passA(T_{}, T_{});
-      else { passA(T_{}, F_{}); break; }
+      else if (fact) passA(T_{}, T_{});
+      else passA(T_{}, F_{});
+      // the previous solve changed no weight: this system equals it, so its solution is final
+      // (interior z in the g slots from this pass A, separators from the previous reduction)
+      if (it >= 2 && !__any_sync(0xffffffffu, iflip || sep_flip)) break;
+      if (!fact) break;
       // ---------------- far spike columns (nonzero only in the last two eliminated rows: after the
       //                  loop the shift registers hold t = nn-1 in *1 and t = nn-2 in *2)
       double Cff_aa = 0.0, Cff_ab = 0.0, Cff_bb = 0.0;                 // far x far (fa, ff)
@@ -292,29 +320,33 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
       {   // from lane s + 1
         const double mine[10] = {CLL.a, CLL.b, CLL.c, CLL.d, CLR.a, CLR.b, CLR.c, CLR.d, CfL.x, CfL.y};
         double o[10], o2[10];
-        lane_get2<NL, 10>(mine, s + 1, o, s + 1, o2, xs);
+        lane_get2<10>(mine, s + 1, o, s + 1, o2);
         nLL = {o[0], o[1], o[2], o[3]};
         nLR = {o[4], o[5], o[6], o[7]};
         nCfL = make_double2(o[8], o[9]);
       }
+      unsigned char* const sep0 = shm + nn * RS;        // rows e-2, e-1 (segment rows nn, nn+1)
+      unsigned char* const sep1 = sep0 + RS;
       M2 Dk = {1.0, 0.0, 0.0, 1.0}, Uk = {0.0, 0.0, 0.0, 0.0};
       double2 rk = make_double2(0.0, 0.0);
+      double ys0 = 0.0, ys1 = 0.0;
       if (hasR) {
         const int i0s = e - 2, i1s = e - 1;
-        const int l0 = (i0s - b) * NL + s, l1x = (i1s - b) * NL + s;
-        const double w0 = it == 0 ? 1.0 : (sw[l0] ? p : q);
-        const double w1 = it == 0 ? 1.0 : (sw[l1x] ? p : q);
+        ys0 = ld_y<TY>(sep0, s);
+        ys1 = ld_y<TY>(sep1, s);
+        const double w0 = it == 0 ? 1.0 : (ws0 ? p : q);
+        const double w1 = it == 0 ? 1.0 : (ws1 ? p : q);
         const double off = lam * d1v(i0s, M);
         Dk = {w0 + lam * d0v(i0s, M) - CRR.a - nLL.a, off - CRR.b - nLL.b, off - CRR.c - nLL.c,
               w1 + lam * d0v(i1s, M) - CRR.d - nLL.d};
         Uk = {-nLR.a, -nLR.b, -nLR.c, -nLR.d};
-        rk = make_double2(w0 * (double)sy[l0] - CfR.x - nCfL.x, w1 * (double)sy[l1x] - CfR.y - nCfL.y);
+        rk = make_double2(w0 * ys0 - CfR.x - nCfL.x, w1 * ys1 - CfR.y - nCfL.y);
       }
       M2 Lk;
       {   // from lane s - 1
         const double mine[4] = {Uk.a, Uk.b, Uk.c, Uk.d};
         double o[4], o2[4];
-        lane_get2<NL, 4>(mine, s - 1, o, s - 1, o2, xs);
+        lane_get2<4>(mine, s - 1, o, s - 1, o2);
         Lk = {o[0], o[1], o[2], o[3]};
       }
       Lk = {Lk.a, Lk.c, Lk.b, Lk.d};   // transpose
@@ -329,7 +361,7 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
         {   // from lanes s - h and s + h
           const double mine[10] = {Pm.a, Pm.b, Pm.c, Pm.d, Qm.a, Qm.b, Qm.c, Qm.d, sv.x, sv.y};
           double dn[10], up[10];
-          lane_get2<NL, 10>(mine, s - h, dn, s + h, up, xs);
+          lane_get2<10>(mine, s - h, dn, s + h, up);
           Pdn = {dn[0], dn[1], dn[2], dn[3]};
           Qdn = {dn[4], dn[5], dn[6], dn[7]};
           sdn = make_double2(dn[8], dn[9]);
@@ -359,16 +391,18 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
       {   // from lane s - 1
         const double mine[2] = {xR.x, xR.y};
         double o[2], o2[2];
-        lane_get2<NL, 2>(mine, s - 1, o, s - 1, o2, xs);
+        lane_get2<2>(mine, s - 1, o, s - 1, o2);
         xL = make_double2(o[0], o[1]);
       }
       if (!hasL) xL = make_double2(0.0, 0.0);
-      if (hasR) {   // separator values of this solve; weights for the next
-        const int l0 = (e - 2 - b) * NL + s, l1x = (e - 1 - b) * NL + s;
-        sg[l0] = xR.x;
-        sg[l1x] = xR.y;
-        sw[l0] = (double)sy[l0] > xR.x ? 1 : 0;
-        sw[l1x] = (double)sy[l1x] > xR.y ? 1 : 0;
+      sep_flip = false;
+      if (hasR) {   // separator values of this solve (the output if it is the last); weights for the next
+        fld(sep0, RL::OFF_G, s) = xR.x;
+        fld(sep1, RL::OFF_G, s) = xR.y;
+        const bool w0n = ys0 > xR.x, w1n = ys1 > xR.y;
+        sep_flip = it == 0 || w0n != ws0 || w1n != ws1;
+        ws0 = w0n;
+        ws1 = w1n;
       }
       // ---------------- pass B: forward substitution of the corrected interior right-hand side
       {
@@ -380,111 +414,102 @@ __global__ void __launch_bounds__(NL) als_part_kernel(const TY* __restrict__ y, 
         const double cL = cpl(r_last, fa, M, lam) * x_fa + lam * x_ff, cL2 = lam * x_fa;
         auto passB = [&](auto first_c) {
           constexpr bool FIRST = decltype(first_c)::value;
+          if (nn == 0) return;
+          MT cur_m = mask_cursor<MT>(im, nn, dr);
           double g1 = 0.0, g2 = 0.0, l1prev = 0.0, rdm1 = 0.0, rdm2 = 0.0;
-          int ix = ix0;
-          const int ixmaxB = (T - 1) * NL + s;
-          // next row's operands loaded before this row's store (see pass A)
-          unsigned char nw_ = 0;
-          double ny = 0.0, nrd = 0.0, nl1 = 0.0;
-          if (nn > 0) { nw_ = sw[ix]; ny = (double)sy[ix]; nrd = srd[ix]; nl1 = sl1[ix]; }
-          auto stepB = [&](double corr) {
-            const double wv = FIRST ? 1.0 : (nw_ ? p : q);
+          unsigned char* rp = shm + r0 * RS;
+          double ny = ld_y<TY>(rp, s), nrd = fld(rp, RL::OFF_RD, s), nl1 = fld(rp, RL::OFF_L1, s);
+          auto stepB = [&](auto last_c, double corr) {
+            constexpr bool LASTROW = decltype(last_c)::value;
+            const double wv = FIRST ? 1.0 : (mask_take<MT>(cur_m) ? p : q);
             const double f = wv * ny - corr;
             const double rd = nrd;
             const double l1c = nl1;
-            {
-              const int ixn = min(max(ix + dix, s), ixmaxB);
-              nw_ = sw[ixn]; ny = (double)sy[ixn]; nrd = srd[ixn]; nl1 = sl1[ixn];
+            unsigned char* const cur = rp;
+            if constexpr (!LASTROW) {
+              rp += dstep;
+              ny = ld_y<TY>(rp, s); nrd = fld(rp, RL::OFF_RD, s); nl1 = fld(rp, RL::OFF_L1, s);
             }
             const double g = f - l1prev * g1 - lam * rdm2 * g2;
-            sg[ix] = g * rd;
+            fld(cur, RL::OFF_G, s) = g * rd;
             g2 = g1;
             g1 = g;
             l1prev = l1c;
             rdm2 = rdm1;
             rdm1 = rd;
-            ix += dix;
           };
           if (nn < 5) {
-            for (int t = 0; t < nn; ++t)
-              stepB((t == 0 ? c0 : 0.0) + (t == 1 ? c1 : 0.0) + (t == nn - 2 ? cL2 : 0.0) + (t == nn - 1 ? cL : 0.0));
+            for (int t = 0; t < nn; ++t) {
+              const double corr = (t == 0 ? c0 : 0.0) + (t == 1 ? c1 : 0.0) + (t == nn - 2 ? cL2 : 0.0) + (t == nn - 1 ? cL : 0.0);
+              if (t == nn - 1) stepB(T_{}, corr);
+              else stepB(F_{}, corr);
+            }
           } else {
-            stepB(c0);
-            stepB(c1);
+            stepB(F_{}, c0);
+            stepB(F_{}, c1);
 #pragma unroll 2
-            for (int t = 2; t < nn - 2; ++t) stepB(0.0);
-            stepB(cL2);
-            stepB(cL);
+            for (int t = 2; t < nn - 2; ++t) stepB(F_{}, 0.0);
+            stepB(F_{}, cL2);
+            stepB(T_{}, cL);
           }
         };
         if (it == 0) passB(T_{});
         else passB(F_{});
       }
     }
+    solves_local += it;   // solves 0 .. it-1 were completed
     // ---------------- write z (interior from the last back-substitution, separators from the last solve)
-    spectrum_sync<NL>();
+    __syncwarp();
     TZ* zr = z + row * (int64_t)M;
     for (int col = s; col < M; col += NL) {
       const int sc = seg_of(col, M, P);
-      zr[col] = (TZ)sg[(col - seg_b(sc, M, P)) * NL + sc];
+      zr[col] = (TZ)*reinterpret_cast<const double*>(shm + (col - seg_b(sc, M, P)) * RS + RL::OFF_G + 8 * sc);
     }
   }
+  if (solves && s == 0) atomicAdd(solves, solves_local);
+}
+
+template <typename TY>
+size_t als_smem_bytes(int M) {
+  const int P = std::min(NL, M / 4);
+  const int T = (M + P - 1) / P;
+  return (size_t)T * RowLayout<TY>::BYTES;
 }
 
 }  // namespace
 
-// lanes per spectrum: 32 (one warp).  The two-warp variant (64 segments, FKK_ALS_LANES=64) halves every
-// lane's dependent chain but adds a PCR level and shared-memory lane exchanges; measured on cfg3 rows it
-// is no faster (13.06 vs 12.95 ms per 131,072 spectra: the extra exchange/separator work eats the gain)
-static int als_lanes(int M) {
-  const char* ev = getenv("FKK_ALS_LANES");
-  const int want = ev ? atoi(ev) : 32;
-  return (want == 64 && M / 4 >= 64) ? 64 : 32;
-}
-
 size_t als_part_smem(int M, int y_f64) {
-  const int NL = als_lanes(M);
-  const int P = M / 4 < NL ? M / 4 : NL;
-  if (P < 2) return 0;
-  const int T = (M + P - 1) / P;
-  return (size_t)NL * T * (3 * sizeof(double) + (y_f64 ? 8 : 4) + 1) + (NL == 64 ? 10 * (size_t)NL * sizeof(double) : 0);
+  if (M / 4 < 2) return 0;
+  return y_f64 ? als_smem_bytes<double>(M) : als_smem_bytes<float>(M);
 }
 
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s) {
-  const int NL = als_lanes(M);
-  const int P = M / 4 < NL ? M / 4 : NL;
+                     cudaStream_t s, int* solves) {
+  const int P = std::min(NL, M / 4);
   if (P < 2 || n <= 0) return false;
   const int T = (M + P - 1) / P;
-  const size_t sm = (size_t)NL * T * (3 * sizeof(double) + (y_f64 ? 8 : 4) + 1) +
-                    (NL == 64 ? 10 * (size_t)NL * sizeof(double) : 0);
+  if (T > 128) return false;
+  const size_t sm = als_part_smem(M, y_f64);
   int dev = 0, sms = 148, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (sm > (size_t)maxsm) return false;
-#define FKK_ALS_PART(TY, TZ, L)                                                                       \
+#define FKK_ALS_SEG(TY, TZ)                                                                           \
   {                                                                                                   \
-    auto kf = als_part_kernel<TY, TZ, L>;                                                             \
+    auto kf = T <= 64 ? als_seg_kernel<TY, TZ, unsigned long long> : als_seg_kernel<TY, TZ, unsigned __int128>; \
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
     int per = 1;                                                                                      \
-    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, L, sm));                   \
+    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, NL, sm));                  \
     const int64_t g = std::min<int64_t>(n, (int64_t)sms * std::max(per, 1));                         \
-    kf<<<(unsigned)g, L, sm, s>>>((const TY*)y, n, M, P, T, lam, p, iters, (TZ*)z);                   \
+    kf<<<(unsigned)g, NL, sm, s>>>((const TY*)y, n, M, P, T, lam, p, iters, (TZ*)z, solves);          \
   }
-#define FKK_ALS_TYPES(L)                                                                              \
-  if (y_f64 && z_f64) FKK_ALS_PART(double, double, L)                                                 \
-  else if (!y_f64 && !z_f64) FKK_ALS_PART(float, float, L)                                            \
-  else if (!y_f64 && z_f64) FKK_ALS_PART(float, double, L)                                            \
-  else FKK_ALS_PART(double, float, L)
-  if (NL == 64) {
-    FKK_ALS_TYPES(64)
-  } else {
-    FKK_ALS_TYPES(32)
-  }
-#undef FKK_ALS_TYPES
-#undef FKK_ALS_PART
-  check_launch("als_part");
+  if (y_f64 && z_f64) FKK_ALS_SEG(double, double)
+  else if (!y_f64 && !z_f64) FKK_ALS_SEG(float, float)
+  else if (!y_f64 && z_f64) FKK_ALS_SEG(float, double)
+  else FKK_ALS_SEG(double, float)
+#undef FKK_ALS_SEG
+  check_launch("als_seg");
   return true;
 }
 

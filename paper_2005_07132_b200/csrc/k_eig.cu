@@ -853,11 +853,16 @@ __global__ void __launch_bounds__(32) inviter_kernel(const double* __restrict__ 
     dd[i] = 1.0 / v;     // keep reciprocals: the solves multiply
   }
   __syncwarp();
-  // two solves (was three): lambda is within 2 eps ||T|| of the eigenvalue, so each solve grows the
-  // wanted component by ~gap / (eps ||T||) against the others; the CholQR2 that follows restores
-  // orthogonality inside clusters.  The eigensolver tests (clustered plateau with exact ties,
-  // rank-deficient G, residual <= 1e-10 ||G||) hold with two.
-  for (int it = 0; it < 2; ++it) {
+  // two solves: lambda is within 2 eps ||T|| of the eigenvalue, so each solve grows the wanted
+  // component by ~gap / (eps ||T||) against the others; the CholQR2 that follows restores
+  // orthogonality inside clusters.  A near-tie (relative gap to a computed neighbour below 1e-8)
+  // gets a third solve: there the vector's mix inside the cluster converges more slowly, and the
+  // per-column argmax of U S (q, Eqs. 13-15) depends on that mix.
+  double gap = 1e300;
+  if (jj > 0) gap = fmin(gap, fabs(lam[jj - 1] - lam[jj]));
+  if (jj + 1 < k) gap = fmin(gap, fabs(lam[jj + 1] - lam[jj]));
+  const int nsolve = gap < 1e-8 * tn ? 3 : 2;
+  for (int it = 0; it < nsolve; ++it) {
     if (lane == 0) {
       // forward: apply P and L^-1 (the running entry in a register)
       double zi = z[0];
@@ -1432,7 +1437,8 @@ __global__ void apply_rinv_kernel(const double* __restrict__ Z, int M, int k, co
 // the accepted ones (which spans the remaining eigenspace when the cluster is the null space).
 __global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __restrict__ fallback,
                                                                const double* __restrict__ Zin, double* __restrict__ Z,
-                                                               int M, int k) {
+                                                               int M, int k, const double* __restrict__ lam,
+                                                               const double* __restrict__ tnorm, int* __restrict__ flags) {
   if (*fallback == 0) return;
   __shared__ double dots[1024];
   __shared__ double red[32];
@@ -1475,6 +1481,9 @@ __global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __rest
     const double n0 = norm2(zj);
     project_out(zj, j);
     double n1 = norm2(zj);
+    // a replaced vector is an eigenvector only inside the (numerical) null space: a dependent
+    // vector whose eigenvalue is above 2 eps ||T|| is a numerical failure (flag bit 8)
+    if (!(n1 > 1e-12 * n0) && tid == 0 && flags && lam[j] > 2.220446049250313e-16 * 2.0 * tnorm[0]) atomicOr(flags, 8);
     for (int attempt = 0; attempt < 4 && !(n1 > 1e-12 * n0); ++attempt) {
       for (int i = tid; i < M; i += nt) {
         uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(j + 1 + 977 * attempt) + 0xC2B2AE3D27D4EB4Full * (uint64_t)(i + 1);
@@ -1660,7 +1669,7 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
       apply_rinv_kernel<<<agrid, 256, 0, s>>>(zin, M, k, T, zout);
       check_launch("eig_reorth_apply");
     }
-    reorth_fallback_kernel<<<1, 1024, 0, s>>>(fallback, Z, Z3, M, k);
+    reorth_fallback_kernel<<<1, 1024, 0, s>>>(fallback, Z, Z3, M, k, lam, tnorm, flags);
     check_launch("eig_reorth_fallback");
   } else {
     reorth_kernel<<<1, 1024, 0, s>>>(Z, M, k);

@@ -39,9 +39,16 @@ __host__ __device__ inline int pb_part(int kp) { return (kp / 8) * PB_SBO; }    
 __host__ __device__ inline int pb_stage(int kp) { return 2 * pb_part(kp); }
 __host__ __device__ inline int p_stage_bytes(int kp) { return 2 * PA_BYTES + pb_stage(kp); }
 __host__ __device__ inline int p_nstages(int kp) { return kp <= 64 ? 4 : 3; }
-constexpr int PSEG = 512;          // channels per hi*hi accumulator segment
-__host__ __device__ inline int p_nseg(int M) { return (M + PSEG - 1) / PSEG; }
-__host__ __device__ inline int p_set_cols(int M, int kp) { return (p_nseg(M) + 1) * kp; }
+// channels per hi*hi accumulator segment: 512 (the truncating fp32 TMEM accumulation stays within
+// the 1e-5 projection bar), longer when the (segments + cross) accumulator set would not leave two
+// A slots (128 columns) of tensor memory: k = 100 (kp = 128) at M = 1600 takes 2 segments of 800
+__host__ __device__ inline int p_seg_len(int M, int kp) {
+  int nseg = (M + 511) / 512;
+  while (nseg > 1 && (nseg + 1) * kp > 384) --nseg;
+  return (((M + nseg - 1) / nseg) + 31) & ~31;
+}
+__host__ __device__ inline int p_nseg(int M, int kp) { return (M + p_seg_len(M, kp) - 1) / p_seg_len(M, kp); }
+__host__ __device__ inline int p_set_cols(int M, int kp) { return (p_nseg(M, kp) + 1) * kp; }
 __host__ __device__ inline int p_nbuf(int M, int kp) { return 2 * p_set_cols(M, kp) <= 512 ? 2 : 1; }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -75,7 +82,8 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&acc_full[b], 1); tc::mbar_init(&acc_empty[b], 128); }
     tc::fence_mbar_init();
   }
-  const int nseg = p_nseg(M), setc = p_set_cols(M, kp), nbuf = p_nbuf(M, kp);
+  const int nseg = p_nseg(M, kp), setc = p_set_cols(M, kp), nbuf = p_nbuf(M, kp);
+  const int pseg = p_seg_len(M, kp);
   if (warp == 12) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
@@ -251,9 +259,9 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
         tc::tc_fence_after();
         const uint64_t dah = tc::sdesc_add(da0, (uint32_t)(stage * SB)), dal = tc::sdesc_add(dah, PA_BYTES);
         const uint64_t dbh = tc::sdesc_add(dw0, (uint32_t)(stage * SB)), dbl = tc::sdesc_add(dbh, (uint32_t)WP);
-        const int sg = (st * PKC) / PSEG;
+        const int sg = (st * PKC) / pseg;
         const uint32_t dh = dset + sg * kp;
-        const bool seg_start = (st * PKC) % PSEG == 0;
+        const bool seg_start = (st * PKC) % pseg == 0;
         if (tc::elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < PKC / 8; ++ks) {
@@ -361,7 +369,8 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
     tc::fence_mbar_init();
     tma::prefetch_map(&amap);
   }
-  const int nseg = p_nseg(M), setc = p_set_cols(M, kp);
+  const int nseg = p_nseg(M, kp), setc = p_set_cols(M, kp);
+  const int pseg = p_seg_len(M, kp);
   if (ir_smem)
     for (int c = tid; c < ((M + 31) & ~31); c += blockDim.x) sir[c] = inv_ref[c];
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -569,9 +578,9 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
         const uint32_t sw = tc::smem_u32(ring_w + rw.slot * 2 * WP);
         const uint64_t dbh = make_sdesc_sw128(sw), dbl = make_sdesc_sw128(sw + WP);
         const uint32_t tah = tmem_a + (uint32_t)(rt.slot * 2 * QKC), tal = tah + QKC;
-        const int sg = (st * QKC) / PSEG;
+        const int sg = (st * QKC) / pseg;
         const uint32_t dh = dset + sg * kp;
-        const bool seg_start = (st * QKC) % PSEG == 0;
+        const bool seg_start = (st * QKC) % pseg == 0;
         if (tc::elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < QKC / 8; ++ks) {

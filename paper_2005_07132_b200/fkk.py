@@ -69,6 +69,7 @@ _SIGS = {
     "fkk_transform_host": (_i32, [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
     "fkk_apply_trained_basis_host": (_i32, [_vp, _vp, _vp, _i64, _vp]),
     "kk_direct_batch_host": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "fkk_apply_trained_basis_stream": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, ctypes.POINTER(ctypes.c_float)]),
     "fkk_basis_destroy": (_i32, [_vp]),
     "fkk_basis_info": (_i32, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "fkk_stage_size": (ctypes.c_size_t, [_vp, _i32]),
@@ -77,6 +78,7 @@ _SIGS = {
     "fkk_enable_timing": (_i32, [_vp, _i32]),
     "fkk_stage_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _i32]),
     "fkk_last_launch_count": (_i64, [_vp]),
+    "fkk_debug_als_solves": (_i64, [_vp]),
     "fkk_host_eig_topk": (_i32, [_dp, _i32, _i32, _dp, _dp]),
     "fkk_debug_tc_mma": (_i32, [_i32, _vp, _vp, _vp, _i32]),
     "fkk_debug_eig_topk": (_i32, [_vp, _i32, _i32, _vp, _vp]),
@@ -282,6 +284,16 @@ class Plan:
         _check(self._h, _lib.kk_direct_batch_host(self._h, self._host_ptr(I), I.shape[0], self._host_ptr(Iref),
                                                   self._host_ptr(out)))
 
+    def apply_stream(self, basis: Basis, I, out, batch: int) -> np.ndarray:
+        """fkk_apply_trained_basis_stream: host cube (pinned) -> host output in `batch`-spectrum batches;
+        returns the per-batch end-to-end latencies (ms)."""
+        nb = max(1, -(-I.shape[0] // batch))
+        ms = np.zeros(nb, dtype=np.float32)
+        _check(self._h, _lib.fkk_apply_trained_basis_stream(self._h, basis.handle, self._host_ptr(I), I.shape[0], batch,
+                                                            self._host_ptr(out),
+                                                            ms.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return ms
+
     def apply_host(self, basis: Basis, I, out):
         _check(self._h, _lib.fkk_apply_trained_basis_host(self._h, basis.handle, self._host_ptr(I), I.shape[0],
                                                           self._host_ptr(out)))
@@ -322,6 +334,10 @@ class Plan:
     @property
     def launches(self) -> int:
         return int(_lib.fkk_last_launch_count(self._h))
+
+    def als_solves(self) -> int:
+        """ALS solves summed over the direct-path spectra since the last query (then reset)."""
+        return int(_lib.fkk_debug_als_solves(self._h))
 
 
 def kk_direct_batch_raw(handle, I, Iref, out) -> int:

@@ -68,23 +68,11 @@ def test_direct_cfg2_sample_f32(torch_cuda, fkk):
     assert np.array_equal(Ki, K[:4096].imag)
 
 
-@pytest.mark.parametrize("M", [16, 100, 1600])
+@pytest.mark.parametrize("M", [16, 100, 1600, 2048])
 def test_direct_segment_edge_sizes(torch_cuda, fkk, M):
     """The warp-partitioned ALS splits M into min(32, M/4) segments: M = 16 (4 segments of 4 rows,
-    2-row interiors), 100 (25 segments), 1600 (32 segments of 50, the cfg4 channel count)."""
-    cfg = CONFIGS["cfg1"].with_(height=4, width=9, n_freq=M)
-    I, Iref, _ = generate(cfg)
-    K_or = O.kk_direct(I, Iref, O.Params())
-    plan = fkk.Plan(M, 4, I.shape[0], in_dtype="f64")
-    K = plan.direct(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
-    assert _rel_inf(K, K_or) <= 1e-5
-
-
-@pytest.mark.parametrize("M", [256, 1000])
-def test_direct_two_warp_als(torch_cuda, fkk, M, monkeypatch):
-    """The opt-in two-warp ALS (64 segments per spectrum, shared-memory lane exchanges, 6 PCR
-    levels): M = 256 gives 4-row segments (2-row interiors)."""
-    monkeypatch.setenv("FKK_ALS_LANES", "64")
+    2-row interiors), 100 (25 segments), 1600 (32 segments of 50, the cfg4 channel count), 2048 (64-row
+    segments: the full 64-bit weight mask; L = 4096, the largest direct-path FFT)."""
     cfg = CONFIGS["cfg1"].with_(height=4, width=9, n_freq=M)
     I, Iref, _ = generate(cfg)
     K_or = O.kk_direct(I, Iref, O.Params())
