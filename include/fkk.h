@@ -66,6 +66,7 @@ typedef enum { FKK_IN_F32 = 0, FKK_IN_F64 = 1 } fkk_in_dtype;
 typedef enum { FKK_GEMM_3XTF32 = 0, FKK_GEMM_FP32_SIMT = 1 } fkk_gemm_impl;
 typedef enum { FKK_F_ONE = 0, FKK_F_EQ9 = 1 } fkk_f_mode;
 
+typedef enum { FKK_SVD_GRAM = 0, FKK_SVD_RANGE_FINDER = 1 } fkk_svd_mode;
 typedef struct fkk_plan* fkk_plan_t;
 typedef struct fkk_basis* fkk_basis_t;
 
@@ -93,6 +94,16 @@ typedef struct {
   const uint8_t* nccl_id;    /* 128-byte ncclUniqueId from fkk_get_nccl_unique_id; NULL iff world_size == 1 */
   int32_t loopback_shards;   /* >1: run the Gram/projection per virtual shard on one GPU and combine
                                 in the multi-rank order (partition-invariance test mode) */
+  /* F2-F4 method ("random sampling ('randomized') SVD", Halko 2011):
+   * FKK_SVD_GRAM (default) = Gram A^T A + fp64 eigensolver; FKK_SVD_RANGE_FINDER = randomized subspace
+   * iteration: Y = A Omega (Omega: M x (k + rf_oversample) Gaussian from SplitMix64 counters keyed by
+   * rf_seed, oracle/range_finder_omega), rf_power_iters times {Y = A orth(A^T orth(Y))}, then the SVD
+   * of B = orth(Y)^T A.  Needs k + rf_oversample <= min(M, 128), f32 input, world_size/loopback as
+   * the Gram path (the l x M and l x l products are all-reduced). */
+  int32_t svd_mode;          /* fkk_svd_mode, default FKK_SVD_GRAM */
+  int32_t rf_oversample;     /* p >= 0, default 10 */
+  int32_t rf_power_iters;    /* q >= 0, default 1 */
+  uint64_t rf_seed;          /* test-matrix seed, default 0 */
 } fkk_plan_desc;
 
 /* Fill *d with the defaults above for the given M, k and max_rows. */
@@ -194,6 +205,31 @@ int64_t fkk_last_launch_count(fkk_plan_t p);
  * (the ALS stops once a solve changes no weight, PAPER.md:45 / reading A6; iters per spectrum =
  * this / spectra).  Synchronises the plan stream and resets the counter; -1 on a CUDA error. */
 int64_t fkk_debug_als_solves(fkk_plan_t p);
+/* Host helper (no GPU): the range finder's test matrix Omega for seed, M x l row-major
+ * into out_Mxl: entry (j, i) = sqrt(-2 ln u1) cos(2 pi u2), u1 = ((h(2c) >> 11) + 1) / 2^53,
+ * u2 = (h(2c+1) >> 11) / 2^53, h = SplitMix64, counter c = seed 2^40 + j l + i.  Returns 0, or 1 on bad
+ * arguments. */
+int32_t fkk_range_finder_omega(uint64_t seed, int32_t M, int32_t l, double* out_Mxl);
+
+/* Collectives supplied by the caller (host buffers; each returns 0 on success), for running the sharded
+ * transform's exchange sequence without GPUs. */
+typedef struct {
+  void* ctx;
+  int32_t world_size, rank;
+  int32_t (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);   /* recv: world x bytes */
+  int32_t (*allreduce_sum_f64)(void* ctx, double* data, size_t n);
+  int32_t (*allreduce_max_i32)(void* ctx, int32_t* data, size_t n);
+} fkk_host_collectives;
+/* The collective sequence of a pixel-sharded fkk_transform on host data, through
+ * the same C++ sequence functions the NCCL path calls: row-count allgather (-> *row0_out, *n_global_out),
+ * Gram all-reduce (G: M x M local partial in, global sum out), extremes allgather + merge (ext_val /
+ * ext_idx: shards x k x 2 local column max / min and their GLOBAL pixel indices; -> q_out (<= 2k,
+ * ascending), *nq_out), X = US[q] all-reduce (US_local: n_rows x k row-major; X_out: nq x k), error-flag
+ * max-reduce (*flags in/out).  Collective over the caller's ranks; no GPU needed. */
+fkk_status fkk_exchange_selftest(const fkk_host_collectives* comm, int64_t n_rows, int32_t M, int32_t k, int32_t shards,
+                                 double* G, const float* ext_val, const int64_t* ext_idx, const float* US_local,
+                                 int32_t* flags, int64_t* row0_out, int64_t* n_global_out, int64_t* q_out,
+                                 int32_t* nq_out, double* X_out);
 
 /* Test hook (tensor-core plumbing self-test): one tcgen05.mma kind::tf32 of A (128 x 8, row-major
  * fp32, device) times B^T (B: N x 8, N in {16, 32, ..., 256}) into D (128 x N fp32, device) with the

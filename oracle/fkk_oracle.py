@@ -317,6 +317,74 @@ def fkk_ec(I: np.ndarray, I_ref: np.ndarray, k: int, p: Params = Params()) -> di
     return out
 
 
+# ----------------------------------------------------------------------------------------------
+# Randomized range finder SVD ("random sampling ('randomized') SVD
+# ... [Halko 2011]"): randomized subspace iteration followed by the SVD of the small projected matrix.
+# ----------------------------------------------------------------------------------------------
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """SplitMix64 finaliser on uint64 counters (Steele, Lea & Flood 2014): the counter-based generator
+    the range finder draws its test matrix from (the CUDA library implements the same function)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def range_finder_omega(seed: int, M: int, l: int) -> np.ndarray:
+    """Gaussian test matrix Omega (M x l) by Box-Muller from two SplitMix64 draws per entry:
+    u1 = (h(2c) >> 11 + 1) / 2^53, u2 = (h(2c+1) >> 11) / 2^53 with counter c = seed * 2^40 + j * l + i
+    for entry (j, i);  Omega[j, i] = sqrt(-2 ln u1) cos(2 pi u2)."""
+    j, i = np.meshgrid(np.arange(M, dtype=np.uint64), np.arange(l, dtype=np.uint64), indexing="ij")
+    c = np.uint64(seed) * np.uint64(1 << 40) + j * np.uint64(l) + i
+    h1 = splitmix64(np.uint64(2) * c)
+    h2 = splitmix64(np.uint64(2) * c + np.uint64(1))
+    u1 = ((h1 >> np.uint64(11)).astype(np.float64) + 1.0) / 9007199254740992.0
+    u2 = (h2 >> np.uint64(11)).astype(np.float64) / 9007199254740992.0
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+
+
+def _orth(Y: np.ndarray) -> np.ndarray:
+    """Orthonormal basis of range(Y) (Householder QR, numpy.linalg.qr)."""
+    return np.linalg.qr(Y)[0]
+
+
+def randomized_svd(A: np.ndarray, k: int, omega: np.ndarray, q: int) -> tuple[np.ndarray, np.ndarray]:
+    """Halko, Martinsson & Tropp (2011), Alg. 4.4 (randomized subspace iteration) + Alg. 5.1 (direct
+    SVD): Y = A Omega; Q = orth(Y); q times {Q = orth(A orth(A^T Q))}; B = Q^T A; B = U~ S V^T.
+    Returns V_k (M x k, the sign rule of eig_topk) and s_k."""
+    Q = _orth(A @ omega)
+    for _ in range(q):
+        Q = _orth(A.T @ Q)
+        Q = _orth(A @ Q)
+    B = Q.T @ A
+    _, sv, Vt = np.linalg.svd(B, full_matrices=False)
+    V = Vt[:k].T.copy()
+    for i in range(k):
+        jmax = int(np.argmax(np.abs(V[:, i])))
+        if V[jmax, i] < 0:
+            V[:, i] = -V[:, i]
+    return V, sv[:k]
+
+
+def fkk_ec_randomized(I: np.ndarray, I_ref: np.ndarray, k: int, oversample: int, q: int, seed: int,
+                      p: Params = Params()) -> dict:
+    """fKK-EC with the randomized range finder in place of the Gram eigensolver (F2-F4), then F5..F11
+    as fkk_ec (PAPER.md:226 with Fig. 1(b))."""
+    f = noise_scale_f(I, p)
+    A = log_ratio(I, I_ref, p, f)
+    omega = range_finder_omega(seed, A.shape[1], k + oversample)
+    V, s = randomized_svd(A, k, omega, q)
+    US = A @ V
+    qq = select_q(US)
+    out = fkk_ec_from(I, I_ref, V, s, qq, p, f=f, A=A)
+    out.update(f=f, V=V, s=s, omega=omega)
+    return out
+
+
 def fkk_ec_from(I, I_ref, V, s, q, p: Params = Params(), f=None, A=None) -> dict:
     """F5..F11 with a given V_k, s and q (stage-wise parity, DESIGN.md parity contract)."""
     if f is None:

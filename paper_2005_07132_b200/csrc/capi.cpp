@@ -16,6 +16,8 @@
 
 #include "../../include/fkk.h"
 #include "fkk_internal.h"
+#include "exchange.h"
+#include <thread>
 
 using fkk::Status;
 
@@ -30,6 +32,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -43,6 +46,7 @@ struct NcclApi {
     FKK_SYM(CommInitRank, "ncclCommInitRank");
     FKK_SYM(CommDestroy, "ncclCommDestroy");
     FKK_SYM(CommAbort, "ncclCommAbort");
+    FKK_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
     FKK_SYM(AllReduce, "ncclAllReduce");
     FKK_SYM(AllGather, "ncclAllGather");
     FKK_SYM(GetErrorString, "ncclGetErrorString");
@@ -109,6 +113,9 @@ struct fkk_plan {
   std::string err;
   // NCCL
   ncclComm_t comm = nullptr;
+  std::unique_ptr<fkk::Collectives> coll;   // the sharded exchange's collectives (local copy or NCCL)
+  unsigned char* xscratch = nullptr;        // device staging of the control collectives (NCCL)
+  size_t xscratch_bytes = 0;
   // device workspace (factorized)
   int* flags = nullptr;
   int* h_flags = nullptr;   // pinned
@@ -152,6 +159,13 @@ struct fkk_plan {
   unsigned char* apre = nullptr;   // pre-split MMA image of A0
   int apre_blocks = 0;
   double* gtc_part = nullptr;
+  // randomized range finder (svd_mode = FKK_SVD_RANGE_FINDER): l = k + oversample columns
+  int rf_l = 0, rf_nsplit = 0;
+  double *rf_omega = nullptr, *rf_part = nullptr, *rf_Z = nullptr, *rf_Zq = nullptr, *rf_Z2 = nullptr,
+         *rf_SY = nullptr, *rf_S = nullptr, *rf_T = nullptr, *rf_U = nullptr, *rf_lam = nullptr;
+  float *rf_wimg = nullptr, *rf_Y = nullptr;
+  int2* rf_tiles = nullptr;
+  int* rf_fallback = nullptr;
   // direct path (lazy)
   int64_t direct_batch = 0;
   float *phi = nullptr, *phierr = nullptr;
@@ -182,7 +196,8 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, pmap, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, d_in_cube,
+                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, rf_omega, rf_part, rf_Z, rf_Zq, rf_Z2, rf_SY, rf_S, rf_T, rf_U, rf_lam,
+                    rf_wimg, rf_Y, rf_tiles, rf_fallback, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
@@ -190,6 +205,8 @@ struct fkk_plan {
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     for (auto& m : marks) cudaEventDestroy(m.second);
+    coll.reset();
+    if (xscratch) cudaFree(xscratch);
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -230,9 +247,13 @@ struct fkk_plan {
   // the others blocked in the next collective.
   void check_flags_sync(bool collective = false);
   void check_flags_sync_impl(bool collective) {
-    if (collective && comm) nccl_allreduce_flags();
+    if (collective && d.world_size > 1) {
+      if (!comm) throw Status(FKK_ERR_STATE, "the communicator was aborted by an earlier failure; recreate the plan");
+      nccl_allreduce_flags();
+    }
     FKK_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    FKK_CUDA_CHECK(cudaStreamSynchronize(stream));
+    if (collective) coll->sync();
+    else FKK_CUDA_CHECK(cudaStreamSynchronize(stream));
     const int f = *h_flags;
     if (f) {
       FKK_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), stream));
@@ -256,9 +277,69 @@ struct fkk_plan {
   }
 };
 
-void fkk_plan::nccl_allreduce_flags() {
-  nccl_check(g_nccl.AllReduce(flags, flags, 1, ncclInt32, ncclMax, comm, stream), "AllReduce(flags)");
-}
+// one rank: the collectives are identities (the sequence code is shared with the NCCL path)
+struct LocalCollectives : fkk::Collectives {
+  fkk_plan* p;
+  explicit LocalCollectives(fkk_plan* pl) : p(pl) {}
+  void allgather_host(const void* send, void* recv, size_t bytes) override { std::memcpy(recv, send, bytes); }
+  void allreduce_sum_f64(double*, size_t) override {}
+  void allreduce_max_i32(int*, size_t) override {}
+  void sync() override { FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream)); }
+};
+
+// NCCL over the plan's communicator, enqueued on the plan stream.  Control data is staged through a
+// device scratch buffer sized at plan creation (no per-call allocation).  sync() polls the stream and
+// ncclCommGetAsyncError against a deadline (FKK_NCCL_TIMEOUT_S, default 600 s): a peer that failed
+// before a collective leaves this rank waiting, and the deadline turns that into ncclCommAbort and
+// FKK_ERR_NCCL instead of a hang.
+struct NcclCollectives : fkk::Collectives {
+  fkk_plan* p;
+  explicit NcclCollectives(fkk_plan* pl) : p(pl) {
+    world = pl->d.world_size;
+    rank = pl->d.rank;
+  }
+  void allgather_host(const void* send, void* recv, size_t bytes) override {
+    if ((size_t)(world + 1) * bytes > p->xscratch_bytes) throw Status(FKK_ERR_STATE, "collective scratch too small");
+    unsigned char* mine = p->xscratch + (size_t)world * bytes;
+    FKK_CUDA_CHECK(cudaMemcpyAsync(mine, send, bytes, cudaMemcpyHostToDevice, p->stream));
+    nccl_check(g_nccl.AllGather(mine, p->xscratch, bytes, ncclInt8, p->comm, p->stream), "AllGather");
+    FKK_CUDA_CHECK(cudaMemcpyAsync(recv, p->xscratch, (size_t)world * bytes, cudaMemcpyDeviceToHost, p->stream));
+    sync();
+  }
+  void allreduce_sum_f64(double* d, size_t n) override {
+    nccl_check(g_nccl.AllReduce(d, d, n, ncclFloat64, ncclSum, p->comm, p->stream), "AllReduce(sum)");
+  }
+  void allreduce_max_i32(int* d, size_t n) override {
+    nccl_check(g_nccl.AllReduce(d, d, n, ncclInt32, ncclMax, p->comm, p->stream), "AllReduce(max)");
+  }
+  void sync() override {
+    static const double limit = getenv("FKK_NCCL_TIMEOUT_S") ? atof(getenv("FKK_NCCL_TIMEOUT_S")) : 600.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t e = cudaStreamQuery(p->stream);
+      if (e == cudaSuccess) return;
+      if (e != cudaErrorNotReady) FKK_CUDA_CHECK(e);
+      ncclResult_t ar = ncclSuccess;
+      if (p->comm && g_nccl.CommGetAsyncError(p->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        abort_comm();
+        throw Status(FKK_ERR_NCCL, std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(ar));
+      }
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > limit) {
+        abort_comm();
+        throw Status(FKK_ERR_NCCL, "collective not complete after " + std::to_string((int)limit) +
+                                       " s (a peer rank failed or diverged): communicator aborted");
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
+  void abort_comm() {
+    if (p->comm && g_nccl.CommAbort) g_nccl.CommAbort(p->comm);
+    p->comm = nullptr;
+  }
+};
+
+void fkk_plan::nccl_allreduce_flags() { coll->allreduce_max_i32(flags, 1); }
 void fkk_plan::check_flags_sync(bool collective) { check_flags_sync_impl(collective); }
 
 namespace {
@@ -289,6 +370,15 @@ void validate_desc(const fkk_plan_desc* d) {
   if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) throw Status(FKK_ERR_INVALID_ARG, "bad world_size/rank");
   if ((d->world_size > 1) != (d->nccl_id != nullptr)) throw Status(FKK_ERR_INVALID_ARG, "nccl_id must be given iff world_size > 1");
   if (d->loopback_shards < 0 || d->loopback_shards > 64) throw Status(FKK_ERR_INVALID_ARG, "loopback_shards must be in [0, 64]");
+  if (d->svd_mode != FKK_SVD_GRAM && d->svd_mode != FKK_SVD_RANGE_FINDER) throw Status(FKK_ERR_INVALID_ARG, "bad svd_mode");
+  if (d->svd_mode == FKK_SVD_RANGE_FINDER) {
+    if (d->rf_oversample < 0 || d->rf_power_iters < 0 || d->rf_power_iters > 16)
+      throw Status(FKK_ERR_INVALID_ARG, "range finder: oversample >= 0, 0 <= power_iters <= 16");
+    if (d->rank_k + d->rf_oversample > std::min(d->n_freq, 128))
+      throw Status(FKK_ERR_INVALID_ARG, "range finder: k + oversample must be <= min(M, 128)");
+    if (d->in_dtype != FKK_IN_F32 || d->gemm_impl != FKK_GEMM_3XTF32)
+      throw Status(FKK_ERR_NOT_IMPLEMENTED, "range finder: f32 cube on the tensor-core path");
+  }
 }
 
 void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
@@ -366,7 +456,9 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     FKK_CUDA_CHECK(cudaMemcpy(p->gtc_tile_of, tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
     if (mode <= 1) {
       p->apre_blocks = mode == 1 ? fkk::gram_pre2_image_blocks(M) : (M + 127) / 128;
-      p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, p->apre_blocks));
+      // the range finder appends Y (N x 128) as one more image block
+      const int extra = d->svd_mode == FKK_SVD_RANGE_FINDER ? 1 : 0;
+      p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, p->apre_blocks + extra));
     }
     p->gtc_part = dalloc<double>(p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
                                              : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
@@ -406,30 +498,57 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
   p->wimg = dalloc<float>(fkk::project_tc_wimg_floats(M, kp));
   p->eig_work = dalloc<double>(fkk::eig_workspace_doubles(M, k));
   p->lam_d = dalloc<double>(k);
+  if (d->svd_mode == FKK_SVD_RANGE_FINDER) {
+    if (!p->apre) throw Status(FKK_ERR_NOT_IMPLEMENTED, "range finder: needs the pre-split image Gram path");
+    const int l = k + d->rf_oversample;
+    p->rf_l = l;
+    const int nT = (M + 127) / 128;
+    std::vector<int2> tl;
+    for (int cb = 0; cb < nT; ++cb) tl.push_back(make_int2(cb, p->apre_blocks));
+    tl.push_back(make_int2(p->apre_blocks, p->apre_blocks));
+    p->rf_tiles = dalloc<int2>(tl.size());
+    FKK_CUDA_CHECK(cudaMemcpy(p->rf_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    p->rf_nsplit = fkk::gram_tc_splits(nT + 1, n);
+    p->rf_part = dalloc<double>((size_t)(nT + 1) * p->rf_nsplit * 128 * 128);
+    p->rf_omega = dalloc<double>((size_t)l * M);
+    std::vector<double> om((size_t)l * M);
+    fkk::rf_omega_host(d->rf_seed, M, l, om.data());
+    FKK_CUDA_CHECK(cudaMemcpy(p->rf_omega, om.data(), om.size() * sizeof(double), cudaMemcpyHostToDevice));
+    p->rf_wimg = dalloc<float>(fkk::project_tc_wimg_floats(M, 128));
+    p->rf_Y = dalloc<float>((size_t)n * 128);
+    p->rf_Z = dalloc<double>((size_t)l * M);
+    p->rf_Zq = dalloc<double>((size_t)l * M);
+    p->rf_Z2 = dalloc<double>((size_t)l * M);
+    p->rf_SY = dalloc<double>((size_t)l * l);
+    p->rf_S = dalloc<double>((size_t)l * l);
+    p->rf_T = dalloc<double>((size_t)l * l);
+    p->rf_U = dalloc<double>((size_t)l * k);
+    p->rf_lam = dalloc<double>(k);
+    p->rf_fallback = dalloc<int>(1);
+  }
   if (d->world_size > 1) {
     std::string e;
     if (!g_nccl.load(e)) throw Status(FKK_ERR_NCCL, e);
     ncclUniqueId id;
     std::memcpy(&id, d->nccl_id, sizeof(id));
     nccl_check(g_nccl.CommInitRank(&p->comm, d->world_size, id, d->rank), "CommInitRank");
+    // control collectives: row counts (8 B) and the per-shard column extremes (shards x k x 2 x 8 B)
+    const int shards = std::max(1, d->loopback_shards);
+    p->xscratch_bytes = (size_t)(d->world_size + 1) * std::max<size_t>(64, (size_t)shards * k * 2 * sizeof(int64_t));
+    p->xscratch = dalloc<unsigned char>(p->xscratch_bytes);
+    p->coll.reset(new NcclCollectives(p));
+  } else {
+    p->coll.reset(new LocalCollectives(p));
   }
 }
 
 struct Shard { int64_t row0, rows; };
 
-// Rows of all ranks (global row offset of this rank, global N): allgather of n_rows.
+// Rows of all ranks (global row offset of this rank, global N): step 1 of exchange.h.
 void exchange_rows(fkk_plan* p, int64_t n_rows, int64_t& row0, int64_t& n_global) {
-  if (p->d.world_size == 1) { row0 = 0; n_global = n_rows; return; }
-  int64_t* buf = dalloc<int64_t>(p->d.world_size + 1);
-  std::vector<int64_t> h(p->d.world_size);
-  FKK_CUDA_CHECK(cudaMemcpyAsync(buf + p->d.world_size, &n_rows, sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
-  nccl_check(g_nccl.AllGather(buf + p->d.world_size, buf, 1, ncclInt64, p->comm, p->stream), "AllGather(rows)");
-  FKK_CUDA_CHECK(cudaMemcpyAsync(h.data(), buf, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
-  FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
-  cudaFree(buf);
-  row0 = 0;
-  n_global = 0;
-  for (int r = 0; r < p->d.world_size; ++r) { if (r < p->d.rank) row0 += h[r]; n_global += h[r]; }
+  if (p->d.world_size > 1 && !p->comm)
+    throw Status(FKK_ERR_STATE, "the communicator was aborted by an earlier failure; recreate the plan");
+  fkk::exchange_rows(*p->coll, n_rows, &row0, &n_global);
 }
 
 void check_cube_args(fkk_plan* p, const void* cube, int64_t n_rows, const void* ref, const void* out) {
@@ -456,6 +575,64 @@ static void gram_from_image(fkk_plan* p, int64_t n_rows, int64_t nr, bool accumu
   }
 }
 
+// F2-F4 by the randomized range finder (Halko 2011 Alg. 4.4 + 5.1, as the oracle's
+// randomized_svd): Y = A Omega; q times {Z = A^T orth(Y); Y = A orth(Z)}; then with Q = orth(Y):
+// B = Q^T A = (A^T Q)^T, B B^T = U~ S^2 U~^T, V = B^T U~ S^-1.  orth(Y) is implicit: A^T Y and Y^T Y
+// come out of one image-Gram launch (Y as an extra image block), Y^T Y = R^T R, A^T Q = (A^T Y) R^-1.
+void rf_svd(fkk_plan* p, const float* cube, int64_t n_rows) {
+  cudaStream_t s = p->stream;
+  const int M = p->M, k = p->k, l = p->rf_l, nT = (M + 127) / 128;
+  const int64_t nq = (n_rows + 31) / 32;
+  unsigned char* yimg = p->apre + (size_t)p->apre_blocks * nq * 2 * 16640;
+  FKK_CUDA_CHECK(cudaMemsetAsync(p->rf_fallback, 0, sizeof(int), s));
+  // Y = A (D_f Omega)
+  fkk::launch_build_wimg(p->rf_omega, p->f64, nullptr, M, l, 128, p->rf_wimg, s);
+  fkk::launch_project_tc(cube, n_rows, M, p->rf_wimg, l, 128, p->rf_Y, p->ext_val, p->ext_idx, 0, 0, s, p->inv_ref,
+                         (float)p->d.ratio_floor);
+  const int q = p->d.rf_power_iters;
+  const int ns = std::min(p->rf_nsplit, fkk::gram_tc_splits(nT + 1, std::max<int64_t>(n_rows, 1)));
+  for (int it = 0; it <= q; ++it) {
+    // A^T Y (nT tiles) and Y^T Y (one tile) from the image, all-reduced over ranks
+    fkk::launch_logratio_pre(p->rf_Y, n_rows, 128, 1, p->inv_ref, 0.f, nullptr, yimg, p->flags, s, 1);
+    fkk::launch_gram_pre(p->apre, n_rows, p->rf_tiles, nT + 1, ns, p->rf_part, s);
+    fkk::launch_rf_reduce(p->rf_part, nT, ns, M, l, p->f64, p->rf_Z, p->rf_SY, s);
+    p->coll->allreduce_sum_f64(p->rf_Z, (size_t)l * M);
+    p->coll->allreduce_sum_f64(p->rf_SY, (size_t)l * l);
+    // Zq = A^T Q = (A^T Y) R^-1 with Y^T Y = R^T R
+    fkk::launch_chol_rinv(p->rf_SY, l, p->rf_T, p->rf_fallback, s);
+    fkk::launch_apply_rinv(p->rf_Z, M, l, p->rf_T, p->rf_Zq, s);
+    if (it == q) break;
+    // power iteration: Y = A (D_f orth(Zq)), orth by CholQR2
+    fkk::launch_gram_rows(p->rf_Zq, M, l, p->rf_S, s);
+    fkk::launch_chol_rinv(p->rf_S, l, p->rf_T, p->rf_fallback, s);
+    fkk::launch_apply_rinv(p->rf_Zq, M, l, p->rf_T, p->rf_Z2, s);
+    fkk::launch_gram_rows(p->rf_Z2, M, l, p->rf_S, s);
+    fkk::launch_chol_rinv(p->rf_S, l, p->rf_T, p->rf_fallback, s);
+    fkk::launch_apply_rinv(p->rf_Z2, M, l, p->rf_T, p->rf_Zq, s);
+    fkk::launch_build_wimg(p->rf_Zq, p->f64, nullptr, M, l, 128, p->rf_wimg, s);
+    fkk::launch_project_tc(cube, n_rows, M, p->rf_wimg, l, 128, p->rf_Y, p->ext_val, p->ext_idx, 0, 0, s, p->inv_ref,
+                           (float)p->d.ratio_floor);
+  }
+  p->mark("range_finder");
+  // B B^T = Zq^T Zq (l x l); its top-k eigenpairs; V = Zq U diag(1/sigma), sign rule
+  fkk::launch_gram_rows(p->rf_Zq, M, l, p->rf_S, s);
+  fkk::launch_eig_topk(p->rf_S, l, k, p->eig_work, p->rf_U, p->rf_lam, p->flags, s);
+  fkk::launch_rf_combine(p->rf_Zq, M, l, p->rf_U, p->rf_lam, k, p->V64, s);
+  FKK_CUDA_CHECK(cudaMemcpyAsync(p->lam_d, p->rf_lam, k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  std::vector<double> hl(k);
+  int hfb = 0;
+  FKK_CUDA_CHECK(cudaMemcpyAsync(hl.data(), p->rf_lam, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FKK_CUDA_CHECK(cudaMemcpyAsync(&hfb, p->rf_fallback, sizeof(int), cudaMemcpyDeviceToHost, s));
+  p->check_flags_sync(true);
+  if (hfb) throw Status(FKK_ERR_NUMERICAL, "range finder: CholQR met a numerically rank-deficient block (lower k + oversample)");
+  p->h_s.assign(k, 0.0);
+  for (int i = 0; i < k; ++i) {
+    if (!std::isfinite(hl[i])) throw Status(FKK_ERR_NUMERICAL, "range finder produced a non-finite singular value");
+    p->h_s[i] = std::sqrt(std::max(hl[i], 0.0));
+  }
+  p->mark("eig");
+}
+
 void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_iref, int64_t n_global) {
   cudaStream_t s = p->stream;
   const int M = p->M, k = p->k;
@@ -472,13 +649,17 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
   if (p->d.f_mode == FKK_F_EQ9) {
     FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
     fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);
-    if (p->d.world_size > 1) nccl_check(g_nccl.AllReduce(p->colsum, p->colsum, M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(colsum)");
+    p->coll->allreduce_sum_f64(p->colsum, M);
     fkk::launch_noise_scale_from_sums(p->colsum, M, 1.0 / (double)std::max<int64_t>(n_global, 1), p->d.f_alpha, p->d.f_sigma_g, p->f64, p->f32, s);
   } else {
     fkk::launch_fill(p->f64, 1.0, M, s);
     fkk::launch_fill_f(p->f32, 1.0f, M, s);
   }
   p->mark("logratio");
+  if (p->d.svd_mode == FKK_SVD_RANGE_FINDER) {
+    rf_svd(p, static_cast<const float*>(d_icars), n_rows);
+    return;
+  }
   // Gram: per (virtual) shard in rank order, fp64 partial sums
   const int shards = std::max(1, p->d.loopback_shards);
   for (int sh = 0; sh < shards; ++sh) {
@@ -503,8 +684,7 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
       fkk::launch_gram_reduce(p->gram_part, ns, M, p->G, sh > 0, s);
     }
   }
-  if (p->d.world_size > 1)
-    nccl_check(g_nccl.AllReduce(p->G, p->G, (size_t)M * M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(G)");
+  p->coll->allreduce_sum_f64(p->G, (size_t)M * M);
   if (p->d.f_mode == FKK_F_EQ9) fkk::launch_scale_gram(p->G, p->f64, M, s);
   p->mark("gram");
   // eig on the GPU (fp64): Householder tridiagonalisation, bisection, inverse iteration
@@ -532,7 +712,6 @@ void transform_rest(fkk_plan* p, const void* cube, int64_t n_rows, int64_t row0,
   const int shards = std::max(1, p->d.loopback_shards);
   std::vector<float> hv;
   std::vector<int64_t> hi;
-  const int nparts = shards * p->d.world_size;
   for (int sh = 0; sh < shards; ++sh) {
     int64_t r0, r1;
     fkk_shard_range(n_rows, shards, sh, &r0, &r1);
@@ -563,45 +742,24 @@ void transform_rest(fkk_plan* p, const void* cube, int64_t n_rows, int64_t row0,
   if (h_q_in) {
     q.assign(h_q_in, h_q_in + nq_in);
   } else {
-    // merge the per-shard (and per-rank) extremes into q (reading A12)
+    // merge the per-shard (and per-rank) extremes into q (reading A12; step 4 of exchange.h)
     const size_t per = (size_t)k * 2;
-    float* gv = p->ext_out_val;
-    int64_t* gi = p->ext_out_idx;
-    if (p->d.world_size > 1) {
-      // each rank contributes its `shards` blocks; gather them after the local ones
-      float* tv = dalloc<float>(per * shards * p->d.world_size);
-      int64_t* ti = dalloc<int64_t>(per * shards * p->d.world_size);
-      nccl_check(g_nccl.AllGather(p->ext_out_val, tv, per * shards, ncclFloat32, p->comm, s), "AllGather(ext val)");
-      nccl_check(g_nccl.AllGather(p->ext_out_idx, ti, per * shards, ncclInt64, p->comm, s), "AllGather(ext idx)");
-      hv.resize(per * nparts);
-      hi.resize(per * nparts);
-      FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), tv, hv.size() * 4, cudaMemcpyDeviceToHost, s));
-      FKK_CUDA_CHECK(cudaMemcpyAsync(hi.data(), ti, hi.size() * 8, cudaMemcpyDeviceToHost, s));
-      FKK_CUDA_CHECK(cudaStreamSynchronize(s));
-      cudaFree(tv);
-      cudaFree(ti);
-    } else {
-      hv.resize(per * nparts);
-      hi.resize(per * nparts);
-      FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), gv, hv.size() * 4, cudaMemcpyDeviceToHost, s));
-      FKK_CUDA_CHECK(cudaMemcpyAsync(hi.data(), gi, hi.size() * 8, cudaMemcpyDeviceToHost, s));
-      FKK_CUDA_CHECK(cudaStreamSynchronize(s));
-    }
-    q.resize(2 * k);
-    const int nq = fkk_merge_extremes(hv.data(), hi.data(), nparts, k, q.data());
-    q.resize(nq);
+    hv.resize(per * shards);
+    hi.resize(per * shards);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(hv.data(), p->ext_out_val, hv.size() * 4, cudaMemcpyDeviceToHost, s));
+    FKK_CUDA_CHECK(cudaMemcpyAsync(hi.data(), p->ext_out_idx, hi.size() * 8, cudaMemcpyDeviceToHost, s));
+    FKK_CUDA_CHECK(cudaStreamSynchronize(s));
+    q = fkk::exchange_extremes(*p->coll, hv.data(), hi.data(), shards, k);
   }
   const int nq = (int)q.size();
   if (nq < 1 || nq > p->nq_cap()) throw Status(FKK_ERR_INVALID_ARG, "q must have 1..2k entries");
   p->h_q = q;
   // X = US[q] (rows owned by this rank; others contribute zeros and are summed over ranks)
-  std::vector<int64_t> ql(nq);
-  for (int i = 0; i < nq; ++i) ql[i] = (q[i] >= row0 && q[i] < row0 + n_rows) ? q[i] - row0 : -1;
+  const std::vector<int64_t> ql = fkk::local_rows(q, row0, n_rows);   // step 5 of exchange.h
   FKK_CUDA_CHECK(cudaMemcpyAsync(p->q_dev, ql.data(), nq * sizeof(int64_t), cudaMemcpyHostToDevice, s));
   fkk::launch_gather_rows(p->US, k, kp, p->q_dev, nq, p->X, s);
-  FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // ql is a stack buffer
-  if (p->d.world_size > 1)
-    nccl_check(g_nccl.AllReduce(p->X, p->X, (size_t)nq * k, ncclFloat64, ncclSum, p->comm, s), "AllReduce(X)");
+  FKK_CUDA_CHECK(cudaStreamSynchronize(s));   // ql is a host vector
+  p->coll->allreduce_sum_f64(p->X, (size_t)nq * k);
   p->mark("select_q");
   // ---- basis (F6..F10), fp64
   fkk::launch_vt_over_f(p->V64, p->f64, M, k, p->Vt_f, s);
@@ -784,6 +942,10 @@ void fkk_plan_desc_init(fkk_plan_desc* d, int32_t n_freq, int32_t rank_k, int64_
   d->rank = 0;
   d->nccl_id = nullptr;
   d->loopback_shards = 0;
+  d->svd_mode = FKK_SVD_GRAM;
+  d->rf_oversample = 10;
+  d->rf_power_iters = 1;
+  d->rf_seed = 0;
 }
 
 fkk_status fkk_get_nccl_unique_id(uint8_t out[128]) {
@@ -892,7 +1054,7 @@ fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows,
     if (p->d.f_mode == FKK_F_EQ9) {
       FKK_CUDA_CHECK(cudaMemsetAsync(p->colsum, 0, M * sizeof(double), s));
       fkk::launch_colsum(d_icars, p->in_f64, n_rows, M, p->colsum, s);
-      if (p->d.world_size > 1) nccl_check(g_nccl.AllReduce(p->colsum, p->colsum, M, ncclFloat64, ncclSum, p->comm, s), "AllReduce(colsum)");
+      p->coll->allreduce_sum_f64(p->colsum, M);
       fkk::launch_noise_scale_from_sums(p->colsum, M, 1.0 / (double)std::max<int64_t>(ng, 1), p->d.f_alpha, p->d.f_sigma_g, p->f64, p->f32, s);
     } else {
       fkk::launch_fill(p->f64, 1.0, M, s);

@@ -144,6 +144,15 @@ void launch_assemble_B(const double* Vt_f, const double* HPhi, const double* Vse
 
 // ---- GPU eigensolver (k_eig.cu): top-k eigenpairs of the symmetric M x M fp64 G (device);
 // V: k vectors of length M (= M x k column-major), lam_out: k descending.
+void launch_gram_rows(const double* Z, int M, int k, double* S, cudaStream_t s);
+void launch_chol_rinv(const double* S, int k, double* T, int* fallback, cudaStream_t s);
+void launch_apply_rinv(const double* Z, int M, int k, const double* T, double* Zn, cudaStream_t s);
+// ---- randomized range finder (k_rf.cu)
+void rf_omega_host(uint64_t seed, int M, int l, double* omega_lxM);
+void launch_rf_reduce(const double* partials, int nT, int nsplit, int M, int l, const double* f, double* Zraw,
+                      double* SY, cudaStream_t s);
+void launch_rf_combine(const double* Zq, int M, int l, const double* U, const double* lam, int k, double* V,
+                       cudaStream_t s);
 size_t eig_workspace_doubles(int M, int k);
 // M >= 3; flags |= 8 if the re-orthogonalisation finds dependent vectors.  G is not modified.
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,

@@ -84,11 +84,6 @@ __device__ __forceinline__ void lane_get2(const double (&mine)[W], int src1, dou
 
 // segment of lane s: rows [seg_b(s), seg_b(s+1))
 __device__ __forceinline__ int seg_b(int s, int M, int P) { return (s * M) / P; }   // s*M < 2^31 (M <= 4096)
-__device__ __forceinline__ int seg_of(int col, int M, int P) {
-  int s = (col * P) / M;
-  if (s + 1 <= P && seg_b(s + 1, M, P) <= col) ++s;
-  return s;
-}
 
 // interior weights of a segment: one bit per interior row (bit r <-> segment row r; 1 <-> w = p) in
 // a 64-bit (T <= 64) or 128-bit register.  A pass visits the rows in elimination order (ascending or
@@ -125,9 +120,7 @@ struct RowLayout {
   static constexpr int OFF_RD = 8 * NL;
   static constexpr int OFF_G = 16 * NL;
   static constexpr int OFF_Y = 24 * NL;
-  // + 8 B: consecutive rows start 2 banks apart, so the coalesced-load scatter of y (32 consecutive
-  // channels = 32 consecutive rows of one segment) is 2-way instead of 32-way bank conflicted
-  static constexpr int BYTES = 24 * NL + (int)sizeof(TY) * NL + 8;
+  static constexpr int BYTES = 24 * NL + (int)sizeof(TY) * NL;
 };
 
 template <typename TY>
@@ -158,9 +151,13 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
   for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
     const TY* yr = y + row * (int64_t)M;
     __syncwarp();
-    for (int col = s; col < M; col += NL) {           // coalesced read, scatter to [t][lane]
-      const int sc = seg_of(col, M, P);
-      *reinterpret_cast<TY*>(shm + (col - seg_b(sc, M, P)) * RS + RL::OFF_Y + sc * (int)sizeof(TY)) = yr[col];
+    // lane s reads its own segment (L1 serves the strided lanes from the row's 32 cached lines); the
+    // [row][lane] shared stores are conflict-free (a coalesced read scattered by segment was 32-way
+    // bank conflicted: 32 consecutive channels are 32 rows of one lane)
+    if (act) {
+      const int len = e - b;
+      for (int t = 0; t < len; ++t)
+        *reinterpret_cast<TY*>(shm + t * RS + RL::OFF_Y + s * (int)sizeof(TY)) = yr[b + t];
     }
     __syncwarp();
     MT im = 0;                 // interior weights (bit 1 <-> p); w^0 = 1 is handled by it == 0
@@ -461,9 +458,9 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
     // ---------------- write z (interior from the last back-substitution, separators from the last solve)
     __syncwarp();
     TZ* zr = z + row * (int64_t)M;
-    for (int col = s; col < M; col += NL) {
-      const int sc = seg_of(col, M, P);
-      zr[col] = (TZ)*reinterpret_cast<const double*>(shm + (col - seg_b(sc, M, P)) * RS + RL::OFF_G + 8 * sc);
+    if (act) {
+      const int len = e - b;
+      for (int t = 0; t < len; ++t) zr[b + t] = (TZ)*reinterpret_cast<const double*>(shm + t * RS + RL::OFF_G + 8 * s);
     }
   }
   if (solves && s == 0) atomicAdd(solves, solves_local);

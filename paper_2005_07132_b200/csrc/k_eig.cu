@@ -1504,6 +1504,29 @@ __global__ void __launch_bounds__(1024) reorth_fallback_kernel(const int* __rest
 
 }  // namespace
 
+// CholQR building blocks for other stages (the range finder, k_rf.cu): S = Z Z^T of k vectors of
+// length M (row-major k x k), T = R^-1 of S = R^T R (fallback |= 1 on a pivot that lost > 8 digits),
+// Zn = Z R^-1 (column vectors of Z_mat, i.e. Zn[c] = sum_{b <= c} T[b][c] Z[b]).
+void launch_gram_rows(const double* Z, int M, int k, double* S, cudaStream_t s) {
+  const int npairs = k * (k + 1) / 2;
+  gram_rows_kernel<<<(npairs * 32 + 255) / 256, 256, 0, s>>>(Z, M, k, S);
+  check_launch("gram_rows");
+}
+void launch_chol_rinv(const double* S, int k, double* T, int* fallback, cudaStream_t s) {
+  const size_t csm = (2 * (size_t)k * k + 2 * k) * sizeof(double);
+  FKK_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+  chol_inv_kernel<<<1, 256, csm, s>>>(S, k, T, fallback);
+  check_launch("chol_rinv");
+}
+void launch_apply_rinv(const double* Z, int M, int k, const double* T, double* Zn, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int agrid = (int)std::min<int64_t>(((int64_t)M * k + 255) / 256, 4 * sms);
+  apply_rinv_kernel<<<agrid, 256, 0, s>>>(Z, M, k, T, Zn);
+  check_launch("apply_rinv");
+}
+
 size_t eig_workspace_doubles(int M, int k) {
   // d, e, tau (3M) + p / LL words (16M) + lam, tnorm (k+1) + Z, Z2, Z3 (3kM) + S, T (2k^2) + flag + A (M*M)
   return 19 * (size_t)M + (size_t)k + 1 + 3 * (size_t)k * M + 2 * (size_t)k * k + 18 + (size_t)M * M +

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256, 4) logratio_pre_kernel(const float* __res
     for (int e = 0; e < 4; ++e) x[e] = xn[e];
     load(it + gridDim.x);
     float4 ir = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (col < M) ir = *reinterpret_cast<const float4*>(inv_ref + col);
+    if (!raw && col < M) ir = *reinterpret_cast<const float4*>(inv_ref + col);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int64_t px = q * GKC + 4 * p4 + e;

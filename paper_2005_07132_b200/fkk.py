@@ -28,6 +28,7 @@ STATUS = {0: "FKK_OK", 1: "FKK_ERR_INVALID_ARG", 2: "FKK_ERR_NONFINITE_INPUT", 3
 PAD = {"reflect": 0, "zero": 1}
 GEMM = {"3xtf32": 0, "fp32_simt": 1}
 F_MODE = {"one": 0, "eq9": 1}
+SVD_MODE = {"gram": 0, "range_finder": 1}
 STAGES = {"G": 0, "S": 1, "V": 2, "US": 3, "Q": 4, "HV": 5, "PHI_ERR": 6, "PHI_PEC": 7, "V_SEC": 8, "B": 9,
           "LAMBDA": 10, "F": 11}
 
@@ -49,6 +50,8 @@ class PlanDesc(ctypes.Structure):
         ("ml_ridge_rel", ctypes.c_double), ("gemm_impl", ctypes.c_int32), ("out_layout", ctypes.c_int32),
         ("in_dtype", ctypes.c_int32), ("device", ctypes.c_int32), ("world_size", ctypes.c_int32),
         ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("loopback_shards", ctypes.c_int32),
+        ("svd_mode", ctypes.c_int32), ("rf_oversample", ctypes.c_int32), ("rf_power_iters", ctypes.c_int32),
+        ("rf_seed", ctypes.c_uint64),
     ]
 
 
@@ -79,6 +82,11 @@ _SIGS = {
     "fkk_stage_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float), _i32]),
     "fkk_last_launch_count": (_i64, [_vp]),
     "fkk_debug_als_solves": (_i64, [_vp]),
+    "fkk_range_finder_omega": (_i32, [ctypes.c_uint64, _i32, _i32, _dp]),
+    "fkk_exchange_selftest": (_i32, [_vp, _i64, _i32, _i32, _i32, _dp, ctypes.POINTER(ctypes.c_float),
+                                     ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_i32),
+                                     ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                     ctypes.POINTER(_i32), _dp]),
     "fkk_host_eig_topk": (_i32, [_dp, _i32, _i32, _dp, _dp]),
     "fkk_debug_tc_mma": (_i32, [_i32, _vp, _vp, _vp, _i32]),
     "fkk_debug_eig_topk": (_i32, [_vp, _i32, _i32, _vp, _vp]),
@@ -146,7 +154,8 @@ class Plan:
                  als_lambda: float = 1e4, als_p: float = 1e-3, als_iters: int = 10, sg_window: int = 0,
                  ridge_rel: float = 1e-3, ml_ridge_rel: float = 0.0, gemm: str | None = None,
                  imag_only: bool = False, in_dtype: str = "f32", device: int = 0, world_size: int = 1,
-                 rank: int = 0, nccl_id: bytes | None = None, loopback_shards: int = 0, timing: bool = False):
+                 rank: int = 0, nccl_id: bytes | None = None, loopback_shards: int = 0, timing: bool = False,
+                 svd: str = "gram", rf_oversample: int = 10, rf_power_iters: int = 1, rf_seed: int = 0):
         d = PlanDesc()
         _lib.fkk_plan_desc_init(ctypes.byref(d), n_freq, rank_k, max_rows)
         d.fft_len = fft_len
@@ -166,6 +175,8 @@ class Plan:
         self._nccl_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         d.nccl_id = ctypes.cast(self._nccl_buf, ctypes.c_void_p) if self._nccl_buf is not None else None
         d.loopback_shards = loopback_shards
+        d.svd_mode = SVD_MODE[svd]
+        d.rf_oversample, d.rf_power_iters, d.rf_seed = rf_oversample, rf_power_iters, rf_seed
         self.desc = d
         self.n_freq, self.rank_k, self.max_rows = n_freq, rank_k, max_rows
         self.imag_only = imag_only
@@ -398,6 +409,76 @@ def fkk_debug_tridiag(G):
 
 def fkk_debug_eig_path(M: int) -> int:
     return int(_lib.fkk_debug_eig_path(M))
+
+
+def fkk_range_finder_omega(seed: int, M: int, l: int) -> np.ndarray:
+    """The range finder's Gaussian test matrix Omega (M x l), generated by the library (host code)."""
+    out = np.zeros((M, l))
+    if _lib.fkk_range_finder_omega(seed, M, l, out.ctypes.data_as(_dp)) != 0:
+        raise FkkError(1, "bad arguments")
+    return out
+
+
+_ALLGATHER = ctypes.CFUNCTYPE(_i32, _vp, _vp, _vp, ctypes.c_size_t)
+_ALLRED_F64 = ctypes.CFUNCTYPE(_i32, _vp, _dp, ctypes.c_size_t)
+_ALLRED_I32 = ctypes.CFUNCTYPE(_i32, _vp, ctypes.POINTER(_i32), ctypes.c_size_t)
+
+
+class HostCollectives(ctypes.Structure):
+    _fields_ = [("ctx", _vp), ("world_size", _i32), ("rank", _i32), ("allgather", _ALLGATHER),
+                ("allreduce_sum_f64", _ALLRED_F64), ("allreduce_max_i32", _ALLRED_I32)]
+
+
+def fkk_exchange_selftest(world: int, rank: int, allgather, allreduce_sum, allreduce_max, n_rows: int, M: int, k: int,
+                          shards: int, G: np.ndarray, ext_val: np.ndarray, ext_idx: np.ndarray, US_local: np.ndarray,
+                          flags: int):
+    """Run the sharded transform's exchange sequence (the library's C++ code) on host data through the
+    given collectives (python callables on numpy arrays: allgather(send_bytes) -> world x bytes,
+    allreduce_sum(float64 array) in place, allreduce_max(int32 array) in place)."""
+    def ag(ctx, send, recv, nbytes):
+        try:
+            src = np.ctypeslib.as_array(ctypes.cast(send, ctypes.POINTER(ctypes.c_uint8)), (nbytes,)).copy()
+            out = allgather(src)
+            ctypes.memmove(recv, out.ctypes.data, out.nbytes)
+            return 0
+        except Exception:
+            return 1
+
+    def ars(ctx, data, n):
+        try:
+            a = np.ctypeslib.as_array(data, (n,))
+            a[:] = allreduce_sum(a.copy())
+            return 0
+        except Exception:
+            return 1
+
+    def arm(ctx, data, n):
+        try:
+            a = np.ctypeslib.as_array(data, (n,))
+            a[:] = allreduce_max(a.copy())
+            return 0
+        except Exception:
+            return 1
+
+    cb = (_ALLGATHER(ag), _ALLRED_F64(ars), _ALLRED_I32(arm))
+    hc = HostCollectives(None, world, rank, *cb)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    ev = np.ascontiguousarray(ext_val, dtype=np.float32)
+    ei = np.ascontiguousarray(ext_idx, dtype=np.int64)
+    us = np.ascontiguousarray(US_local, dtype=np.float32)
+    fl = _i32(flags)
+    row0, ng, nq = _i64(), _i64(), _i32()
+    q = np.zeros(2 * k, dtype=np.int64)
+    X = np.zeros((2 * k, k))
+    st = _lib.fkk_exchange_selftest(ctypes.byref(hc), n_rows, M, k, shards, G.ctypes.data_as(_dp),
+                                    ev.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                    ei.ctypes.data_as(ctypes.POINTER(_i64)),
+                                    us.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), ctypes.byref(fl),
+                                    ctypes.byref(row0), ctypes.byref(ng), q.ctypes.data_as(ctypes.POINTER(_i64)),
+                                    ctypes.byref(nq), X.ctypes.data_as(_dp))
+    if st != FKK_OK:
+        raise FkkError(st, "exchange self-test failed")
+    return dict(row0=row0.value, n_global=ng.value, G=G, q=q[:nq.value], X=X[:nq.value], flags=fl.value)
 
 
 def fkk_get_nccl_unique_id() -> bytes:

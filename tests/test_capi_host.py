@@ -89,7 +89,9 @@ def test_merge_extremes_ties_and_union():
     assert list(q) == [1, 3, 9]
 
 
-def _gloo_worker(rank, world, port, q_out):
+def _gloo_worker(rank, world, port, q_out, nan_rank):
+    """One rank of the sharded transform's exchange sequence, run by the LIBRARY (fkk_exchange_selftest:
+    the same C++ sequence functions the NCCL path calls) over gloo collectives on CPU."""
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -100,26 +102,50 @@ def _gloo_worker(rank, world, port, q_out):
     cfg = CONFIGS["cfg1"]
     I, Iref, _ = generate(cfg)
     A = O.log_ratio(I, Iref, O.Params())
-    r0, r1 = fkk.fkk_shard_range(A.shape[0], world, rank)
-    # the exchange steps of the sharded path: all-reduce of the Gram partials ...
-    G = torch.from_numpy(A[r0:r1].T @ A[r0:r1])
-    dist.all_reduce(G)
-    V, lam = fkk.fkk_host_eig_topk(G.numpy(), cfg.rank_k)
-    # ... and all-gather of the per-column (value, global index) extremes
-    US = A[r0:r1] @ V
-    vals = np.stack([US.max(0), US.min(0)], axis=1).astype(np.float32)
-    idx = np.stack([US.argmax(0), US.argmin(0)], axis=1).astype(np.int64) + r0
-    tv = [torch.zeros(cfg.rank_k, 2) for _ in range(world)]
-    ti = [torch.zeros(cfg.rank_k, 2, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(tv, torch.from_numpy(vals))
-    dist.all_gather(ti, torch.from_numpy(idx))
-    q = fkk.fkk_merge_extremes(np.stack([t.numpy() for t in tv]), np.stack([t.numpy() for t in ti]), cfg.rank_k)
+    k = cfg.rank_k
+    # uneven shards: rank r owns a contiguous block of 1000 + 1000 r rows (the global offsets come from
+    # the library's row-count allgather, not from here)
+    sizes = [1000 + 1000 * r for r in range(world)]
+    r0 = sum(sizes[:rank])
+    Al = A[r0:r0 + sizes[rank]]
+
+    def allgather(b):
+        out = [torch.zeros(b.size, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(out, torch.from_numpy(b))
+        return np.concatenate([o.numpy() for o in out])
+
+    def allreduce_sum(a):
+        t = torch.from_numpy(a)
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def allreduce_max(a):
+        t = torch.from_numpy(a)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.numpy()
+
+    # local inputs of the exchange: the Gram partial, and (after the eig of the global G, which every
+    # rank computes identically) the local projection's column extremes with GLOBAL indices
+    Gl = Al.T @ Al
+    Gtot = torch.from_numpy(Gl.copy())
+    dist.all_reduce(Gtot)
+    V, lam = fkk.fkk_host_eig_topk(Gtot.numpy(), k)
+    US = (Al @ V).astype(np.float32)
+    vals = np.stack([US.max(0), US.min(0)], axis=1)[None]
+    idx = (np.stack([US.argmax(0), US.argmin(0)], axis=1) + r0)[None]
+    flags = 2 if rank == nan_rank else 0      # a non-finite value seen by one rank only
+    res = fkk.fkk_exchange_selftest(world, rank, allgather, allreduce_sum, allreduce_max, Al.shape[0], A.shape[1], k,
+                                    1, Gl, vals, idx, US, flags)
     if rank == 0:
-        q_out.put((q, G.numpy(), V))
+        q_out.put((res, V))
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sharded_q_matches_single_process():
+def test_two_rank_gloo_library_exchange_sequence():
+    """The pixel-sharded exchange through the library's own sequence code on 2 gloo
+    ranks with uneven shards: row offsets / global N from the row-count allgather, the all-reduced
+    Gram equals the single-process Gram, q from the merged extremes equals the oracle's select_q, X =
+    US[q] is the global one, and an error flag raised on ONE rank reaches every rank."""
     import multiprocessing as mp
     import socket
     with socket.socket() as s:
@@ -127,19 +153,24 @@ def test_two_rank_gloo_sharded_q_matches_single_process():
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     qq = ctx.Queue()
-    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, qq)) for r in range(2)]
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, qq, 1)) for r in range(2)]
     for p in ps:
         p.start()
-    q, G, V = qq.get(timeout=300)
+    res, V = qq.get(timeout=300)
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
     from synth import CONFIGS, generate
     cfg = CONFIGS["cfg1"]
     I, Iref, _ = generate(cfg)
-    A = O.log_ratio(I, Iref, O.Params())
-    assert np.max(np.abs(G - A.T @ A)) / np.max(np.abs(G)) < 1e-13
-    assert list(q) == list(O.select_q(A @ V))
+    A = O.log_ratio(I, Iref, O.Params())[:3000]
+    assert res["row0"] == 0 and res["n_global"] == 3000
+    assert np.max(np.abs(res["G"] - A.T @ A)) / np.max(np.abs(A.T @ A)) < 1e-13
+    US = A @ V
+    q = O.select_q(US.astype(np.float32))
+    assert list(res["q"]) == list(q)
+    assert np.max(np.abs(res["X"] - US.astype(np.float32)[q])) < 1e-6
+    assert res["flags"] == 2
 
 
 def test_library_has_no_undefined_internal_symbols():
@@ -154,3 +185,14 @@ def test_library_has_no_undefined_internal_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", b.LIB], capture_output=True, text=True).stdout
     bad = [ln for ln in out.splitlines() if ln.split()[0] == "U" and "fkk" in ln]
     assert not bad, bad
+
+
+def test_range_finder_test_matrix_matches_oracle_generator():
+    """The library's host generator of the range finder's Omega (SplitMix64 + Box-Muller) against the
+    oracle's independent implementation (oracle.range_finder_omega, pinned to SplitMix64's reference
+    vectors by P27): identical to the last bit or so (both fp64 libm)."""
+    fkk = _fkk()
+    M, l = 257, 13
+    out = fkk.fkk_range_finder_omega(11, M, l)
+    ref = O.range_finder_omega(11, M, l)
+    assert np.max(np.abs(out - ref)) <= 1e-14

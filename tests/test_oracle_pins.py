@@ -497,3 +497,77 @@ def test_P22_conventional_full_rank_equals_direct():
     K_conv = O.conventional_workflow(I, Iref, 64)
     K_dir = O.kk_direct(I, Iref)
     assert np.max(np.abs(K_conv - K_dir)) <= 1e-9 * np.max(np.abs(K_dir))
+
+
+# ------------------------------------------------------------------ randomized range finder (NEXT row 1)
+def test_P27_splitmix64_reference_vectors():
+    """The counter-based generator behind the range finder's test matrix against SplitMix64's published
+    outputs (tests/golden/paper_values.json)."""
+    g = GOLD["splitmix64_vectors"]
+    gamma = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        got = [int(O.splitmix64(np.uint64(1234567) + np.uint64(i) * gamma)) for i in range(5)]
+    assert got == g["seed_1234567_first5"]
+    assert int(O.splitmix64(np.uint64(0))) == g["seed_0_first"]
+    om = O.range_finder_omega(3, 1000, 70)            # Box-Muller Gaussians: moments of 70,000 draws
+    assert abs(om.mean()) < 0.02 and abs(om.std() - 1.0) < 0.02
+    assert np.array_equal(om, O.range_finder_omega(3, 1000, 70))
+    assert not np.array_equal(om, O.range_finder_omega(4, 1000, 70))
+
+
+def test_P28_randomized_svd_full_sampling_is_exact():
+    """l = M (the test matrix spans the whole row space): range(Q) = range(A), so the SVD of B = Q^T A is
+    the exact SVD of A (numpy.linalg.svd) whatever Omega and q are (Halko 2011, Alg. 4.1 + 5.1)."""
+    rng = np.random.default_rng(21)
+    A = rng.standard_normal((300, 40))
+    U, S, Vt = np.linalg.svd(A, full_matrices=False)
+    for q in (0, 1):
+        V, s = O.randomized_svd(A, 10, O.range_finder_omega(5, 40, 40), q)
+        assert np.max(np.abs(s - S[:10])) / S[0] < 1e-12
+        assert np.max(np.abs(np.abs(V.T @ Vt[:10].T) - np.eye(10))) < 1e-10
+
+
+def test_P29_randomized_svd_exact_on_low_rank():
+    """Exact rank r <= l: Y = A Omega spans range(A) with probability 1, so even q = 0 recovers the top-k
+    singular triplets exactly (Halko 2011, section 1.3)."""
+    rng = np.random.default_rng(22)
+    r = 9
+    A = rng.standard_normal((400, r)) @ np.diag(np.linspace(3, 1, r)) @ rng.standard_normal((r, 60))
+    S = np.linalg.svd(A, compute_uv=False)
+    V, s = O.randomized_svd(A, 6, O.range_finder_omega(6, 60, 12), 0)
+    assert np.max(np.abs(s - S[:6])) / S[0] < 1e-12
+    assert np.max(np.abs(A @ V @ V.T @ V - A @ V)) < 1e-10
+
+
+def test_P30_randomized_svd_error_decays_with_power_iterations():
+    """Geometric spectrum sigma_i = 0.7^i: the rank-k error ||A - A V_k V_k^T||_2 approaches the optimum
+    sigma_{k+1} (Eckart-Young) as q grows, and the singular values converge (Halko 2011, Cor. 10.10:
+    the excess error falls like (sigma_{k+1}/sigma_k)^(2q))."""
+    rng = np.random.default_rng(23)
+    n, m, k = 500, 40, 8
+    Qa = np.linalg.qr(rng.standard_normal((n, m)))[0]
+    Qb = np.linalg.qr(rng.standard_normal((m, m)))[0]
+    sig = 0.7 ** np.arange(m)
+    A = Qa @ np.diag(sig) @ Qb.T
+    errs, serr = [], []
+    for q in range(4):
+        V, s = O.randomized_svd(A, k, O.range_finder_omega(8, m, k + 4), q)
+        errs.append(np.linalg.norm(A - A @ V @ V.T, 2) / sig[k])
+        serr.append(np.max(np.abs(s - sig[:k])) / sig[0])
+    assert all(e >= 1 - 1e-12 for e in errs)
+    assert errs[0] > errs[1] > errs[2] - 1e-12 and errs[2] < 1 + 1e-6
+    assert serr[0] > 100 * serr[1] and serr[3] < 1e-11
+
+
+def test_P31_randomized_svd_stays_accurate_over_many_power_iterations():
+    """Orthonormalising between applications of A^T and A (Halko 2011, Alg. 4.4 vs 4.3): with q = 8 and
+    sigma_1 / sigma_k = 2^11, (A A^T)^q A Omega without re-orthonormalisation collapses onto the leading
+    direction in fp64 (dynamic range 2^176); with it the trailing kept singular values stay exact."""
+    rng = np.random.default_rng(24)
+    n, m, k = 400, 40, 12
+    Qa = np.linalg.qr(rng.standard_normal((n, m)))[0]
+    Qb = np.linalg.qr(rng.standard_normal((m, m)))[0]
+    sig = 0.5 ** np.arange(m)
+    A = Qa @ np.diag(sig) @ Qb.T
+    V, s = O.randomized_svd(A, k, O.range_finder_omega(9, m, k + 4), 8)
+    assert np.max(np.abs(s - sig[:k]) / sig[:k]) < 1e-8
