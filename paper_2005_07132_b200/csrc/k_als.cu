@@ -73,15 +73,6 @@ __device__ __forceinline__ double2 mulv(const M2& x, double2 v) {
   return make_double2(x.a * v.x + x.b * v.y, x.c * v.x + x.d * v.y);
 }
 
-template <int W>
-__device__ __forceinline__ void lane_get2(const double (&mine)[W], int src1, double (&out1)[W], int src2, double (&out2)[W]) {
-#pragma unroll
-  for (int i = 0; i < W; ++i) {
-    out1[i] = __shfl_sync(0xffffffffu, mine[i], src1 & 31);
-    out2[i] = __shfl_sync(0xffffffffu, mine[i], src2 & 31);
-  }
-}
-
 // segment of lane s: rows [seg_b(s), seg_b(s+1))
 __device__ __forceinline__ int seg_b(int s, int M, int P) { return (s * M) / P; }   // s*M < 2^31 (M <= 4096)
 
@@ -314,13 +305,14 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
       // ---------------- reduced block-tridiagonal system on the separators, lane s <-> S_s
       M2 nLL, nLR;
       double2 nCfL;
-      {   // from lane s + 1
-        const double mine[10] = {CLL.a, CLL.b, CLL.c, CLL.d, CLR.a, CLR.b, CLR.c, CLR.d, CfL.x, CfL.y};
-        double o[10], o2[10];
-        lane_get2<10>(mine, s + 1, o, s + 1, o2);
-        nLL = {o[0], o[1], o[2], o[3]};
-        nLR = {o[4], o[5], o[6], o[7]};
-        nCfL = make_double2(o[8], o[9]);
+      {   // from lane s + 1 (CLL is symmetric: 3 values)
+        const double mine[9] = {CLL.a, CLL.b, CLL.d, CLR.a, CLR.b, CLR.c, CLR.d, CfL.x, CfL.y};
+        double o[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) o[i] = __shfl_down_sync(0xffffffffu, mine[i], 1);
+        nLL = {o[0], o[1], o[1], o[2]};
+        nLR = {o[3], o[4], o[5], o[6]};
+        nCfL = make_double2(o[7], o[8]);
       }
       unsigned char* const sep0 = shm + nn * RS;        // rows e-2, e-1 (segment rows nn, nn+1)
       unsigned char* const sep1 = sep0 + RS;
@@ -339,58 +331,53 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         Uk = {-nLR.a, -nLR.b, -nLR.c, -nLR.d};
         rk = make_double2(w0 * ys0 - CfR.x - nCfL.x, w1 * ys1 - CfR.y - nCfL.y);
       }
-      M2 Lk;
-      {   // from lane s - 1
-        const double mine[4] = {Uk.a, Uk.b, Uk.c, Uk.d};
-        double o[4], o2[4];
-        lane_get2<4>(mine, s - 1, o, s - 1, o2);
-        Lk = {o[0], o[1], o[2], o[3]};
-      }
-      Lk = {Lk.a, Lk.c, Lk.b, Lk.d};   // transpose
-      if (s == 0 || !hasR) Lk = {0.0, 0.0, 0.0, 0.0};
+      // symmetric PCR (the separator system is SPD block tridiagonal, so L_s = U_{s-h}^T at every level):
+      // with Dinv = D^-1, A = Dinv U, b = Dinv r, a level of stride h is
+      //   D_s -= U_{s-h}^T A_{s-h} + U_s Dinv_{s+h} U_s^T,  r_s -= U_{s-h}^T b_{s-h} + U_s b_{s+h},
+      //   U_s <- -U_s A_{s+h}
+      // (14 doubles exchanged per level instead of 20 for the general form; D kept as (a, b, d))
+      double Da = Dk.a, Db = Dk.b, Dd = Dk.d;
 #pragma unroll
       for (int h = 1; h < NL; h <<= 1) {
-        const M2 Di = inv(Dk);
-        const M2 Pm = mul(Di, Lk), Qm = mul(Di, Uk);
-        const double2 sv = mulv(Di, rk);
-        M2 Pdn, Qdn, Pup, Qup;
-        double2 sdn, sup;
-        {   // from lanes s - h and s + h
-          const double mine[10] = {Pm.a, Pm.b, Pm.c, Pm.d, Qm.a, Qm.b, Qm.c, Qm.d, sv.x, sv.y};
-          double dn[10], up[10];
-          lane_get2<10>(mine, s - h, dn, s + h, up);
-          Pdn = {dn[0], dn[1], dn[2], dn[3]};
-          Qdn = {dn[4], dn[5], dn[6], dn[7]};
-          sdn = make_double2(dn[8], dn[9]);
-          Pup = {up[0], up[1], up[2], up[3]};
-          Qup = {up[4], up[5], up[6], up[7]};
-          sup = make_double2(up[8], up[9]);
+        const double idet = rcp64a(Da * Dd - Db * Db);
+        const double ia = Dd * idet, ib = -Db * idet, id = Da * idet;
+        const M2 A = {ia * Uk.a + ib * Uk.c, ia * Uk.b + ib * Uk.d, ib * Uk.a + id * Uk.c, ib * Uk.b + id * Uk.d};
+        const double2 bv = make_double2(ia * rk.x + ib * rk.y, ib * rk.x + id * rk.y);
+        const double caa = Uk.a * A.a + Uk.c * A.c, cab = Uk.a * A.b + Uk.c * A.d, cbb = Uk.b * A.b + Uk.d * A.d;
+        const double2 ev = make_double2(Uk.a * bv.x + Uk.c * bv.y, Uk.b * bv.x + Uk.d * bv.y);
+        double up[9], dn[5];
+        {
+          const double mu[9] = {ia, ib, id, bv.x, bv.y, A.a, A.b, A.c, A.d};
+          const double md[5] = {caa, cab, cbb, ev.x, ev.y};
+#pragma unroll
+          for (int i = 0; i < 9; ++i) up[i] = __shfl_down_sync(0xffffffffu, mu[i], h);
+#pragma unroll
+          for (int i = 0; i < 5; ++i) dn[i] = __shfl_up_sync(0xffffffffu, md[i], h);
         }
-        M2 nL = {0.0, 0.0, 0.0, 0.0}, nU = {0.0, 0.0, 0.0, 0.0};
         if (s - h >= 0) {
-          const M2 a1 = mul(Lk, Pdn), a2 = mul(Lk, Qdn);
-          const double2 a3 = mulv(Lk, sdn);
-          nL = {-a1.a, -a1.b, -a1.c, -a1.d};
-          Dk = {Dk.a - a2.a, Dk.b - a2.b, Dk.c - a2.c, Dk.d - a2.d};
-          rk = make_double2(rk.x - a3.x, rk.y - a3.y);
+          Da -= dn[0]; Db -= dn[1]; Dd -= dn[2];
+          rk = make_double2(rk.x - dn[3], rk.y - dn[4]);
         }
+        M2 nU = {0.0, 0.0, 0.0, 0.0};
         if (s + h < NL) {
-          const M2 b1 = mul(Uk, Qup), b2 = mul(Uk, Pup);
-          const double2 b3 = mulv(Uk, sup);
-          nU = {-b1.a, -b1.b, -b1.c, -b1.d};
-          Dk = {Dk.a - b2.a, Dk.b - b2.b, Dk.c - b2.c, Dk.d - b2.d};
-          rk = make_double2(rk.x - b3.x, rk.y - b3.y);
+          const double ja = up[0], jb = up[1], jd = up[2];
+          const M2 Tm = {Uk.a * ja + Uk.b * jb, Uk.a * jb + Uk.b * jd, Uk.c * ja + Uk.d * jb, Uk.c * jb + Uk.d * jd};
+          Da -= Tm.a * Uk.a + Tm.b * Uk.b;
+          Db -= Tm.a * Uk.c + Tm.b * Uk.d;
+          Dd -= Tm.c * Uk.c + Tm.d * Uk.d;
+          rk = make_double2(rk.x - (Uk.a * up[3] + Uk.b * up[4]), rk.y - (Uk.c * up[3] + Uk.d * up[4]));
+          nU = {-(Uk.a * up[5] + Uk.b * up[7]), -(Uk.a * up[6] + Uk.b * up[8]), -(Uk.c * up[5] + Uk.d * up[7]),
+                -(Uk.c * up[6] + Uk.d * up[8])};
         }
-        Lk = nL;
         Uk = nU;
       }
-      xR = hasR ? mulv(inv(Dk), rk) : make_double2(0.0, 0.0);
-      {   // from lane s - 1
-        const double mine[2] = {xR.x, xR.y};
-        double o[2], o2[2];
-        lane_get2<2>(mine, s - 1, o, s - 1, o2);
-        xL = make_double2(o[0], o[1]);
+      if (hasR) {
+        const double idet = rcp64a(Da * Dd - Db * Db);
+        xR = make_double2((Dd * rk.x - Db * rk.y) * idet, (Da * rk.y - Db * rk.x) * idet);
+      } else {
+        xR = make_double2(0.0, 0.0);
       }
+      xL = make_double2(__shfl_up_sync(0xffffffffu, xR.x, 1), __shfl_up_sync(0xffffffffu, xR.y, 1));   // from lane s - 1
       if (!hasL) xL = make_double2(0.0, 0.0);
       sep_flip = false;
       if (hasR) {   // separator values of this solve (the output if it is the last); weights for the next

@@ -207,18 +207,51 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
     });
     __syncthreads();
     // pointwise: a' = a + H{phi_err}, phi' = phi - phi_err, K' = exp(a') cis(phi'); chunk moments of Re K'
+    // (a full 8-channel f32 chunk moves as float4 pairs: the scalar loads were the largest stall)
     float kre[2][8], kim[2][8];
     double s[6] = {0, 0, 0, 0, 0, 0};
+    const bool vec = sizeof(TIn) == 4 && C == 8 && j0 + 8 <= M;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int j = j0 + c;
-      if (c < C && j < M) {
+    for (int r = 0; r < 2; ++r) {
+      const int64_t o = r ? o1 : o0;
+      float va[8], vh[8], vp[8];
+      if (vec) {
+        const float4* ip = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(I) + o + j0);
+        const float4* rp = reinterpret_cast<const float4*>(inv_ref + j0);
+        const float4* pp4 = reinterpret_cast<const float4*>(phi + o + j0);
+        const float4* ep4 = reinterpret_cast<const float4*>(phierr + o + j0);
+        const float4* hp4 = reinterpret_cast<const float4*>(hb + r * M + j0);
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int64_t o = r ? o1 : o0;
-          const float a = log_ratio_elem<TIn>(I[o + j], inv_ref[j], ref64[j], floor);
-          const float ap = a + hb[r * M + j];
-          const float pp = phi[o + j] - phierr[o + j];
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const float4 x = __ldcs(ip + h2), ir = rp[h2], f = __ldcs(pp4 + h2), e = __ldcs(ep4 + h2), hh = hp4[h2];
+          const float xs[4] = {x.x, x.y, x.z, x.w}, is[4] = {ir.x, ir.y, ir.z, ir.w};
+          const float fs[4] = {f.x, f.y, f.z, f.w}, es[4] = {e.x, e.y, e.z, e.w}, hs[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            va[4 * h2 + u] = 0.5f * __logf(fmaxf(xs[u] * is[u], floor));
+            vh[4 * h2 + u] = hs[u];
+            vp[4 * h2 + u] = fs[u] - es[u];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = j0 + c;
+          va[c] = vh[c] = vp[c] = 0.f;
+          if (c < C && j < M) {
+            va[c] = log_ratio_elem<TIn>(I[o + j], inv_ref[j], ref64[j], floor);
+            vh[c] = hb[r * M + j];
+            vp[c] = phi[o + j] - phierr[o + j];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int j = j0 + c;
+        kre[r][c] = kim[r][c] = 0.f;
+        if (c < C && j < M) {
+          const float ap = va[c] + vh[c];
+          const float pp = vp[c];
           // hardware sin/cos after a two-term reduction to [-pi, pi] and the hardware exp (reading A27)
           const float kq = __fsub_rn(__fadd_rn(pp * 0.15915494309189535f, 12582912.0f), 12582912.0f);
           const float rr = fmaf(kq, 1.7484556e-07f, fmaf(-kq, 6.2831854820251465f, pp));
@@ -336,13 +369,29 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       const int64_t o = r ? o1 : o0;
       const bool fb = (r ? gmin1 : gmin0) <= 0.0;
       const float imean = r ? im1 : im0;
+      float it[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int j = j0 + c;
-        if (c < C && j < M) {
-          const float it = fb ? imean : tr[r][c];
-          if (imag_only) reinterpret_cast<float*>(out)[o + j] = kim[r][c] * it;
-          else reinterpret_cast<float2*>(out)[o + j] = make_float2(kre[r][c] * it, kim[r][c] * it);
+      for (int c = 0; c < 8; ++c) it[c] = fb ? imean : tr[r][c];
+      if (C == 8 && j0 + 8 <= M) {   // 16-B stores (o + j0 is a multiple of 8 elements: M % 4 == 0, j0 = 8t)
+        if (imag_only) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o + j0);
+          __stcs(dst, make_float4(kim[r][0] * it[0], kim[r][1] * it[1], kim[r][2] * it[2], kim[r][3] * it[3]));
+          __stcs(dst + 1, make_float4(kim[r][4] * it[4], kim[r][5] * it[5], kim[r][6] * it[6], kim[r][7] * it[7]));
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float2*>(out) + o + j0);
+#pragma unroll
+          for (int h2 = 0; h2 < 4; ++h2)
+            __stcs(dst + h2, make_float4(kre[r][2 * h2] * it[2 * h2], kim[r][2 * h2] * it[2 * h2],
+                                         kre[r][2 * h2 + 1] * it[2 * h2 + 1], kim[r][2 * h2 + 1] * it[2 * h2 + 1]));
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = j0 + c;
+          if (c < C && j < M) {
+            if (imag_only) reinterpret_cast<float*>(out)[o + j] = kim[r][c] * it[c];
+            else reinterpret_cast<float2*>(out)[o + j] = make_float2(kre[r][c] * it[c], kim[r][c] * it[c]);
+          }
         }
       }
     }

@@ -236,3 +236,59 @@ def truth_imag(cfg: CubeConfig, rows: np.ndarray | None = None) -> np.ndarray:
 def lorentzian_spectrum(omega, centre, hwhm, amp, chi_nr=1.0):
     """chi = chi_nr + amp/(centre - omega - i hwhm): one complex Lorentzian."""
     return chi_nr + amp / (centre - omega - 1j * hwhm)
+
+
+# ------------------------------------------------------------------------------------------------
+# The paper's simulation workload (PAPER.md:194, Fig. 2; SURVEY 8(f) row 4).  Physics of the
+# measurement only (Eq. 1 with C_st = 1, PAPER.md:32): a noiseless 3-chemical mixture of complex
+# Lorentzian Raman spectra (22, 25, 10 peaks in 500-1700 cm^-1), real quadratic chi_nr per chemical
+# with non-negative coefficients, a real linear chi_ref surrogate, sampled over -500..2500 cm^-1.
+# Readings (DESIGN.md A30): 812 channels at the paper's spacing (810 samples, rounded up to a multiple
+# of 4 for the 16-B rows; omega_max = 2500 + 2 x 3000/809); the concentration map (Fig. 2(a), not in
+# the text) = three smooth random fields normalised per pixel to a ternary mixture; peak amplitudes
+# U(0.05, 0.5), HWHM U(4, 15) cm^-1; chi_nr,c = c0 + c1 x + c2 x^2, c ~ U(0.2, 1) (c0) / U(0, 1),
+# x = (omega + 500)/3000; chi_ref = a + b x, a ~ U(0.5, 1), b ~ U(0, 0.5).
+# ------------------------------------------------------------------------------------------------
+SIM_BASE = (74, 246)
+SIM_PEAKS = (22, 25, 10)
+SIM_M = 812
+
+
+def paper_sim_shape(scale: float) -> tuple[int, int]:
+    return int(round(SIM_BASE[0] * scale)), int(round(SIM_BASE[1] * scale))
+
+
+def paper_simulation(scale: float = 1.0, seed: int = 0):
+    """Returns (I [N x 812] f32, I_ref [812] f32, truth Im{chi/chi_nr} [N x 812] f64, omega [812])."""
+    H, W = paper_sim_shape(scale)
+    g = _rng(seed, _STREAM_INSTRUMENT, 7)
+    d = 3000.0 / 809.0
+    w = -500.0 + d * np.arange(SIM_M)
+    x = (w + 500.0) / 3000.0
+    chi_r = np.zeros((3, SIM_M), dtype=np.complex128)
+    for c, npk in enumerate(SIM_PEAKS):
+        cen = g.uniform(500.0, 1700.0, npk)
+        wid = g.uniform(4.0, 15.0, npk)
+        amp = g.uniform(0.05, 0.5, npk)
+        chi_r[c] = np.sum((amp * wid)[:, None] / (cen[:, None] - w[None, :] - 1j * wid[:, None]), axis=0)
+    co = np.stack([g.uniform(0.2, 1.0, 3), g.uniform(0.0, 1.0, 3), g.uniform(0.0, 1.0, 3)], axis=1)
+    chi_nr = co[:, 0:1] + co[:, 1:2] * x[None, :] + co[:, 2:3] * x[None, :] ** 2      # 3 x M, real > 0
+    a, b = g.uniform(0.5, 1.0), g.uniform(0.0, 0.5)
+    chi_ref = a + b * x
+    # concentration map: three smooth fields on the unit square (the same map at every scale)
+    gf = _rng(seed, _STREAM_FIELDS, 7)
+    yy = (np.arange(H) + 0.5)[:, None] / H
+    xx = (np.arange(W) + 0.5)[None, :] / W
+    fields = np.empty((3, H * W))
+    for c in range(3):
+        fld = np.zeros((H, W))
+        for _ in range(3):
+            cy, cx, s = gf.uniform(0, 1), gf.uniform(0, 1), gf.uniform(0.1, 0.35)
+            fld += np.exp(-((yy - cy) ** 2 + ((xx - cx) * W / H / 3.0) ** 2) / (2 * s * s))
+        fields[c] = fld.ravel() + 0.05
+    conc = (fields / fields.sum(axis=0, keepdims=True)).T                               # N x 3, sums to 1
+    chi = conc @ (chi_r + chi_nr)                                                        # N x M
+    nr = conc @ chi_nr                                                                   # N x M, real
+    I = np.abs(chi) ** 2
+    truth = (chi / nr).imag
+    return I.astype(np.float32), (chi_ref ** 2).astype(np.float32), truth, w

@@ -282,3 +282,31 @@ def test_range_finder_parity(torch_cuda, fkk, q):
     assert np.array_equal(plan.stage("Q"), out["q"])
     im_err = np.max(np.abs(K.imag - out["K"].imag)) / np.max(np.abs(out["K"].imag))
     assert im_err <= 1e-3, im_err
+
+
+# ------------------------------------------------------------------------ paper simulation (NEXT 4) -
+def test_paper_simulation_workload_parity_and_rss(torch_cuda, fkk):
+    """The paper's simulated 3-chemical image (Fig. 2; synth.paper_simulation, reading A30)
+    at scale 0.5 (37 x 123 = 4,551 spectra x 812 channels): the GPU fKK-EC (k = 40, within the paper's
+    35-50) against the oracle (q, Im K <= 1e-3), the conventional workflow (k = 6, the paper's count)
+    against the oracle on sampled rows, and Fig. 2(e)'s claim: both well below the Null RSS and close
+    to each other."""
+    from synth.cars import paper_simulation
+    I, Iref, truth, _ = paper_simulation(0.5)
+    I64, R64 = I.astype(np.float64), Iref.astype(np.float64)
+    p = O.Params()
+    plan = fkk.Plan(I.shape[1], 40, I.shape[0])
+    Id, Rd = _dev(torch_cuda, I), _dev(torch_cuda, Iref)
+    K = plan.transform(Id, Rd).cpu().numpy()
+    out = O.fkk_ec(I64, R64, 40, p)
+    assert np.array_equal(plan.stage("Q"), out["q"])
+    assert np.max(np.abs(K.imag - out["K"].imag)) / np.max(np.abs(out["K"].imag)) <= 1e-3
+    Kc = plan.conventional(Id, Rd, 6).cpu().numpy()
+    rows = np.arange(0, I.shape[0], 23)
+    Kc_or = O.kk_direct(O.svd_denoise(I64, 6)[rows], R64, p)
+    assert np.max(np.abs(Kc[rows] - Kc_or)) / np.max(np.abs(Kc_or)) <= 1e-3
+    null = O.rss(np.zeros_like(K), truth).mean()
+    r_f, r_c = O.rss(K, truth).mean(), O.rss(Kc, truth).mean()
+    print(f"paper sim x0.5: <RSS> fKK-EC {r_f:.3f}, conventional {r_c:.3f}, null {null:.3f}")
+    assert r_f < 0.1 * null and r_c < 0.1 * null
+    assert abs(r_f - r_c) < 0.5 * max(r_f, r_c)

@@ -1,0 +1,100 @@
+"""The paper's simulation workload (Fig. 2(d)-(e)) on one B200:
+for the side-scaled sizes 0.5, 1, 2, 3, 4 (4,551 ... 291,264 spectra x 812 channels, synth.paper_simulation)
+run the factorized fKK-EC (k = 40; the paper kept 35-50), ML:fKK-EC (trained on the first 20% of the
+pixels, applied to all), the conventional workflow (SVD denoise to k = 6, the paper's count, then KK +
+PEC + SEC per spectrum) and the direct KK (no denoise); report per size the mean +- std of 3 timed runs
+(CUDA events), the speed-up of each factorized method over the conventional one (Fig. 2(d)), and the
+mean RSS against the known Im{chi/chi_nr} with the Null RSS (Fig. 2(e)).  The oracle's fKK-EC on the
+host cores is timed at the smallest size for context.
+
+    python tools/paper_sim.py [out.json]
+"""
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2005_07132_b200 import fkk  # noqa: E402
+from synth.cars import paper_sim_shape, paper_simulation  # noqa: E402
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.mean(ts), statistics.stdev(ts)
+
+
+def rss(K, truth):
+    return float(np.mean(np.sum((K.imag - truth) ** 2, axis=1)))
+
+
+def main():
+    out_path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "paper_sim.json")
+    res = []
+    for sc in (0.5, 1, 2, 3, 4):
+        I, Iref, truth, _ = paper_simulation(sc)
+        N, M = I.shape
+        Id, Rd = torch.from_numpy(I).cuda(), torch.from_numpy(Iref).cuda()
+        out = torch.empty((N, M), dtype=torch.complex64, device="cuda")
+        plan = fkk.Plan(M, 40, N)
+        t_f = timed(lambda: plan.transform(Id, Rd, out))
+        Kf = out.cpu().numpy()
+        ntr = max(40, N // 5)
+        ptr = fkk.Plan(M, 40, ntr)
+        _, basis = ptr.transform(Id[:ntr], Rd, return_basis=True)
+        pap = fkk.Plan(M, 40, N)
+
+        def ml_all():
+            ptr.transform(Id[:ntr], Rd)
+            pap.apply(basis, Id, out)
+        t_mlt = timed(ml_all)
+        t_ml = timed(lambda: pap.apply(basis, Id, out))
+        Kml = out.cpu().numpy()
+        pc = fkk.Plan(M, 6, N)
+        t_c = timed(lambda: pc.conventional(Id, Rd, 6, out))
+        Kc = out.cpu().numpy()
+        t_d = timed(lambda: pc.direct(Id, Rd, out))
+        Kd = out.cpu().numpy()
+        null = rss(np.zeros_like(Kf), truth)
+        row = {"scale": sc, "shape": paper_sim_shape(sc), "n_spectra": N, "n_freq": M,
+               "ms": {"fkk_ec": t_f, "ml_fkk_ec_plus_train": t_mlt, "ml_fkk_ec_minus_train": t_ml,
+                      "conventional": t_c, "direct": t_d},
+               "speedup_vs_conventional": {"fkk_ec": t_c[0] / t_f[0], "ml_plus_train": t_c[0] / t_mlt[0],
+                                           "ml_minus_train": t_c[0] / t_ml[0]},
+               "us_per_spectrum": {"fkk_ec": 1e3 * t_f[0] / N, "conventional": 1e3 * t_c[0] / N,
+                                   "ml_minus_train": 1e3 * t_ml[0] / N},
+               "mean_rss": {"fkk_ec": rss(Kf, truth), "ml_fkk_ec": rss(Kml, truth), "conventional": rss(Kc, truth),
+                            "direct_no_denoise": rss(Kd, truth), "null": null}}
+        print(json.dumps(row), flush=True)
+        res.append(row)
+        del plan, ptr, pap, pc, basis
+    # context: the fp64 oracle's fKK-EC on the host cores at the smallest size
+    from oracle import fkk_oracle as O
+    I, Iref, truth, _ = paper_simulation(0.5)
+    t0 = time.perf_counter()
+    O.fkk_ec(I.astype(np.float64), Iref.astype(np.float64), 40, O.Params())
+    oracle_s = time.perf_counter() - t0
+    doc = {"workload": "paper simulation (PAPER.md:194): 3-chemical noiseless mixture, 812 channels over -500..2507 cm^-1",
+           "k_factorized": 40, "k_conventional": 6, "ml_training_fraction": 0.2, "rows": res,
+           "oracle_fkk_ec_s_at_scale_0.5": oracle_s, "oracle_cores": len(os.sched_getaffinity(0))}
+    os.makedirs(os.path.dirname(out_path), exist_ok=True)
+    json.dump(doc, open(out_path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
