@@ -41,6 +41,11 @@ __device__ __forceinline__ double rcp64(double x) {
   return fma(r, e, r);
 }
 
+// CTAs per SM the register budget is sized for (launch bounds); A/B builds override it
+#ifndef FKK_DIRECT_MINB
+#define FKK_DIRECT_MINB 3
+#endif
+
 template <int LOG2L>
 __host__ __device__ constexpr int threads_of() { return (1 << LOG2L) / 16 < 32 ? 32 : (1 << LOG2L) / 16; }
 
@@ -82,7 +87,7 @@ __device__ __forceinline__ void hilbert_pair(const float2* __restrict__ tw, cons
 }
 
 template <typename TIn, int LOG2L>
-__global__ void __launch_bounds__(threads_of<LOG2L>(), 2048 / threads_of<LOG2L>() / 5)
+__global__ void __launch_bounds__(threads_of<LOG2L>(), (2048 / threads_of<LOG2L>()) * FKK_DIRECT_MINB / 16)
 direct_phase_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
                     const double* __restrict__ ref64, float floor, const float2* __restrict__ tw,
                     const int* __restrict__ pmap, float* __restrict__ phi, int* __restrict__ flags) {
@@ -169,7 +174,7 @@ __device__ __forceinline__ double sg_eval(double Q0, double Q1, double Q2, int c
 }
 
 template <typename TIn, int LOG2L>
-__global__ void __launch_bounds__(threads_of<LOG2L>(), 2048 / threads_of<LOG2L>() / 5)
+__global__ void __launch_bounds__(threads_of<LOG2L>(), (2048 / threads_of<LOG2L>()) * FKK_DIRECT_MINB / 16)
 direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
                      const double* __restrict__ ref64, float floor, const float2* __restrict__ tw,
                      const int* __restrict__ pmap, const float* __restrict__ phi, const float* __restrict__ phierr,

@@ -1,6 +1,7 @@
 """The paper's simulation workload (Fig. 2(d)-(e)) on one B200:
 for the side-scaled sizes 0.5, 1, 2, 3, 4 (4,551 ... 291,264 spectra x 812 channels, synth.paper_simulation)
-run the factorized fKK-EC (k = 40; the paper kept 35-50), ML:fKK-EC (trained on the first 20% of the
+run the factorized fKK-EC (k = 6: reading A30, the noiseless spectrum falls to sigma_7/sigma_1 = 3.6e-4,
+below what the fp32 path resolves; the paper kept 35-50 in fp64), ML:fKK-EC (trained on the first 20% of the
 pixels, applied to all), the conventional workflow (SVD denoise to k = 6, the paper's count, then KK +
 PEC + SEC per spectrum) and the direct KK (no denoise); report per size the mean +- std of 3 timed runs
 (CUDA events), the speed-up of each factorized method over the conventional one (Fig. 2(d)), and the
@@ -23,6 +24,9 @@ import torch  # noqa: E402
 
 from paper_2005_07132_b200 import fkk  # noqa: E402
 from synth.cars import paper_sim_shape, paper_simulation  # noqa: E402
+
+
+KF = 6
 
 
 def timed(fn, reps=3):
@@ -51,13 +55,13 @@ def main():
         N, M = I.shape
         Id, Rd = torch.from_numpy(I).cuda(), torch.from_numpy(Iref).cuda()
         out = torch.empty((N, M), dtype=torch.complex64, device="cuda")
-        plan = fkk.Plan(M, 40, N)
+        plan = fkk.Plan(M, KF, N)
         t_f = timed(lambda: plan.transform(Id, Rd, out))
         Kf = out.cpu().numpy()
-        ntr = max(40, N // 5)
-        ptr = fkk.Plan(M, 40, ntr)
+        ntr = max(KF, N // 5)
+        ptr = fkk.Plan(M, KF, ntr)
         _, basis = ptr.transform(Id[:ntr], Rd, return_basis=True)
-        pap = fkk.Plan(M, 40, N)
+        pap = fkk.Plan(M, KF, N)
 
         def ml_all():
             ptr.transform(Id[:ntr], Rd)
@@ -86,12 +90,22 @@ def main():
     # context: the fp64 oracle's fKK-EC on the host cores at the smallest size
     from oracle import fkk_oracle as O
     I, Iref, truth, _ = paper_simulation(0.5)
+    I64, R64 = I.astype(np.float64), Iref.astype(np.float64)
     t0 = time.perf_counter()
-    O.fkk_ec(I.astype(np.float64), Iref.astype(np.float64), 40, O.Params())
+    O.fkk_ec(I64, R64, KF, O.Params())
     oracle_s = time.perf_counter() - t0
+    # the oracle's conventional workflow: SVD denoise of the whole cube, KK+PEC+SEC on a 10% sample scaled
+    # up (the paper estimated its conventional time the same way)
+    t0 = time.perf_counter()
+    Ik = O.svd_denoise(I64, 6)
+    t_svd = time.perf_counter() - t0
+    sub = Ik[:: 10]
+    t0 = time.perf_counter()
+    O.kk_direct(sub, R64, O.Params())
+    oracle_conv_s = t_svd + (time.perf_counter() - t0) * I64.shape[0] / sub.shape[0]
     doc = {"workload": "paper simulation (PAPER.md:194): 3-chemical noiseless mixture, 812 channels over -500..2507 cm^-1",
-           "k_factorized": 40, "k_conventional": 6, "ml_training_fraction": 0.2, "rows": res,
-           "oracle_fkk_ec_s_at_scale_0.5": oracle_s, "oracle_cores": len(os.sched_getaffinity(0))}
+           "k_factorized": KF, "k_conventional": 6, "ml_training_fraction": 0.2, "rows": res,
+           "oracle_fkk_ec_s_at_scale_0.5": oracle_s, "oracle_conventional_s_at_scale_0.5": oracle_conv_s, "oracle_cores": len(os.sched_getaffinity(0))}
     os.makedirs(os.path.dirname(out_path), exist_ok=True)
     json.dump(doc, open(out_path, "w"), indent=1)
 
