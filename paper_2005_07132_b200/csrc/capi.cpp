@@ -17,6 +17,7 @@
 #include "../../include/fkk.h"
 #include "fkk_internal.h"
 #include "exchange.h"
+#include <nvtx3/nvToolsExt.h>
 #include <thread>
 
 using fkk::Status;
@@ -213,14 +214,25 @@ struct fkk_plan {
 
   int nq_cap() const { return 2 * k; }
 
+  // NVTX: one range per C-ABI call (its name) and one per stage, closed at the stage's mark, so an
+  // nsys/ncu timeline shows the paper's steps
+  int nvtx_depth = 0;
+  void nvtx_push(const char* name) { nvtxRangePushA(name); ++nvtx_depth; }
+  void nvtx_pop_all() { while (nvtx_depth > 0) { nvtxRangePop(); --nvtx_depth; } }
   void mark(const char* name) {
+    if (nvtx_depth > 1) { nvtxRangePop(); --nvtx_depth; }
+    nvtxMarkA(name);
+    if (nvtx_depth == 1) nvtx_push("stage");
     if (!timing) return;
     cudaEvent_t e;
     FKK_CUDA_CHECK(cudaEventCreate(&e));
     FKK_CUDA_CHECK(cudaEventRecord(e, stream));
     marks.emplace_back(name, e);
   }
-  void begin_call() {
+  void begin_call(const char* name = "fkk_call") {
+    nvtx_pop_all();
+    nvtx_push(name);
+    nvtx_push("stage");
     for (auto& m : marks) cudaEventDestroy(m.second);
     marks.clear();
     fkk::g_launches = 0;
@@ -228,6 +240,7 @@ struct fkk_plan {
     mark("start");
   }
   void end_call() {
+    nvtx_pop_all();
     launches = fkk::g_launches;
     t_names.clear();
     t_ms.clear();
@@ -840,8 +853,10 @@ fkk_status guarded(fkk_plan* p, F&& f) {
     f();
     return FKK_OK;
   } catch (const Status& e) {
+    p->nvtx_pop_all();
     return fail(p, e.code, e.what());
   } catch (const std::exception& e) {
+    p->nvtx_pop_all();
     return fail(p, FKK_ERR_STATE, e.what());
   }
 }
@@ -1003,7 +1018,7 @@ fkk_status fkk_svd(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void
   return guarded(p, [&] {
     check_cube_args(p, d_icars, n_rows, d_iref, d_V_out);
     if (!h_s_out) throw Status(FKK_ERR_INVALID_ARG, "h_s_out is NULL");
-    p->begin_call();
+    p->begin_call("fkk_svd");
     int64_t row0, ng;
     exchange_rows(p, n_rows, row0, ng);
     if (ng < p->k) throw Status(FKK_ERR_INVALID_ARG, "rank_k exceeds the global number of spectra");
@@ -1025,7 +1040,7 @@ fkk_status fkk_transform(fkk_plan_t p, const void* d_icars, int64_t n_rows, cons
   return guarded(p, [&] {
     check_cube_args(p, d_icars, n_rows, d_iref, d_out);
     if (basis_out) *basis_out = nullptr;
-    p->begin_call();
+    p->begin_call("fkk_transform");
     int64_t row0, ng;
     exchange_rows(p, n_rows, row0, ng);
     if (ng < p->k) throw Status(FKK_ERR_INVALID_ARG, "rank_k exceeds the global number of spectra");
@@ -1043,7 +1058,7 @@ fkk_status fkk_transform_from(fkk_plan_t p, const void* d_icars, int64_t n_rows,
   return guarded(p, [&] {
     check_cube_args(p, d_icars, n_rows, d_iref, d_out);
     if (!d_V || !h_s || !h_q || nq < 1 || nq > p->nq_cap()) throw Status(FKK_ERR_INVALID_ARG, "bad V/s/q");
-    p->begin_call();
+    p->begin_call("fkk_transform_from");
     int64_t row0, ng;
     exchange_rows(p, n_rows, row0, ng);
     cudaStream_t s = p->stream;
@@ -1077,7 +1092,7 @@ fkk_status fkk_apply_trained_basis(fkk_plan_t p, fkk_basis_t b, const void* d_ic
   return guarded(p, [&] {
     if (!b) throw Status(FKK_ERR_INVALID_ARG, "basis is NULL");
     check_cube_args(p, d_icars, n_rows, b->ref64, d_out);
-    p->begin_call();
+    p->begin_call("fkk_apply_trained_basis");
     apply_run(p, b, d_icars, n_rows, d_out);
     p->end_call();
   });
@@ -1086,7 +1101,7 @@ fkk_status fkk_apply_trained_basis(fkk_plan_t p, fkk_basis_t b, const void* d_ic
 fkk_status kk_direct_batch(fkk_plan_t p, const void* d_icars, int64_t n_rows, const void* d_iref, void* d_out) {
   return guarded(p, [&] {
     check_cube_args(p, d_icars, n_rows, d_iref, d_out);
-    p->begin_call();
+    p->begin_call("kk_direct_batch");
     direct_run(p, d_icars, n_rows, d_iref, d_out);
     p->end_call();
   });
@@ -1106,7 +1121,7 @@ fkk_status fkk_conventional(fkk_plan_t p, const void* d_icars, int64_t n_rows, c
       throw Status(FKK_ERR_NOT_IMPLEMENTED,
                    "conventional workflow: f32 input, tensor-core path (pre-split Gram, TMA projection), one rank");
     if (n_rows < 1) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be >= 1");
-    p->begin_call();
+    p->begin_call("fkk_conventional");
     cudaStream_t s = p->stream;
     const int M = p->M, k = p->k, kp = p->kp;
     fkk::launch_prep_ref(d_iref, p->in_f64, M, p->inv_ref, p->ref64, p->flags, s);
@@ -1211,7 +1226,7 @@ fkk_status fkk_apply_trained_basis_stream(fkk_plan_t p, fkk_basis_t b, const voi
     }
     if (p->stream_in_bytes < in_b || p->stream_out_bytes < out_b)
       throw Status(FKK_ERR_INVALID_ARG, "batch larger than the first streaming call's batch");
-    p->begin_call();
+    p->begin_call("fkk_apply_trained_basis_stream");
     const int64_t nb = (n_rows + batch - 1) / batch;
     std::vector<cudaEvent_t> ev(4 * std::max<int64_t>(nb, 1));
     for (auto& e : ev) FKK_CUDA_CHECK(cudaEventCreate(&e));
