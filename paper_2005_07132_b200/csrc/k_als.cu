@@ -3,20 +3,26 @@
 // stops early once a solve leaves every weight unchanged: the next system would be identical, so its
 // solution is the current one (the fp64 oracle always runs all `iters` solves).
 //
-// Warp-partitioned solver: ONE warp per spectrum, the M rows split into P <= 32 contiguous segments
-// (lane s owns rows [b_s, b_{s+1})).  The last two rows of every segment but the last are separators;
-// each lane eliminates the interior of its segment (LDL^T of a pentadiagonal block) while
-// forward-substituting the right-hand side and the two near spike columns, accumulating the Schur
-// complement C = Y^T D^-1 Y of its interior onto the adjacent separators.  The separators form a
-// block-tridiagonal system with 2 x 2 blocks, solved by parallel cyclic reduction across the lanes (5
-// shuffle rounds).  Pass B forward-substitutes the corrected interior right-hand side; the next
-// solve's pass A back-substitutes it while it factorises the next system in the opposite direction.
+// Warp-partitioned solver: ONE warp per spectrum, the M rows (extended to Mp = 32 T with zero-weight
+// rows, see als_geo) split into 32 segments of T rows (lane s owns rows [sT, sT+T)).  The last two rows
+// of every segment are separators; each lane eliminates the interior of its segment (LDL^T of a
+// pentadiagonal block) while forward-substituting the right-hand side and the two near spike columns,
+// accumulating the Schur complement C = Y^T D^-1 Y of its interior onto the adjacent separators.  The
+// separators form a block-tridiagonal system with 2 x 2 blocks, solved by parallel cyclic reduction
+// across the lanes (5 shuffle rounds).  Pass B forward-substitutes the corrected interior right-hand
+// side; the next solve's pass A back-substitutes it while it factorises the next system in the
+// opposite direction.  Equal segments make every row step warp-uniform, which the tensor-memory
+// accesses below require.
 //
-// On-chip layout (one warp = one spectrum, everything in shared memory or registers):
-//   row block t (t = row - b_s, the row inside the segment) = { l1[32], 1/D[32], g[32] (fp64),
-//   y[32] (input precision) }, lane s at column s: every access of a row is one base pointer plus
-//   compile-time field offsets, and consecutive rows are one fixed stride apart.
+// On-chip layout (one warp = one spectrum; one CTA per SM of up to 16 warps, up to four per TMEM lane
+// quadrant):
+//   tensor memory: the factor {l1, 1/D} (fp64) of interior row t of segment s at lane s of the warp's
+//   quadrant, columns 4t .. 4t+3 after the warp's column offset (T = 32: 120 columns per spectrum,
+//   four spectra per quadrant);
+//   shared memory: row block t = { g[32] (fp64), y[32] (input precision) }, lane s at column s;
 //   weights: one bit per row in a per-lane register mask (bit t = 1 <-> w = p).
+// Moving the factor to tensor memory halves the shared memory per spectrum (28 -> 12 KB at M = 1000),
+// so 16 instead of 7 spectra (warps) are resident per SM to hide the recurrences' latency.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -25,12 +31,14 @@
 #include <type_traits>
 
 #include "fkk_internal.h"
+#include "tc_common.cuh"
 
 namespace fkk {
 
 namespace {
 
 constexpr int NL = 32;   // lanes (segments) per spectrum
+constexpr int WPC_MAX = 16;   // warps (spectra) per CTA: up to four per TMEM lane quadrant
 
 __device__ __forceinline__ double rcp64a(double x) {
   double r;
@@ -73,9 +81,6 @@ __device__ __forceinline__ double2 mulv(const M2& x, double2 v) {
   return make_double2(x.a * v.x + x.b * v.y, x.c * v.x + x.d * v.y);
 }
 
-// segment of lane s: rows [seg_b(s), seg_b(s+1))
-__device__ __forceinline__ int seg_b(int s, int M, int P) { return (s * M) / P; }   // s*M < 2^31 (M <= 4096)
-
 // interior weights of a segment: one bit per interior row (bit r <-> segment row r; 1 <-> w = p) in
 // a 64-bit (T <= 64) or 128-bit register.  A pass visits the rows in elimination order (ascending or
 // descending); it reads and rebuilds the mask through "position order" words (bit t <-> t-th row
@@ -104,14 +109,30 @@ __device__ __forceinline__ MT mask_final(MT m, int nn, bool desc) {
   return desc ? mask_rev(m) : (MT)(m >> (MaskBits<MT>::N - nn));
 }
 
-// row block of the shared-memory state: l1 | 1/D | g (fp64 x 32 lanes) | y (TY x 32 lanes)
+// TMEM: the factor of interior row t (l1, 1/D as two fp64 = four 32-bit columns 4t .. 4t+3) in the
+// lane of its segment; one 32x32b access moves one row of all 32 segments.  The wait is tied to the
+// destination registers so that no use of them can be scheduled before it.
+__device__ __forceinline__ void tm_ld2(uint32_t ta, double& a, double& b) {
+  uint32_t r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(ta));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3));
+  a = __hiloint2double((int)r1, (int)r0);
+  b = __hiloint2double((int)r3, (int)r2);
+}
+__device__ __forceinline__ void tm_st2(uint32_t ta, double a, double b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta),
+               "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)), "r"(__double2hiint(b)));
+}
+__device__ __forceinline__ void tm_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// shared-memory row block (one per segment row t, all 32 lanes): g (fp64) | y (input precision)
 template <typename TY>
 struct RowLayout {
-  static constexpr int OFF_L1 = 0;
-  static constexpr int OFF_RD = 8 * NL;
-  static constexpr int OFF_G = 16 * NL;
-  static constexpr int OFF_Y = 24 * NL;
-  static constexpr int BYTES = 24 * NL + (int)sizeof(TY) * NL;
+  static constexpr int OFF_G = 0;
+  static constexpr int OFF_Y = 8 * NL;
+  static constexpr int BYTES = 8 * NL + (int)sizeof(TY) * NL;
 };
 
 template <typename TY>
@@ -123,33 +144,42 @@ __device__ __forceinline__ double& fld(unsigned char* rowp, int off, int s) {
 }
 
 template <typename TY, typename TZ, typename MT>
-__global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, int64_t n, int M, int P, int T, double lam,
-                                                     double p, int iters, TZ* __restrict__ z, int* __restrict__ solves) {
-  extern __shared__ __align__(16) unsigned char shm[];
+__global__ void __launch_bounds__(NL * WPC_MAX, 1)
+    als_seg_kernel(const TY* __restrict__ y, int64_t n, int M, int T, int P, uint32_t tcols, double lam, double p,
+                   int iters, TZ* __restrict__ z, int* __restrict__ solves) {
+  extern __shared__ __align__(16) unsigned char shm_all[];
+  __shared__ uint32_t tmem_base_s;
   using RL = RowLayout<TY>;
   constexpr int RS = RL::BYTES;
-  const int s = threadIdx.x;
+  const int warp = threadIdx.x >> 5, s = threadIdx.x & (NL - 1), wpc = blockDim.x >> 5;
+  if (warp == 0) tc::tmem_alloc(&tmem_base_s, tcols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  // lane quadrant warp % 4 (the warps a quadrant can address), columns 4 (T-2) (warp / 4) onwards
+  const uint32_t tbase = tmem_base_s + ((uint32_t)((warp & 3) * NL) << 16) + 4u * (uint32_t)(T - 2) * (uint32_t)(warp >> 2);
+  unsigned char* const shm = shm_all + (size_t)warp * T * RS;
+  const int Mp = P * T, nn = T - 2;         // every segment: interior rows 0 .. nn-1, separators nn, nn+1
   const bool act = s < P;
-  const int b = act ? seg_b(s, M, P) : M, e = act ? seg_b(s + 1, M, P) : M;
-  const bool hasL = act && s > 0, hasR = act && s < P - 1;
-  const int nn = act ? (e - b) - (hasR ? 2 : 0) : 0;   // interior rows b .. b+nn-1
-  // interiors touching rows 0, 1, M-2, M-1 (where D^T D's band differs) take the slow band lookup
-  const bool edge = act && (b <= 1 || b + nn >= M - 1);
+  const int b = s * T, e = b + T;
+  const bool hasL = act && s > 0, hasR = act;
+  const bool edge = s == 0;                 // rows 0 and 1 (D^T D's first band rows) are lane 0's t = 0, 1
+  // rows M .. Mp-1 (padding of the last segment; all rows of inactive lanes) carry weight 0
+  MT realm = 0;
+  for (int t = 0; t < nn; ++t)
+    if (b + t < M) realm |= (MT)1 << t;
+  const bool real0 = e - 2 < M, real1 = e - 1 < M;
   const double q = 1.0 - p;
   const double lam2 = lam * lam, lam6 = 6.0 * lam, lamm4 = -4.0 * lam;
   int solves_local = 0;
 
-  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+  for (int64_t row = (int64_t)blockIdx.x * wpc + warp; row < n; row += (int64_t)gridDim.x * wpc) {
     const TY* yr = y + row * (int64_t)M;
     __syncwarp();
-    // lane s reads its own segment (L1 serves the strided lanes from the row's 32 cached lines); the
-    // [row][lane] shared stores are conflict-free (a coalesced read scattered by segment was 32-way
-    // bank conflicted: 32 consecutive channels are 32 rows of one lane)
-    if (act) {
-      const int len = e - b;
-      for (int t = 0; t < len; ++t)
-        *reinterpret_cast<TY*>(shm + t * RS + RL::OFF_Y + s * (int)sizeof(TY)) = yr[b + t];
-    }
+    // lane s reads its own segment (L1 serves the strided lanes from the row's cached lines); the
+    // [row][lane] shared stores are conflict-free
+    for (int t = 0; t < T; ++t)
+      *reinterpret_cast<TY*>(shm + t * RS + RL::OFF_Y + s * (int)sizeof(TY)) = (b + t < M) ? yr[b + t] : (TY)0;
     __syncwarp();
     MT im = 0;                 // interior weights (bit 1 <-> p); w^0 = 1 is handled by it == 0
     bool ws0 = false, ws1 = false;   // separator weights (rows e-2, e-1)
@@ -161,9 +191,10 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
       const int i0 = dr ? b + nn - 1 : b, di = dr ? -1 : 1;
       const int r0 = dr ? nn - 1 : 0;         // segment row of the first eliminated row
       const int dstep = dr ? -RS : RS;
+      const uint32_t tstep = dr ? (uint32_t)-4 : 4u;
       const int na = dr ? e - 2 : b - 1;      // near-adjacent separator row
       const bool hasN = dr ? hasR : hasL, hasF = dr ? hasL : hasR;
-      const bool bsub = it > 0, fact = it < iters;
+      const bool fact = it < iters;
       // ---------------- pass A: back-substitution of the previous system (it > 0) and factorisation
       //                  + forward substitution of the next (it < iters), in elimination order
       double z1 = 0.0, z2 = 0.0;
@@ -171,29 +202,37 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
       double gf1 = 0.0, gf2 = 0.0, ga1 = 0.0, ga2 = 0.0, gb1 = 0.0, gb2 = 0.0;
       double Caa = 0.0, Cab = 0.0, Cbb = 0.0, Cfa = 0.0, Cfb = 0.0;
       bool iflip = false;
-      const double ea0 = hasN ? cpl(i0, na, M, lam) : 0.0, eb0 = hasN ? lam : 0.0, ea1 = hasN ? lam : 0.0;
+      const double ea0 = hasN ? cpl(i0, na, Mp, lam) : 0.0, eb0 = hasN ? lam : 0.0, ea1 = hasN ? lam : 0.0;
       using T_ = std::true_type;
       using F_ = std::false_type;
       auto passA = [&](auto bsub_c, auto fact_c) {
         constexpr bool BSUB = decltype(bsub_c)::value, FACT = decltype(fact_c)::value;
-        if (nn == 0) return;                      // lanes beyond the P segments
         unsigned char* rp = shm + r0 * RS;
+        uint32_t tc_ = tbase + 4u * (uint32_t)r0;
         int i = i0;
         // the next row's operands are loaded at the top of each step, before this row's stores
         double cy = ld_y<TY>(rp, s), cg = 0.0, cl1 = 0.0, crd = 0.0;
-        if constexpr (BSUB) { cg = fld(rp, RL::OFF_G, s); cl1 = fld(rp, RL::OFF_L1, s); crd = fld(rp, RL::OFF_RD, s); }
+        if constexpr (BSUB) {
+          cg = fld(rp, RL::OFF_G, s);
+          tm_ld2(tc_, cl1, crd);
+        }
         MT new_m = 0;
         // one row in elimination order; ea/eb = near-spike entries (t < 2); LASTROW: l1 = 0 and no
-        // prefetch; EDGE: this position may hold one of the rows 0, 1, M-2, M-1
+        // prefetch; EDGE: this position may hold row 0 or 1
         auto step = [&](auto last_c, auto edge_c, double ea, double eb) {
           constexpr bool LASTROW = decltype(last_c)::value, EDGE = decltype(edge_c)::value;
           const double yv = cy;
           const double g_old = cg, l1_old = cl1, rd_old = crd;
           unsigned char* const cur = rp;
+          const uint32_t ct = tc_;
           if constexpr (!LASTROW) {
             rp += dstep;
+            tc_ += tstep;
             cy = ld_y<TY>(rp, s);
-            if constexpr (BSUB) { cg = fld(rp, RL::OFF_G, s); cl1 = fld(rp, RL::OFF_L1, s); crd = fld(rp, RL::OFF_RD, s); }
+            if constexpr (BSUB) {
+              cg = fld(rp, RL::OFF_G, s);
+              tm_ld2(tc_, cl1, crd);
+            }
           }
           double wv = 1.0;
           if constexpr (BSUB) {
@@ -208,9 +247,12 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
             fld(cur, RL::OFF_G, s) = zv;          // kept: the output if this solve is the last
           }
           if constexpr (FACT) {
+            wv = i < M ? wv : 0.0;
             double ld0 = lam6, ld1 = lamm4;
             if constexpr (EDGE) {
-              if (edge) { ld0 = lam * d0v(i, M); ld1 = lam * d1v(dr ? i - 1 : i, M); }
+              const double e0 = lam * d0v(i, Mp), e1 = lam * d1v(dr ? i - 1 : i, Mp);
+              ld0 = edge ? e0 : ld0;
+              ld1 = edge ? e1 : ld1;
             }
             const double D = (wv + ld0) - L1m1 * L1m1 * Dm1 - lam2 * rDm2;
             const double rd = rcp64n1(D);
@@ -224,8 +266,7 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
             Cbb = fma(gb, ub, Cbb);
             Cfa = fma(gf, ua, Cfa);
             Cfb = fma(gf, ub, Cfb);
-            fld(cur, RL::OFF_L1, s) = l1n;
-            fld(cur, RL::OFF_RD, s) = rd;
+            tm_st2(ct, l1n, rd);
             Dm1 = D;
             rDm2 = rDm1;
             rDm1 = rd;
@@ -237,7 +278,7 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
           }
           i += di;
         };
-        step(F_{}, T_{}, ea0, eb0);               // t = 0   (nn >= 2 on active lanes)
+        step(F_{}, T_{}, ea0, eb0);               // t = 0   (nn >= 2)
         if (nn == 2) {
           step(T_{}, T_{}, ea1, 0.0);
         } else {
@@ -249,7 +290,7 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         }
         if constexpr (BSUB) {
           const MT nm = mask_final<MT>(new_m, nn, dr);
-          iflip = nm != im;
+          iflip = ((nm ^ im) & realm) != 0;
           im = nm;
         }
       };
@@ -270,7 +311,7 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         const int fa = dr ? b - 1 : e - 2;
         const double l1_nm2 = L1m2;                             // l1 of t = nn-2
         const double yfa0 = lam, yff0 = 0.0;                    // t = nn-2
-        const double yfa1 = cpl(r_last, fa, M, lam) - l1_nm2 * lam, yff1 = lam;   // t = nn-1
+        const double yfa1 = cpl(r_last, fa, Mp, lam) - l1_nm2 * lam, yff1 = lam;   // t = nn-1
 #pragma unroll
         for (int k2 = 0; k2 < 2; ++k2) {
           const double yfa = k2 ? yfa1 : yfa0, yff = k2 ? yff1 : yff0, rd = k2 ? rDm1 : rDm2;
@@ -305,11 +346,15 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
       // ---------------- reduced block-tridiagonal system on the separators, lane s <-> S_s
       M2 nLL, nLR;
       double2 nCfL;
-      {   // from lane s + 1 (CLL is symmetric: 3 values)
+      {   // from lane s + 1 (CLL is symmetric: 3 values); lanes beyond the P segments contribute zero
         const double mine[9] = {CLL.a, CLL.b, CLL.d, CLR.a, CLR.b, CLR.c, CLR.d, CfL.x, CfL.y};
         double o[9];
 #pragma unroll
-        for (int i = 0; i < 9; ++i) o[i] = __shfl_down_sync(0xffffffffu, mine[i], 1);
+        for (int i = 0; i < 9; ++i) o[i] = __shfl_down_sync(0xffffffffu, act ? mine[i] : 0.0, 1);
+        if (s + 1 >= P) {   // the last segment's separator couples to nothing on its right
+#pragma unroll
+          for (int i = 0; i < 9; ++i) o[i] = 0.0;
+        }
         nLL = {o[0], o[1], o[1], o[2]};
         nLR = {o[3], o[4], o[5], o[6]};
         nCfL = make_double2(o[7], o[8]);
@@ -323,11 +368,11 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         const int i0s = e - 2, i1s = e - 1;
         ys0 = ld_y<TY>(sep0, s);
         ys1 = ld_y<TY>(sep1, s);
-        const double w0 = it == 0 ? 1.0 : (ws0 ? p : q);
-        const double w1 = it == 0 ? 1.0 : (ws1 ? p : q);
-        const double off = lam * d1v(i0s, M);
-        Dk = {w0 + lam * d0v(i0s, M) - CRR.a - nLL.a, off - CRR.b - nLL.b, off - CRR.c - nLL.c,
-              w1 + lam * d0v(i1s, M) - CRR.d - nLL.d};
+        const double w0 = real0 ? (it == 0 ? 1.0 : (ws0 ? p : q)) : 0.0;
+        const double w1 = real1 ? (it == 0 ? 1.0 : (ws1 ? p : q)) : 0.0;
+        const double off = lam * d1v(i0s, Mp);
+        Dk = {w0 + lam * d0v(i0s, Mp) - CRR.a - nLL.a, off - CRR.b - nLL.b, off - CRR.c - nLL.c,
+              w1 + lam * d0v(i1s, Mp) - CRR.d - nLL.d};
         Uk = {-nLR.a, -nLR.b, -nLR.c, -nLR.d};
         rk = make_double2(w0 * ys0 - CfR.x - nCfL.x, w1 * ys1 - CfR.y - nCfL.y);
       }
@@ -384,35 +429,39 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         fld(sep0, RL::OFF_G, s) = xR.x;
         fld(sep1, RL::OFF_G, s) = xR.y;
         const bool w0n = ys0 > xR.x, w1n = ys1 > xR.y;
-        sep_flip = it == 0 || w0n != ws0 || w1n != ws1;
+        sep_flip = it == 0 || (real0 && w0n != ws0) || (real1 && w1n != ws1);
         ws0 = w0n;
         ws1 = w1n;
       }
+      tm_st_wait();   // this pass A's factor rows are in TMEM before pass B reads them
       // ---------------- pass B: forward substitution of the corrected interior right-hand side
       {
         const double x_na = dr ? xR.x : xL.y, x_nf = dr ? xR.y : xL.x;
         const double x_fa = dr ? xL.y : xR.x, x_ff = dr ? xL.x : xR.y;
         const int fa = dr ? b - 1 : e - 2;
         const int r_last = dr ? b : b + nn - 1;
-        const double c0 = cpl(i0, na, M, lam) * x_na + lam * x_nf, c1 = lam * x_na;
-        const double cL = cpl(r_last, fa, M, lam) * x_fa + lam * x_ff, cL2 = lam * x_fa;
+        const double c0 = cpl(i0, na, Mp, lam) * x_na + lam * x_nf, c1 = lam * x_na;
+        const double cL = cpl(r_last, fa, Mp, lam) * x_fa + lam * x_ff, cL2 = lam * x_fa;
         auto passB = [&](auto first_c) {
           constexpr bool FIRST = decltype(first_c)::value;
-          if (nn == 0) return;
           MT cur_m = mask_cursor<MT>(im, nn, dr);
           double g1 = 0.0, g2 = 0.0, l1prev = 0.0, rdm1 = 0.0, rdm2 = 0.0;
           unsigned char* rp = shm + r0 * RS;
-          double ny = ld_y<TY>(rp, s), nrd = fld(rp, RL::OFF_RD, s), nl1 = fld(rp, RL::OFF_L1, s);
+          uint32_t tc_ = tbase + 4u * (uint32_t)r0;
+          double ny = ld_y<TY>(rp, s), nrd, nl1;
+          tm_ld2(tc_, nl1, nrd);
           auto stepB = [&](auto last_c, double corr) {
             constexpr bool LASTROW = decltype(last_c)::value;
             const double wv = FIRST ? 1.0 : (mask_take<MT>(cur_m) ? p : q);
-            const double f = wv * ny - corr;
+            const double f = wv * ny - corr;      // padding rows: y = 0
             const double rd = nrd;
             const double l1c = nl1;
             unsigned char* const cur = rp;
             if constexpr (!LASTROW) {
               rp += dstep;
-              ny = ld_y<TY>(rp, s); nrd = fld(rp, RL::OFF_RD, s); nl1 = fld(rp, RL::OFF_L1, s);
+              tc_ += tstep;
+              ny = ld_y<TY>(rp, s);
+              tm_ld2(tc_, nl1, nrd);
             }
             const double g = f - l1prev * g1 - lam * rdm2 * g2;
             fld(cur, RL::OFF_G, s) = g * rd;
@@ -441,52 +490,73 @@ __global__ void __launch_bounds__(NL) als_seg_kernel(const TY* __restrict__ y, i
         else passB(F_{});
       }
     }
+    tm_st_wait();
     solves_local += it;   // solves 0 .. it-1 were completed
     // ---------------- write z (interior from the last back-substitution, separators from the last solve)
     __syncwarp();
     TZ* zr = z + row * (int64_t)M;
-    if (act) {
-      const int len = e - b;
-      for (int t = 0; t < len; ++t) zr[b + t] = (TZ)*reinterpret_cast<const double*>(shm + t * RS + RL::OFF_G + 8 * s);
-    }
+    for (int t = 0; t < T; ++t)
+      if (b + t < M) zr[b + t] = (TZ)*reinterpret_cast<const double*>(shm + t * RS + RL::OFF_G + 8 * s);
   }
   if (solves && s == 0) atomicAdd(solves, solves_local);
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem_base_s, tcols);
 }
 
+// segment geometry: T rows per segment (>= 4: two interior rows and the two separator rows), P =
+// ceil(M / T) <= 32 segments, system size Mp = P T >= M.  The rows M .. Mp-1 extend the last segment
+// with weight 0: with zero weight they are free, the second differences they enter vanish on the linear
+// extrapolation of z, so the first M rows of the extended minimiser are exactly the original one (DESIGN
+// reading A31); every segment then has the same shape and the warp runs one row schedule.
+// One CTA per SM (kernels that allocate tensor memory are not co-resident on B200: measured) holding
+// wpc = 4 x (spectra per quadrant) warps, bounded by 16 (128 registers per thread) and shared memory.
+struct Geo {
+  int T, P, wpc;
+  uint32_t cols;   // TMEM columns allocated: (wpc / 4) x 4 (T - 2), rounded up to a power of two
+};
 template <typename TY>
-size_t als_smem_bytes(int M) {
-  const int P = std::min(NL, M / 4);
-  const int T = (M + P - 1) / P;
-  return (size_t)T * RowLayout<TY>::BYTES;
+Geo als_geo(int M, size_t smem_max) {
+  Geo g;
+  g.T = std::max(4, (M + NL - 1) / NL);
+  g.P = (M + g.T - 1) / g.T;
+  const int per_q = std::max(0, std::min(WPC_MAX / 4, 512 / (4 * (g.T - 2))));
+  int wpc = 4 * per_q;
+  while (wpc > 4 && (size_t)wpc * g.T * RowLayout<TY>::BYTES > smem_max) wpc -= 4;
+  g.wpc = wpc;
+  g.cols = 32;
+  while (g.cols < 4u * (uint32_t)(g.T - 2) * (uint32_t)(wpc / 4)) g.cols <<= 1;
+  return g;
 }
 
 }  // namespace
 
 size_t als_part_smem(int M, int y_f64) {
-  if (M / 4 < 2) return 0;
-  return y_f64 ? als_smem_bytes<double>(M) : als_smem_bytes<float>(M);
+  if (M < 8) return 0;
+  const size_t cap = 227 * 1024;
+  if (y_f64) { const Geo g = als_geo<double>(M, cap); return (size_t)g.wpc * g.T * RowLayout<double>::BYTES; }
+  const Geo g = als_geo<float>(M, cap);
+  return (size_t)g.wpc * g.T * RowLayout<float>::BYTES;
 }
 
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
                      cudaStream_t s, int* solves) {
-  const int P = std::min(NL, M / 4);
-  if (P < 2 || n <= 0) return false;
-  const int T = (M + P - 1) / P;
-  if (T > 128) return false;
-  const size_t sm = als_part_smem(M, y_f64);
+  if (M < 8 || n <= 0) return false;
   int dev = 0, sms = 148, maxsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (sm > (size_t)maxsm) return false;
+  const size_t cap = (size_t)maxsm - 64;
+  const Geo g = y_f64 ? als_geo<double>(M, cap) : als_geo<float>(M, cap);
+  if (g.wpc < 4 || g.cols > 512) return false;
+  const size_t sm = (size_t)g.wpc * g.T * (y_f64 ? RowLayout<double>::BYTES : RowLayout<float>::BYTES);
+  if (sm > cap) return false;
+  const int64_t gr = std::min<int64_t>((n + g.wpc - 1) / g.wpc, sms);
 #define FKK_ALS_SEG(TY, TZ)                                                                           \
   {                                                                                                   \
-    auto kf = T <= 64 ? als_seg_kernel<TY, TZ, unsigned long long> : als_seg_kernel<TY, TZ, unsigned __int128>; \
+    auto kf = g.T - 2 <= 64 ? als_seg_kernel<TY, TZ, unsigned long long> : als_seg_kernel<TY, TZ, unsigned __int128>; \
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
-    int per = 1;                                                                                      \
-    FKK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kf, NL, sm));                  \
-    const int64_t g = std::min<int64_t>(n, (int64_t)sms * std::max(per, 1));                         \
-    kf<<<(unsigned)g, NL, sm, s>>>((const TY*)y, n, M, P, T, lam, p, iters, (TZ*)z, solves);          \
+    kf<<<(unsigned)gr, NL * g.wpc, sm, s>>>((const TY*)y, n, M, g.T, g.P, g.cols, lam, p, iters, (TZ*)z, solves); \
   }
   if (y_f64 && z_f64) FKK_ALS_SEG(double, double)
   else if (!y_f64 && !z_f64) FKK_ALS_SEG(float, float)

@@ -68,11 +68,13 @@ def test_direct_cfg2_sample_f32(torch_cuda, fkk):
     assert np.array_equal(Ki, K[:4096].imag)
 
 
-@pytest.mark.parametrize("M", [16, 100, 1600, 2048])
+@pytest.mark.parametrize("M", [16, 100, 132, 1020, 1600, 2048])
 def test_direct_segment_edge_sizes(torch_cuda, fkk, M):
-    """The warp-partitioned ALS splits M into min(32, M/4) segments: M = 16 (4 segments of 4 rows,
-    2-row interiors), 100 (25 segments), 1600 (32 segments of 50, the cfg4 channel count), 2048 (64-row
-    segments: the full 64-bit weight mask; L = 4096, the largest direct-path FFT)."""
+    """The warp-partitioned ALS splits M into P = ceil(M/T) segments of T = max(4, ceil(M/32)) rows and
+    extends the last one with zero-weight rows (reading A31): M = 16 (4 segments of 4 rows, 2-row
+    interiors), 100 (25 x 4, no padding), 132 (27 x 5, 3 padding rows), 1020 (32 x 32, 4 rows),
+    1600 (32 x 50, the cfg4 channel count), 2048 (64-row segments: 62-bit interior masks; L = 4096, the
+    largest direct-path FFT)."""
     cfg = CONFIGS["cfg1"].with_(height=4, width=9, n_freq=M)
     I, Iref, _ = generate(cfg)
     K_or = O.kk_direct(I, Iref, O.Params())
