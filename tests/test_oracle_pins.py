@@ -273,6 +273,30 @@ def test_P9_als_line_shift_and_dense():
                          O.als_baseline(y, O.Params(als_iters=2))[0])) > 1e-3
 
 
+@pytest.mark.parametrize("pad", [1, 3, 24, 60])
+def test_A31_zero_weight_extension_leaves_als_unchanged(pad):
+    """Reading A31 (the GPU solver's equal segments): appending `pad` rows of weight 0 to the Whittaker
+    system (y = 0 there, weights re-derived only on the real rows) leaves the first M rows of every
+    solve unchanged -- the extra second differences vanish on the linear extrapolation of z.  Dense
+    fp64 solves of the extended system against the oracle's banded ALS."""
+    M = 200
+    rng = np.random.default_rng(31 + pad)
+    t = np.arange(M, dtype=float)
+    y = np.cumsum(rng.standard_normal(M)) * 0.05 + np.exp(-((t - 80) / 5) ** 2) + 0.002 * t
+    Mp = M + pad
+    D = np.diff(np.eye(Mp), n=2, axis=0)
+    yp = np.concatenate([y, np.zeros(pad)])
+    w = np.concatenate([np.ones(M), np.zeros(pad)])
+    for it in range(1, 11):
+        z = np.linalg.solve(np.diag(w) + 1e4 * D.T @ D, w * yp)
+        w = np.concatenate([np.where(y > z[:M], 1e-3, 1 - 1e-3), np.zeros(pad)])
+        if it in (1, 3, 10):
+            zo = O.als_baseline(y, O.Params(als_iters=it))[0]
+            assert np.max(np.abs(z[:M] - zo)) <= 1e-8 * np.max(np.abs(zo))
+            # the extension is the linear continuation of the last two real rows
+            assert np.allclose(z[M:], z[M - 1] + (z[M - 1] - z[M - 2]) * np.arange(1, pad + 1), rtol=0, atol=1e-7)
+
+
 def test_P9b_als_hugs_baseline_below_positive_peaks():
     M = 800
     t = np.linspace(-1, 1, M)
