@@ -477,6 +477,8 @@ void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const flo
                           float floor, int L, const float2* tw, const int* pmap, const float* phi, const float* phierr,
                           int sg_half, void* out, int out_imag_only, cudaStream_t s) {
   if (n <= 0) return;
+  // one thread per 16 FFT points holds at most 8 channels of each row
+  if (2 * M > L) throw Status(10, "direct path: the FFT length must be at least 2 M");
   const size_t smem = direct_finish_smem(M, L);
   const int64_t npairs = (n + 1) / 2;
   auto launch = [&](auto lt, auto in_tag) {
