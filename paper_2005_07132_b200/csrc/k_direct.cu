@@ -328,8 +328,19 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const float* yy = r ? y1 : y0;
+      // window moments at the first channel's centre (the centres of a chunk's channels are
+      // non-decreasing by 0 or 1 per channel, so the rest slide)
       double Q0 = 0, Q1 = 0, Q2 = 0;
-      int cprev = -1;
+      int cprev = j0 < h ? h : j0;
+      if (cprev > M - 1 - h) cprev = M - 1 - h;
+      if (j0 < M) {
+        double A0, A1, A2, B0, B1, B2;
+        prefix(r, cprev + h + 1, A0, A1, A2);
+        prefix(r, cprev - h, B0, B1, B2);
+        Q0 = A0 - B0;
+        Q1 = A1 - B1;
+        Q2 = A2 - B2;
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int j = j0 + c;
@@ -337,14 +348,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
         if (c < C && j < M) {
           int cc = j < h ? h : j;
           if (cc > M - 1 - h) cc = M - 1 - h;
-          if (cprev < 0) {
-            double A0, A1, A2, B0, B1, B2;
-            prefix(r, cc + h + 1, A0, A1, A2);
-            prefix(r, cc - h, B0, B1, B2);
-            Q0 = A0 - B0;
-            Q1 = A1 - B1;
-            Q2 = A2 - B2;
-          } else if (cc != cprev) {   // slide by one channel
+          if (cc != cprev) {   // slide by one channel
             const int ia = cc + h, ib = cprev - h;
             const double va = (double)yy[ia], vb = (double)yy[ib], da = (double)ia, db = (double)ib;
             Q0 += va - vb;
