@@ -361,17 +361,30 @@ def run_ours(args) -> dict:
         Ih = torch.from_numpy(I_h).pin_memory()
         Rh = torch.from_numpy(Iref_h).pin_memory()
         Oh = torch.empty((n_loc, M), dtype=torch.complex64).pin_memory()
+        Oh2 = torch.empty((n_loc, M), dtype=torch.complex64).pin_memory()
+        # one cube per call (context): H2D, transform, D2H in sequence
         plan.transform_host(Ih, Rh, Oh)
-        ne = max(1, min(args.steps, 2))
         _barrier(world)
         t0 = time.perf_counter()
-        for _ in range(ne):
-            plan.transform_host(Ih, Rh, Oh)
+        plan.transform_host(Ih, Rh, Oh)
+        _barrier(world)
+        t_single = _max_over_ranks(time.perf_counter() - t0, world)
+        # the e2e number: consecutive cubes through fkk_transform_host_stream (cube i+1's H2D and cube
+        # i-1's D2H overlap cube i's transform; each cube gets its full transform)
+        plan.transform_host_stream([Ih, Ih], Rh, [Oh, Oh2])
+        ne = max(2, min(args.steps, 8))
+        _barrier(world)
+        t0 = time.perf_counter()
+        lat = plan.transform_host_stream([Ih] * ne, Rh, [Oh if i % 2 == 0 else Oh2 for i in range(ne)])
         _barrier(world)
         te = _max_over_ranks((time.perf_counter() - t0) / ne, world)
         e2e = {"value": N / te, "unit": "spectra/s", "h2d_bytes_per_step": int(I_h.nbytes + Iref_h.nbytes),
-               "d2h_bytes_per_step": int(Oh.numel() * 8), "ms_per_step": te * 1e3,
-               "how": "fkk_transform_host: pinned host cube -> device, transform, complex64 cube -> pinned host"}
+               "d2h_bytes_per_step": int(Oh.numel() * 8), "ms_per_step": te * 1e3, "cubes": ne,
+               "cube_latency_ms_median": float(np.median(lat)),
+               "how": "fkk_transform_host_stream: pinned host cube -> device, transform, complex64 cube -> pinned "
+                      "host, per cube; the copies of neighbouring cubes overlap the transforms",
+               "single_cube_call": {"value": N / t_single, "ms": t_single * 1e3, "how": "fkk_transform_host"}}
+        del Oh2
         if ml is not None and world == 1 and Ia_h.shape == tuple(Ih.shape):
             # config 5 streamed from pinned host memory in 50,000-spectrum batches (H2D, apply, D2H pipelined)
             Ih.copy_(torch.from_numpy(Ia_h))

@@ -159,6 +159,15 @@ fkk_status fkk_conventional(fkk_plan_t p, const void* d_icars, int64_t n_rows, c
  * plan's stream; they synchronise before returning).  h_* may be pageable or pinned. */
 fkk_status fkk_transform_host(fkk_plan_t p, const void* h_icars, int64_t n_rows, const void* h_iref,
                               void* h_out, fkk_basis_t* basis_out);
+/* fKK-EC (as fkk_transform) of n_cubes host-resident cubes of n_rows spectra each, streamed: cube
+ * i+1's host->device copy and cube i-1's device->host copy overlap cube i's transform, over two copy
+ * streams and two device cube-buffer pairs (allocated on first use, kept by the plan; 2 (in + out)
+ * cube bytes).  h_icars[i] / h_out[i]: host cubes (pinned for the copies to overlap; an output
+ * buffer may repeat with a stride of 2 or more).  h_cube_ms (nullable, n_cubes floats): per-cube
+ * latency, H2D start to D2H end (CUDA events).  Each cube's result equals fkk_transform_host's.
+ * Synchronises before returning; errors as fkk_transform. */
+fkk_status fkk_transform_host_stream(fkk_plan_t p, const void* const* h_icars, int32_t n_cubes, int64_t n_rows,
+                                     const void* h_iref, void* const* h_out, float* h_cube_ms);
 fkk_status fkk_apply_trained_basis_host(fkk_plan_t p, fkk_basis_t b, const void* h_icars,
                                         int64_t n_rows, void* h_out);
 fkk_status kk_direct_batch_host(fkk_plan_t p, const void* h_icars, int64_t n_rows,

@@ -181,6 +181,9 @@ struct fkk_plan {
   void* stream_bufs[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t stream_in_bytes = 0, stream_out_bytes = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  // streamed host transform (lazy): two input and two output cube buffers
+  void* cube_bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t cube_in_bytes = 0, cube_out_bytes = 0;
   // last-call host state
   std::vector<double> h_s;
   std::vector<int64_t> h_q;
@@ -203,6 +206,7 @@ struct fkk_plan {
     for (void* p : ptrs) if (p) cudaFree(p);
     if (h_flags) cudaFreeHost(h_flags);
     for (void* b : stream_bufs) if (b) cudaFree(b);
+    for (void* b : cube_bufs) if (b) cudaFree(b);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     for (auto& m : marks) cudaEventDestroy(m.second);
@@ -1164,6 +1168,71 @@ fkk_status fkk_transform_host(fkk_plan_t p, const void* h_icars, int64_t n_rows,
     if (st != FKK_OK) throw Status(st, p->err);
     FKK_CUDA_CHECK(cudaMemcpyAsync(h_out, dout, out_bytes, cudaMemcpyDeviceToHost, p->stream));
     FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+// Host cubes streamed through the transform: cube i+1's host->device copy and cube i-1's device->host
+// copy (copy streams s_in / s_out, two device buffer pairs) overlap cube i's transform, and cube i's
+// device->host copy overlaps cube i+2's host->device copy (the link is full duplex).  Every cube gets
+// its own transform (Gram, eigensolve, basis, K), exactly as fkk_transform_host.
+fkk_status fkk_transform_host_stream(fkk_plan_t p, const void* const* h_icars, int32_t n_cubes, int64_t n_rows,
+                                     const void* h_iref, void* const* h_out, float* h_cube_ms) {
+  return guarded(p, [&] {
+    if (!h_icars || !h_iref || !h_out || n_cubes < 0) throw Status(FKK_ERR_INVALID_ARG, "NULL argument");
+    for (int i = 0; i < n_cubes; ++i)
+      if (!h_icars[i] || !h_out[i]) throw Status(FKK_ERR_INVALID_ARG, "NULL host cube");
+    if (n_rows < 1 || n_rows > p->d.max_rows) throw Status(FKK_ERR_INVALID_ARG, "n_rows must be in [1, max_rows]");
+    const int M = p->M;
+    const size_t in_b = (size_t)n_rows * M * p->in_elem;
+    const size_t out_b = (size_t)n_rows * M * (p->d.out_layout == FKK_OUT_IMAG_F32 ? 4 : 8);
+    if (p->cube_in_bytes < in_b || p->cube_out_bytes < out_b) {
+      for (void*& b : p->cube_bufs) if (b) { cudaFree(b); b = nullptr; }
+      for (int i = 0; i < 2; ++i) {
+        p->cube_bufs[i] = dalloc<char>(in_b);
+        p->cube_bufs[2 + i] = dalloc<char>(out_b);
+      }
+      p->cube_in_bytes = in_b;
+      p->cube_out_bytes = out_b;
+    }
+    if (!p->s_in) FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    if (!p->s_out) FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    if (!p->d_ref_buf) p->d_ref_buf = dalloc<double>(p->M);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(p->d_ref_buf, h_iref, (size_t)M * p->in_elem, cudaMemcpyHostToDevice, p->stream));
+    std::vector<cudaEvent_t> ev(4 * (size_t)std::max(n_cubes, 1));
+    for (auto& e : ev) FKK_CUDA_CHECK(cudaEventCreate(&e));
+    // ev[4i]: H2D start, ev[4i+1]: H2D done, ev[4i+2]: transform done, ev[4i+3]: D2H done
+    auto h2d = [&](int i) {
+      if (i >= 2) FKK_CUDA_CHECK(cudaStreamWaitEvent(p->s_in, ev[4 * (i - 2) + 2], 0));   // slot's last reader
+      FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i], p->s_in));
+      FKK_CUDA_CHECK(cudaMemcpyAsync(p->cube_bufs[i & 1], h_icars[i], in_b, cudaMemcpyHostToDevice, p->s_in));
+      FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 1], p->s_in));
+    };
+    try {
+      if (n_cubes > 0) h2d(0);
+      for (int i = 0; i < n_cubes; ++i) {
+        if (i + 1 < n_cubes) h2d(i + 1);   // enqueued before the transform blocks the host
+        FKK_CUDA_CHECK(cudaStreamWaitEvent(p->stream, ev[4 * i + 1], 0));
+        if (i >= 2) FKK_CUDA_CHECK(cudaStreamWaitEvent(p->stream, ev[4 * (i - 2) + 3], 0));   // output slot drained
+        const fkk_status st = fkk_transform(p, p->cube_bufs[i & 1], n_rows, p->d_ref_buf, p->cube_bufs[2 + (i & 1)], nullptr);
+        if (st != FKK_OK) throw Status(st, p->err);
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 2], p->stream));
+        FKK_CUDA_CHECK(cudaStreamWaitEvent(p->s_out, ev[4 * i + 2], 0));
+        FKK_CUDA_CHECK(cudaMemcpyAsync(h_out[i], p->cube_bufs[2 + (i & 1)], out_b, cudaMemcpyDeviceToHost, p->s_out));
+        FKK_CUDA_CHECK(cudaEventRecord(ev[4 * i + 3], p->s_out));
+      }
+      FKK_CUDA_CHECK(cudaStreamSynchronize(p->s_out));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(p->s_in));
+      FKK_CUDA_CHECK(cudaStreamSynchronize(p->stream));
+      if (h_cube_ms)
+        for (int i = 0; i < n_cubes; ++i) FKK_CUDA_CHECK(cudaEventElapsedTime(h_cube_ms + i, ev[4 * i], ev[4 * i + 3]));
+    } catch (...) {
+      cudaStreamSynchronize(p->s_in);
+      cudaStreamSynchronize(p->s_out);
+      cudaStreamSynchronize(p->stream);
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
   });
 }
 

@@ -71,6 +71,8 @@ _SIGS = {
     "fkk_conventional": (_i32, [_vp, _vp, _i64, _vp, _i32, _vp]),
     "fkk_transform_host": (_i32, [_vp, _vp, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
     "fkk_apply_trained_basis_host": (_i32, [_vp, _vp, _vp, _i64, _vp]),
+    "fkk_transform_host_stream": (_i32, [_vp, ctypes.POINTER(_vp), _i32, _i64, _vp, ctypes.POINTER(_vp),
+                                         ctypes.POINTER(ctypes.c_float)]),
     "kk_direct_batch_host": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "fkk_apply_trained_basis_stream": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, ctypes.POINTER(ctypes.c_float)]),
     "fkk_basis_destroy": (_i32, [_vp]),
@@ -290,6 +292,20 @@ class Plan:
         _check(self._h, _lib.fkk_transform_host(self._h, self._host_ptr(I), I.shape[0], self._host_ptr(Iref),
                                                 self._host_ptr(out), ctypes.byref(bh) if return_basis else None))
         return Basis(bh) if return_basis else None
+
+    def transform_host_stream(self, cubes, Iref, outs) -> np.ndarray:
+        """fkk_transform_host_stream: one transform per host cube (pinned; equal row counts), the copies
+        of neighbouring cubes overlapping the transforms; returns the per-cube latencies (ms)."""
+        n = len(cubes)
+        if len(outs) != n or any(c.shape != cubes[0].shape for c in cubes):
+            raise ValueError("cubes / outs: equal counts and shapes")
+        ins = (_vp * max(n, 1))(*[self._host_ptr(c) for c in cubes])
+        ous = (_vp * max(n, 1))(*[self._host_ptr(o) for o in outs])
+        ms = np.zeros(max(n, 1), dtype=np.float32)
+        _check(self._h, _lib.fkk_transform_host_stream(self._h, ins, n, cubes[0].shape[0] if n else 1,
+                                                       self._host_ptr(Iref), ous,
+                                                       ms.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return ms[:n]
 
     def direct_host(self, I, Iref, out):
         _check(self._h, _lib.kk_direct_batch_host(self._h, self._host_ptr(I), I.shape[0], self._host_ptr(Iref),

@@ -311,3 +311,26 @@ def test_host_buffer_variants(torch_cuda, fkk, cfg1):
     Kt_dev = plan.transform(_dev(torch_cuda, I), _dev(torch_cuda, Iref)).cpu().numpy()
     plan.transform_host(I, Iref, out)
     assert np.max(np.abs(out - Kt_dev)) <= 1e-6 * np.max(np.abs(Kt_dev))
+
+
+def test_transform_host_stream_matches_per_cube_calls(torch_cuda, fkk, cfg1):
+    """fkk_transform_host_stream: three different host cubes through the copy/compute pipeline, each
+    equal to its own fkk_transform_host; an output buffer reused with stride 2 holds the later cube."""
+    I, Iref = cfg1
+    rng = np.random.default_rng(5)
+    cubes = [np.ascontiguousarray(I * s * np.exp(0.05 * rng.standard_normal(I.shape))) for s in (1.0, 1.7, 0.6)]
+    plan = fkk.Plan(512, 12, I.shape[0], in_dtype="f64")
+    ref = []
+    for c in cubes:
+        o = np.empty((I.shape[0], 512), np.complex64)
+        plan.transform_host(c, Iref, o)
+        ref.append(o)
+    outs = [np.empty((I.shape[0], 512), np.complex64) for _ in range(3)]
+    ms = plan.transform_host_stream(cubes, Iref, outs)
+    assert ms.shape == (3,) and np.all(ms > 0)
+    for o, r in zip(outs, ref):
+        assert np.max(np.abs(o - r)) <= 1e-6 * np.max(np.abs(r))
+    shared = [outs[0], outs[1], outs[0]]
+    plan.transform_host_stream(cubes, Iref, shared)
+    assert np.max(np.abs(outs[0] - ref[2])) <= 1e-6 * np.max(np.abs(ref[2]))
+    assert np.max(np.abs(outs[1] - ref[1])) <= 1e-6 * np.max(np.abs(ref[1]))
