@@ -340,14 +340,41 @@ def run_ours(args) -> dict:
             nb += 1
         e1.record(stream)
         _barrier(world)
+        tm1 = _max_over_ranks(e0.elapsed_time(e1), world)
+        # independent batches alternate over two streams (two plans, two output buffers): one batch's
+        # projection fills the SMs the other's reconstruction tail leaves idle
+        papply2 = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local)
+        oa2 = torch.empty_like(oa)
+        sts = [torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)]
+        plans2, outs2 = [papply, papply2], [oa, oa2]
+        for b in range(2):
+            with torch.cuda.stream(sts[b]):
+                plans2[b].apply(basis, Ia[:batch], outs2[b])
+        torch.cuda.synchronize()
+        _barrier(world)
+        e0.record(stream)
+        for st in sts:
+            st.wait_event(e0)
+        for i, b0 in enumerate(range(0, a1 - a0, batch)):
+            nbb = min(batch, a1 - a0 - b0)
+            with torch.cuda.stream(sts[i & 1]):
+                plans2[i & 1].apply(basis, Ia[b0:b0 + nbb], outs2[i & 1][:nbb])
+        for st in sts:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            stream.wait_event(ev)
+        e1.record(stream)
+        _barrier(world)
         tm = _max_over_ranks(e0.elapsed_time(e1), world)
+        del papply2, oa2
         nbytes = 12.0 * (a1 - a0) * ap.n_freq           # read the cube (4 B) + write complex64 K (8 B) per element
         gbs = nbytes / (tm / 1e3) / 1e9
         ptime = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local, timing=True)   # per-kernel split of one full batch
         ptime.apply(basis, Ia[:batch], oa)
         ptime.apply(basis, Ia[:batch], oa)
         ml = {"value": ap.n_pixels / (tm / 1e3), "unit": "spectra/s", "ms_per_pass": tm,
-              "batches": nb, "ms_per_batch": tm / max(nb, 1), "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches",
+              "batches": nb, "ms_per_batch": tm / max(nb, 1), "streams": 2, "ms_per_batch_one_stream": tm1 / max(nb, 1),
+              "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches",
               "stage_ms_full_batch": ptime.stage_times(),
               "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                            "bytes_per_pass": nbytes}}

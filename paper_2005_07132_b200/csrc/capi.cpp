@@ -161,6 +161,7 @@ struct fkk_plan {
   int apre_blocks = 0;
   double* gtc_part = nullptr;
   int* gtc_sched = nullptr;   // balanced CTA-pair Gram schedule (mode 1)
+  int64_t gtc_sched_key = -1;  // (rows, tiles) the device schedule was built for
   // randomized range finder (svd_mode = FKK_SVD_RANGE_FINDER): l = k + oversample columns
   int rf_l = 0, rf_nsplit = 0;
   double *rf_omega = nullptr, *rf_part = nullptr, *rf_Z = nullptr, *rf_Zq = nullptr, *rf_Z2 = nullptr,
@@ -590,7 +591,7 @@ static void gram_from_image(fkk_plan* p, int64_t n_rows, int64_t nr, bool accumu
   if (p->gtc_pair) {
     (void)nr;
     fkk::launch_gram_pre2(p->apre, n_rows, M, p->gtc_tiles, p->gtc_tile_of, p->gtc_nTj, p->gtc_ntiles, p->gtc_sched,
-                          p->gtc_part, p->G, accumulate, s);
+                          &p->gtc_sched_key, p->gtc_part, p->G, accumulate, s);
   } else {
     const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
     fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);

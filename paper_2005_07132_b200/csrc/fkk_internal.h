@@ -98,7 +98,8 @@ int gram_pre2_pairs();
 size_t gram_pre2_partial_doubles(int ntiles);
 size_t gram_pre2_sched_ints(int ntiles);
 void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d_tiles, const int* d_tile_of, int nT,
-                      int ntiles, int* d_sched, double* partials, double* G, int accumulate, cudaStream_t s);
+                      int ntiles, int* d_sched, int64_t* sched_key, double* partials, double* G, int accumulate,
+                      cudaStream_t s);
 void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
                      double* partials, cudaStream_t s);
 // tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.

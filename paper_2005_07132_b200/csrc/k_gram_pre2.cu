@@ -365,7 +365,8 @@ size_t gram_pre2_sched_ints(int ntiles) {
 }
 
 void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d_tiles, const int* d_tile_of, int nT,
-                      int ntiles, int* d_sched, double* partials, double* G, int accumulate, cudaStream_t s) {
+                      int ntiles, int* d_sched, int64_t* sched_key, double* partials, double* G, int accumulate,
+                      cudaStream_t s) {
   const int64_t nq = (n + KC - 1) / KC;
   // schedule: W = ntiles x nq units, P contiguous ranges (at least 8 stages each)
   const int64_t W = (int64_t)ntiles * nq;
@@ -396,8 +397,13 @@ void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d
     for (int v : tslots[t]) sl[k++] = v;
   }
   tp[ntiles] = k;
-  // (pageable source: staged before the call returns, no device synchronisation)
-  FKK_CUDA_CHECK(cudaMemcpyAsync(d_sched, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  // uploaded once per (rows, tiles) of the owning plan (*sched_key): a copy in the stream ahead of every
+  // Gram cost ~40 us (pageable source: staged before the call returns, no device synchronisation)
+  const int64_t key = n * 65536 + ntiles;
+  if (!sched_key || *sched_key != key) {
+    FKK_CUDA_CHECK(cudaMemcpyAsync(d_sched, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (sched_key) *sched_key = key;
+  }
   FKK_CUDA_CHECK(cudaFuncSetAttribute(gram_pre2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * P);
