@@ -160,8 +160,6 @@ struct fkk_plan {
   unsigned char* apre = nullptr;   // pre-split MMA image of A0
   int apre_blocks = 0;
   double* gtc_part = nullptr;
-  int* gtc_sched = nullptr;   // balanced CTA-pair Gram schedule (mode 1)
-  int64_t gtc_sched_key = -1;  // (rows, tiles) the device schedule was built for
   // randomized range finder (svd_mode = FKK_SVD_RANGE_FINDER): l = k + oversample columns
   int rf_l = 0, rf_nsplit = 0;
   double *rf_omega = nullptr, *rf_part = nullptr, *rf_Z = nullptr, *rf_Zq = nullptr, *rf_Z2 = nullptr,
@@ -202,7 +200,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, pmap, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, gtc_sched, apre, phi, phierr, als_solves, rf_omega, rf_part, rf_Z, rf_Zq, rf_Z2, rf_SY, rf_S, rf_T, rf_U, rf_lam,
+                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, rf_omega, rf_part, rf_Z, rf_Zq, rf_Z2, rf_SY, rf_S, rf_T, rf_U, rf_lam,
                     rf_wimg, rf_Y, rf_tiles, rf_fallback, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
@@ -479,13 +477,8 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
       const int extra = d->svd_mode == FKK_SVD_RANGE_FINDER ? 1 : 0;
       p->apre = dalloc<unsigned char>(fkk::gram_pre_bytes(n, p->apre_blocks + extra));
     }
-    size_t part_doubles = p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
-                                      : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit);
-    if (mode == 1) {   // balanced pair schedule
-      part_doubles = std::max(part_doubles, fkk::gram_pre2_partial_doubles(p->gtc_ntiles));
-      p->gtc_sched = dalloc<int>(fkk::gram_pre2_sched_ints(p->gtc_ntiles));
-    }
-    p->gtc_part = dalloc<double>(part_doubles);
+    p->gtc_part = dalloc<double>(p->gtc_pair ? fkk::gram_tc2_partial_doubles(p->gtc_ntiles, p->gtc_nsplit)
+                                             : fkk::gram_tc_partial_doubles(p->gtc_ntiles, p->gtc_nsplit));
   } else {
     p->gram_nsplit_cap = fkk::gram_num_splits(n, M);
     p->gram_part = dalloc<double>((size_t)p->gram_nsplit_cap * fkk::gram_num_tiles(M) * 128 * 128);
@@ -589,9 +582,9 @@ void check_cube_args(fkk_plan* p, const void* cube, int64_t n_rows, const void* 
 static void gram_from_image(fkk_plan* p, int64_t n_rows, int64_t nr, bool accumulate, cudaStream_t s) {
   const int M = p->M;
   if (p->gtc_pair) {
-    (void)nr;
-    fkk::launch_gram_pre2(p->apre, n_rows, M, p->gtc_tiles, p->gtc_tile_of, p->gtc_nTj, p->gtc_ntiles, p->gtc_sched,
-                          &p->gtc_sched_key, p->gtc_part, p->G, accumulate, s);
+    const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
+    fkk::launch_gram_pre2(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
+    fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, accumulate, s);
   } else {
     const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
     fkk::launch_gram_pre(p->apre, n_rows, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);

@@ -91,15 +91,8 @@ void launch_logratio_pre(const float* I, int64_t n, int M, int nT, const float* 
                          unsigned char* Apre, int* flags, cudaStream_t s, int raw = 0);
 // CTA-pair Gram fed by the image (k_gram_pre2.cu): 256 x 256 tiles (gram_tc2_tiles / _splits / _reduce)
 int gram_pre2_image_blocks(int M);
-// CTA-pair Gram from the image (k_gram_pre2.cu): balanced (tile, stage) schedule over the SM pairs, the
-// partial slots reduced into G (accumulated when `accumulate`).  d_sched: gram_pre2_sched_ints(ntiles)
-// ints; partials: gram_pre2_partial_doubles(ntiles) doubles.
-int gram_pre2_pairs();
-size_t gram_pre2_partial_doubles(int ntiles);
-size_t gram_pre2_sched_ints(int ntiles);
-void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d_tiles, const int* d_tile_of, int nT,
-                      int ntiles, int* d_sched, int64_t* sched_key, double* partials, double* G, int accumulate,
-                      cudaStream_t s);
+void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
+                      double* partials, cudaStream_t s);
 void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
                      double* partials, cudaStream_t s);
 // tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.

@@ -70,17 +70,6 @@ __device__ __forceinline__ double cpl(int i, int j, int M, double lam) {
 struct M2 {   // 2 x 2 matrix, row-major
   double a, b, c, d;
 };
-__device__ __forceinline__ M2 mul(const M2& x, const M2& y) {
-  return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c, x.c * y.b + x.d * y.d};
-}
-__device__ __forceinline__ M2 inv(const M2& x) {
-  const double r = rcp64a(x.a * x.d - x.b * x.c);
-  return {x.d * r, -x.b * r, -x.c * r, x.a * r};
-}
-__device__ __forceinline__ double2 mulv(const M2& x, double2 v) {
-  return make_double2(x.a * v.x + x.b * v.y, x.c * v.x + x.d * v.y);
-}
-
 // interior weights of a segment: one bit per interior row (bit r <-> segment row r; 1 <-> w = p) in
 // a 64-bit (T <= 64) or 128-bit register.  A pass visits the rows in elimination order (ascending or
 // descending); it reads and rebuilds the mask through "position order" words (bit t <-> t-th row

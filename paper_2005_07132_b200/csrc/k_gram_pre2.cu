@@ -99,14 +99,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uin
                : "memory");
 }
 
-// Work schedule: the ntiles x nq (tile, 32-pixel stage) units in tile-major order are cut into one
-// contiguous range per pair (as many pairs as the SMs hold, not a multiple of the tile count), so a
-// pair runs up to MAXSEG segments (tile, [qb, qe)), each into its own fp64 partial slot.
-constexpr int MAXSEG = 4;
-
 __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char* __restrict__ Apre, int64_t nq,
-                                                            const int2* __restrict__ tiles,
-                                                            const int4* __restrict__ sched,
+                                                            const int2* __restrict__ tiles, int ntiles,
                                                             double* __restrict__ partials,
                                                             unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -121,7 +115,11 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cta_rank();
   const int pair = blockIdx.x >> 1;
-  const int4* seg = sched + (size_t)pair * MAXSEG;   // (tile, qb, qe, slot); tile < 0 ends the list
+  const int t = pair % ntiles, split = pair / ntiles, nsplit = (gridDim.x >> 1) / ntiles;
+  const int bi = tiles[t].x, bj = tiles[t].y;
+  const bool diag = bi == bj;
+  const int64_t qb = nq * split / nsplit, qe = nq * (split + 1) / nsplit;
+  const int64_t nper = qe > qb ? (qe - qb + SPP - 1) / SPP : 0;
 
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) {
@@ -148,51 +146,47 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
     // ------------------------------------------------------------ epilogue
     const int lg = warp & 3, chalf = warp >> 2;
     const int i = (int)rank * H + lg * 32 + lane;          // tile row
+    double* part = partials + (int64_t)pair * (T2 * T2);  // [j][i]
     float S[128];
 #pragma unroll
     for (int q = 0; q < 128; ++q) S[q] = 0.f;
     uint32_t ph[2] = {0, 0};
-    int64_t gp = 0;   // periods over all segments (accumulator buffer parity)
-    for (int sg = 0; sg < MAXSEG; ++sg) {
-      const int4 sd = seg[sg];
-      if (sd.x < 0) break;
-      double* part = partials + (int64_t)sd.w * (T2 * T2);  // [j][i]
-      const int64_t nper = ((int64_t)sd.z - sd.y + SPP - 1) / SPP;
-      bool first = true;
-      for (int64_t pidx = 0; pidx < nper; ++pidx, ++gp) {
-        const int b = (int)(gp & 1);
-        tc::mbar_wait(&acc_full[b], ph[b]);
-        ph[b] ^= 1;
-        tc::tc_fence_after();
-        const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 128 * chalf);
+    bool first = true;
+    for (int64_t pidx = 0; pidx < nper; ++pidx) {
+      const int b = (int)(pidx & 1);
+      tc::mbar_wait(&acc_full[b], ph[b]);
+      ph[b] ^= 1;
+      tc::tc_fence_after();
+      const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 128 * chalf);
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 16) {
-          float h[16];
-          tc::tmem_ld16(tb + c0, h);
+      for (int c0 = 0; c0 < 128; c0 += 16) {
+        float h[16];
+        tc::tmem_ld16(tb + c0, h);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) S[c0 + q] += h[q];
-        }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_on_relaxed(&acc_empty[b], 0);   // TMEM drained: orders no memory
-        const bool last = pidx == nper - 1;
-        if (last || ((pidx + 1) * PERIOD) % FLUSH == 0) {
-          // fp64 flush in batches of 16 (one L2 round trip per batch, as gram_pre_kernel)
+        for (int q = 0; q < 16; ++q) S[c0 + q] += h[q];
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_on_relaxed(&acc_empty[b], 0);   // TMEM drained: orders no memory
+      const bool last = pidx == nper - 1;
+      if (last || ((pidx + 1) * PERIOD) % FLUSH == 0) {
+        // fp64 flush in batches of 16 (one L2 round trip per batch, as gram_pre_kernel)
 #pragma unroll
-          for (int q0 = 0; q0 < 128; q0 += 16) {
-            double old[16];
+        for (int q0 = 0; q0 < 128; q0 += 16) {
+          double old[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) old[u] = first ? 0.0 : part[(int64_t)(128 * chalf + q0 + u) * T2 + i];
+          for (int u = 0; u < 16; ++u) old[u] = first ? 0.0 : part[(int64_t)(128 * chalf + q0 + u) * T2 + i];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-              part[(int64_t)(128 * chalf + q0 + u) * T2 + i] = old[u] + (double)S[q0 + u];
-              S[q0 + u] = 0.f;
-            }
+          for (int u = 0; u < 16; ++u) {
+            part[(int64_t)(128 * chalf + q0 + u) * T2 + i] = old[u] + (double)S[q0 + u];
+            S[q0 + u] = 0.f;
           }
-          first = false;
         }
+        first = false;
       }
     }
+    if (nper == 0)
+      for (int q = 0; q < 128; ++q) part[(int64_t)(128 * chalf + q) * T2 + i] = 0.0;
   } else if (warp == 8) {
     if (rank == 0) {
       // ---------------------------------------------------------- MMA issue (leader)
@@ -203,52 +197,45 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
       const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), LBO, SBO);
       unsigned long long w_full = 0, w_peer = 0, w_acc = 0;   // dbg cycle split
       const unsigned long long t_start = clock64();
-      int64_t gp = 0;
-      for (int sg = 0; sg < MAXSEG; ++sg) {
-        const int4 sd = seg[sg];
-        if (sd.x < 0) break;
-        const bool diag = tiles[sd.x].x == tiles[sd.x].y;
-        const int64_t nper = ((int64_t)sd.z - sd.y + SPP - 1) / SPP;
-        for (int64_t pidx = 0; pidx < nper; ++pidx, ++gp) {
-          const int b = (int)(gp & 1);
-          if (gp >= 2) {
-            const unsigned long long c0 = dbg ? clock64() : 0;
-            wait_cluster(&acc_empty[b], eph[b]);
-            if (dbg) w_acc += clock64() - c0;
-            eph[b] ^= 1;
-            tc::tc_fence_after();
-          }
-          const uint32_t d = tmem + 256 * b;
-          const int64_t q0 = sd.y + pidx * SPP, q1 = ((int64_t)sd.z < q0 + SPP) ? (int64_t)sd.z : (q0 + SPP);
-          uint32_t acc = 0;
-          for (int64_t q = q0; q < q1; ++q) {
-            const unsigned long long c0 = dbg ? clock64() : 0;
-            tc::mbar_wait(&full[stage], phase);
-            const unsigned long long c1 = dbg ? clock64() : 0;
-            wait_cluster(&pfull[stage], phase);
-            if (dbg) { w_full += c1 - c0; w_peer += clock64() - c1; }
-            tc::tc_fence_after();
-            const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * STB)), dal = tc::sdesc_add(dah, OPB);
-            const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, HALF);
-            const uint64_t dbl = diag ? dal : tc::sdesc_add(dah, HALF + OPB);
-            if (tc::elect_one()) {
-#pragma unroll
-              for (int ks = 0; ks < KC / 8; ++ks) {
-                const uint32_t ko = ks * 2 * LBO;
-                mma2(d, tc::sdesc_add(dal, ko), tc::sdesc_add(dbh, ko), idesc, acc);   // lo_i * hi_j
-                mma2(d, tc::sdesc_add(dah, ko), tc::sdesc_add(dbl, ko), idesc, 1);     // hi_i * lo_j
-                mma2(d, tc::sdesc_add(dah, ko), tc::sdesc_add(dbh, ko), idesc, 1);     // hi_i * hi_j
-                acc = 1;
-              }
-              commit2(&empty[stage]);
-            }
-            acc = 1;
-            __syncwarp();
-            if (++stage == NSTG) { stage = 0; phase ^= 1; }
-          }
-          if (tc::elect_one()) commit2(&acc_full[b]);
-          __syncwarp();
+      for (int64_t pidx = 0; pidx < nper; ++pidx) {
+        const int b = (int)(pidx & 1);
+        if (pidx >= 2) {
+          const unsigned long long c0 = dbg ? clock64() : 0;
+          wait_cluster(&acc_empty[b], eph[b]);
+          if (dbg) w_acc += clock64() - c0;
+          eph[b] ^= 1;
+          tc::tc_fence_after();
         }
+        const uint32_t d = tmem + 256 * b;
+        const int64_t q0 = qb + pidx * SPP, q1 = (qe < q0 + SPP) ? qe : (q0 + SPP);
+        uint32_t acc = 0;
+        for (int64_t q = q0; q < q1; ++q) {
+          const unsigned long long c0 = dbg ? clock64() : 0;
+          tc::mbar_wait(&full[stage], phase);
+          const unsigned long long c1 = dbg ? clock64() : 0;
+          wait_cluster(&pfull[stage], phase);
+          if (dbg) { w_full += c1 - c0; w_peer += clock64() - c1; }
+          tc::tc_fence_after();
+          const uint64_t dah = tc::sdesc_add(d00, (uint32_t)(stage * STB)), dal = tc::sdesc_add(dah, OPB);
+          const uint64_t dbh = diag ? dah : tc::sdesc_add(dah, HALF);
+          const uint64_t dbl = diag ? dal : tc::sdesc_add(dah, HALF + OPB);
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < KC / 8; ++ks) {
+              const uint32_t ko = ks * 2 * LBO;
+              mma2(d, tc::sdesc_add(dal, ko), tc::sdesc_add(dbh, ko), idesc, acc);   // lo_i * hi_j
+              mma2(d, tc::sdesc_add(dah, ko), tc::sdesc_add(dbl, ko), idesc, 1);     // hi_i * lo_j
+              mma2(d, tc::sdesc_add(dah, ko), tc::sdesc_add(dbh, ko), idesc, 1);     // hi_i * hi_j
+              acc = 1;
+            }
+            commit2(&empty[stage]);
+          }
+          acc = 1;
+          __syncwarp();
+          if (++stage == NSTG) { stage = 0; phase ^= 1; }
+        }
+        if (tc::elect_one()) commit2(&acc_full[b]);
+        __syncwarp();
       }
       if (dbg && lane == 0) {
         dbg[pair * 4 + 0] = clock64() - t_start;
@@ -261,39 +248,29 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
     if (lane == 0) {
       // ---------------------------------------------------------- bulk loader (both CTAs)
       const uint32_t sbase = tc::smem_u32(smem);
+      const uint32_t bytes = (diag ? 1u : 2u) * HALF;
+      const int cA = 2 * bi + (int)rank, cB = 2 * bj + (int)rank;     // 128-channel image blocks
       int stage = 0;
       uint32_t phase = 0;
-      for (int sg = 0; sg < MAXSEG; ++sg) {
-        const int4 sd = seg[sg];
-        if (sd.x < 0) break;
-        const int bi = tiles[sd.x].x, bj = tiles[sd.x].y;
-        const bool diag = bi == bj;
-        const uint32_t bytes = (diag ? 1u : 2u) * HALF;
-        const int cA = 2 * bi + (int)rank, cB = 2 * bj + (int)rank;     // 128-channel image blocks
-        for (int64_t q = sd.y; q < sd.z; ++q) {
-          tc::mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t st = sbase + stage * STB;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[stage])),
-                       "r"(bytes)
-                       : "memory");
-          bulk_g2s(st, Apre + (size_t)(cA * nq + q) * HALF, HALF, &full[stage]);
-          if (!diag) bulk_g2s(st + HALF, Apre + (size_t)(cB * nq + q) * HALF, HALF, &full[stage]);
-          if (++stage == NSTG) { stage = 0; phase ^= 1; }
-        }
+      for (int64_t q = qb; q < qe; ++q) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t st = sbase + stage * STB;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[stage])),
+                     "r"(bytes)
+                     : "memory");
+        bulk_g2s(st, Apre + (size_t)(cA * nq + q) * HALF, HALF, &full[stage]);
+        if (!diag) bulk_g2s(st + HALF, Apre + (size_t)(cB * nq + q) * HALF, HALF, &full[stage]);
+        if (++stage == NSTG) { stage = 0; phase ^= 1; }
       }
     }
   } else if (rank == 1 && lane == 0) {
     // ------------------------------------------------------------ forwarder (peer): stage landed -> leader
     int stage = 0;
     uint32_t phase = 0;
-    for (int sg = 0; sg < MAXSEG; ++sg) {
-      const int4 sd = seg[sg];
-      if (sd.x < 0) break;
-      for (int64_t q = sd.y; q < sd.z; ++q) {
-        tc::mbar_wait(&full[stage], phase);
-        arrive_on(&pfull[stage], 0);
-        if (++stage == NSTG) { stage = 0; phase ^= 1; }
-      }
+    for (int64_t q = qb; q < qe; ++q) {
+      tc::mbar_wait(&full[stage], phase);
+      arrive_on(&pfull[stage], 0);
+      if (++stage == NSTG) { stage = 0; phase ^= 1; }
     }
   } else if (rank == 0 && lane == 0) {
     // leader: its own stages need no forwarding; complete pfull for the single-CTA degenerate case
@@ -310,103 +287,12 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
 
 int gram_pre2_image_blocks(int M) { return 2 * ((M + T2 - 1) / T2); }
 
-namespace {
-// G[r][c] from the partial slots of the tile holding (min(r,c), max(r,c)): slots tile_ptr[t] .. tile_ptr[t+1]
-__global__ void gram_pre2_reduce_kernel(const double* __restrict__ partials, int M, const int* __restrict__ tile_of,
-                                        int nT, const int* __restrict__ tile_ptr, const int* __restrict__ slots,
-                                        double* __restrict__ G, int accumulate) {
-  const int64_t total = (int64_t)M * M;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / M), c = (int)(e % M);
-    const int i = min(r, c), j = max(r, c);
-    const int ti = i / T2, tj = j / T2;
-    const int t = tile_of[ti * nT + tj];
-    const int64_t off = (int64_t)(j - tj * T2) * T2 + (i - ti * T2);
-    double sum = 0.0;
-    for (int k = tile_ptr[t]; k < tile_ptr[t + 1]; ++k) sum += partials[(int64_t)slots[k] * (T2 * T2) + off];
-    G[e] = accumulate ? G[e] + sum : sum;
-  }
-}
-}  // namespace
-
-// pairs: cudaOccupancyMaxActiveClusters reports all 74 SM pairs of a B200, but 72 or 74 pairs run the
-// cfg3 Gram in 4.0 ms against 3.34 ms for 70 (FKK_GRAM_PAIRS A/B, the MMA warp's own-stage waits +40%),
-// so the schedule takes at most 70
-int gram_pre2_pairs() {
-  static int cached = 0;
-  if (cached) return cached;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  FKK_CUDA_CHECK(cudaFuncSetAttribute(gram_pre2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * (sms / 2));
-  cfg.blockDim = dim3(NTHR);
-  cfg.dynamicSmemBytes = SMEM;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int nc = 0;
-  if (cudaOccupancyMaxActiveClusters(&nc, gram_pre2_kernel, &cfg) != cudaSuccess || nc < 1) {
-    cudaGetLastError();
-    nc = sms / 2;
-  }
-  cached = std::min(std::min(nc, sms / 2), 70);
-  return cached;
-}
-size_t gram_pre2_partial_doubles(int ntiles) { return (size_t)(gram_pre2_pairs() + ntiles) * T2 * T2; }
-size_t gram_pre2_sched_ints(int ntiles) {
-  const int P = gram_pre2_pairs();
-  return (size_t)4 * P * MAXSEG + (ntiles + 1) + (P + ntiles);
-}
-
-void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d_tiles, const int* d_tile_of, int nT,
-                      int ntiles, int* d_sched, int64_t* sched_key, double* partials, double* G, int accumulate,
-                      cudaStream_t s) {
+void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
+                      double* partials, cudaStream_t s) {
   const int64_t nq = (n + KC - 1) / KC;
-  // schedule: W = ntiles x nq units, P contiguous ranges (at least 8 stages each)
-  const int64_t W = (int64_t)ntiles * nq;
-  int Pcap = gram_pre2_pairs();
-  if (const char* ev = getenv("FKK_GRAM_PAIRS")) Pcap = std::max(1, std::min(Pcap, atoi(ev)));   // A/B only
-  const int P = (int)std::max<int64_t>(1, std::min<int64_t>(Pcap, W / 8));
-  std::vector<int> h((size_t)4 * P * MAXSEG + (ntiles + 1) + (P + ntiles), -1);
-  std::vector<std::vector<int>> tslots(ntiles);
-  int nslot = 0;
-  for (int p = 0; p < P; ++p) {
-    const int64_t L0 = W * p / P, L1 = W * (p + 1) / P;
-    int sg = 0;
-    for (int64_t t = L0 / std::max<int64_t>(nq, 1); L1 > L0 && t <= (L1 - 1) / nq; ++t) {
-      const int64_t qb = std::max(L0, t * nq) - t * nq, qe = std::min(L1, (t + 1) * nq) - t * nq;
-      if (qe <= qb) continue;
-      if (sg == MAXSEG) throw Status(10, "gram_pre2: more tiles per pair than the schedule holds");
-      int* e = &h[(size_t)4 * (p * MAXSEG + sg)];
-      e[0] = (int)t; e[1] = (int)qb; e[2] = (int)qe; e[3] = nslot;
-      tslots[t].push_back(nslot++);
-      ++sg;
-    }
-  }
-  int* tp = &h[(size_t)4 * P * MAXSEG];
-  int* sl = tp + (ntiles + 1);
-  int k = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    tp[t] = k;
-    for (int v : tslots[t]) sl[k++] = v;
-  }
-  tp[ntiles] = k;
-  // uploaded once per (rows, tiles) of the owning plan (*sched_key): a copy in the stream ahead of every
-  // Gram cost ~40 us (pageable source: staged before the call returns, no device synchronisation)
-  const int64_t key = n * 65536 + ntiles;
-  if (!sched_key || *sched_key != key) {
-    FKK_CUDA_CHECK(cudaMemcpyAsync(d_sched, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-    if (sched_key) *sched_key = key;
-  }
   FKK_CUDA_CHECK(cudaFuncSetAttribute(gram_pre2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * P);
+  cfg.gridDim = dim3(2 * ntiles * nsplit);
   cfg.blockDim = dim3(NTHR);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
@@ -420,24 +306,21 @@ void launch_gram_pre2(const unsigned char* Apre, int64_t n, int M, const int2* d
   // FKK_GRAM_DBG (debug only): leader MMA-warp cycle split per pair, printed to stderr; synchronises
   static const bool gdbg = getenv("FKK_GRAM_DBG") != nullptr;
   unsigned long long* dbg = nullptr;
-  if (gdbg) FKK_CUDA_CHECK(cudaMalloc(&dbg, (size_t)P * 4 * sizeof(unsigned long long)));
-  FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gram_pre2_kernel, Apre, nq, d_tiles,
-                                    reinterpret_cast<const int4*>(d_sched), partials, dbg));
+  const int npair = ntiles * nsplit;
+  if (gdbg) FKK_CUDA_CHECK(cudaMalloc(&dbg, (size_t)npair * 4 * sizeof(unsigned long long)));
+  FKK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gram_pre2_kernel, Apre, nq, d_tiles, ntiles, partials, dbg));
   check_launch("gram_pre2");
   if (gdbg) {
-    std::vector<unsigned long long> hd((size_t)P * 4);
-    FKK_CUDA_CHECK(cudaMemcpyAsync(hd.data(), dbg, hd.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> h((size_t)npair * 4);
+    FKK_CUDA_CHECK(cudaMemcpyAsync(h.data(), dbg, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     FKK_CUDA_CHECK(cudaStreamSynchronize(s));
     cudaFree(dbg);
     double tot[4] = {0, 0, 0, 0};
-    for (int b = 0; b < P; ++b)
-      for (int q = 0; q < 4; ++q) tot[q] += (double)hd[b * 4 + q] / P;
+    for (int b = 0; b < npair; ++b)
+      for (int q = 0; q < 4; ++q) tot[q] += (double)h[b * 4 + q] / npair;
     fprintf(stderr, "gram_pre2 dbg: %d pairs, mean cycles total %.0f, wait own stage %.0f, wait peer %.0f, wait epilogue %.0f\n",
-            P, tot[0], tot[1], tot[2], tot[3]);
+            npair, tot[0], tot[1], tot[2], tot[3]);
   }
-  gram_pre2_reduce_kernel<<<1024, 256, 0, s>>>(partials, M, d_tile_of, nT, d_sched + 4 * P * MAXSEG,
-                                                d_sched + 4 * P * MAXSEG + (ntiles + 1), G, accumulate);
-  check_launch("gram_pre2_reduce");
 }
 
 }  // namespace fkk
