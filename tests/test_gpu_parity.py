@@ -334,3 +334,19 @@ def test_transform_host_stream_matches_per_cube_calls(torch_cuda, fkk, cfg1):
     plan.transform_host_stream(cubes, Iref, shared)
     assert np.max(np.abs(outs[0] - ref[2])) <= 1e-6 * np.max(np.abs(ref[2]))
     assert np.max(np.abs(outs[1] - ref[1])) <= 1e-6 * np.max(np.abs(ref[1]))
+
+
+def test_q_ties_take_the_lowest_pixel(torch_cuda, fkk, cfg2):
+    """Every spectrum duplicated (rows 2i and 2i+1 equal, in the same projection tile): each column
+    extreme of US ties between two pixels, and q (Eqs. 13-15, ties -> lowest pixel, reading A12) must
+    hold only even pixels and equal the oracle's q on the same cube."""
+    I, Iref = cfg2
+    Id2 = np.repeat(I[:6000], 2, axis=0)
+    plan = fkk.Plan(1000, 40, Id2.shape[0])
+    plan.transform(_dev(torch_cuda, Id2), _dev(torch_cuda, Iref))
+    q = plan.stage("Q")
+    US = plan.stage("US")
+    assert np.array_equal(US[0::2], US[1::2])          # the duplicated rows project bit-identically
+    assert np.all(q % 2 == 0), q
+    out = O.fkk_ec(Id2.astype(np.float64), Iref.astype(np.float64), 40, O.Params())
+    assert np.array_equal(q, out["q"])
