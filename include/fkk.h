@@ -91,7 +91,9 @@ typedef struct {
   int32_t in_dtype;          /* fkk_in_dtype of the cube and of I_ref */
   int32_t device;            /* CUDA device ordinal */
   int32_t world_size, rank;  /* pixel shards: this rank owns a contiguous block of rows */
-  const uint8_t* nccl_id;    /* 128-byte ncclUniqueId from fkk_get_nccl_unique_id; NULL iff world_size == 1 */
+  const uint8_t* nccl_id;    /* 128-byte ncclUniqueId from fkk_get_nccl_unique_id: required when world_size > 1;
+                                with world_size == 1 it selects the NCCL backend over a 1-rank communicator
+                                (exercises the collective path on one GPU); NULL: no communicator */
   int32_t loopback_shards;   /* >1: run the Gram/projection per virtual shard on one GPU and combine
                                 in the multi-rank order (partition-invariance test mode) */
   /* F2-F4 method ("random sampling ('randomized') SVD", Halko 2011):

@@ -23,7 +23,7 @@
 using fkk::Status;
 
 // ------------------------------------------------------------------------------------------------
-// NCCL, resolved at run time (only when world_size > 1), so the library loads without it.
+// NCCL, resolved at run time (only when the plan is given an nccl_id), so the library loads without it.
 // ------------------------------------------------------------------------------------------------
 namespace {
 
@@ -114,6 +114,7 @@ struct fkk_plan {
   std::string err;
   // NCCL
   ncclComm_t comm = nullptr;
+  bool use_nccl = false;   // nccl_id given: the NCCL backend (world_size > 1, or a 1-rank communicator)
   std::unique_ptr<fkk::Collectives> coll;   // the sharded exchange's collectives (local copy or NCCL)
   unsigned char* xscratch = nullptr;        // device staging of the control collectives (NCCL)
   size_t xscratch_bytes = 0;
@@ -264,7 +265,7 @@ struct fkk_plan {
   // the others blocked in the next collective.
   void check_flags_sync(bool collective = false);
   void check_flags_sync_impl(bool collective) {
-    if (collective && d.world_size > 1) {
+    if (collective && use_nccl) {
       if (!comm) throw Status(FKK_ERR_STATE, "the communicator was aborted by an earlier failure; recreate the plan");
       nccl_allreduce_flags();
     }
@@ -385,7 +386,7 @@ void validate_desc(const fkk_plan_desc* d) {
   if (d->out_layout != FKK_OUT_COMPLEX64 && d->out_layout != FKK_OUT_IMAG_F32) throw Status(FKK_ERR_INVALID_ARG, "bad out_layout");
   if (d->in_dtype != FKK_IN_F32 && d->in_dtype != FKK_IN_F64) throw Status(FKK_ERR_INVALID_ARG, "bad in_dtype");
   if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) throw Status(FKK_ERR_INVALID_ARG, "bad world_size/rank");
-  if ((d->world_size > 1) != (d->nccl_id != nullptr)) throw Status(FKK_ERR_INVALID_ARG, "nccl_id must be given iff world_size > 1");
+  if (d->world_size > 1 && !d->nccl_id) throw Status(FKK_ERR_INVALID_ARG, "nccl_id must be given when world_size > 1");
   if (d->loopback_shards < 0 || d->loopback_shards > 64) throw Status(FKK_ERR_INVALID_ARG, "loopback_shards must be in [0, 64]");
   if (d->svd_mode != FKK_SVD_GRAM && d->svd_mode != FKK_SVD_RANGE_FINDER) throw Status(FKK_ERR_INVALID_ARG, "bad svd_mode");
   if (d->svd_mode == FKK_SVD_RANGE_FINDER) {
@@ -543,7 +544,8 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     p->rf_lam = dalloc<double>(k);
     p->rf_fallback = dalloc<int>(1);
   }
-  if (d->world_size > 1) {
+  if (d->nccl_id) {   // (world_size 1 with an id: the NCCL backend over a 1-rank communicator)
+    p->use_nccl = true;
     std::string e;
     if (!g_nccl.load(e)) throw Status(FKK_ERR_NCCL, e);
     ncclUniqueId id;
@@ -563,7 +565,7 @@ struct Shard { int64_t row0, rows; };
 
 // Rows of all ranks (global row offset of this rank, global N): step 1 of exchange.h.
 void exchange_rows(fkk_plan* p, int64_t n_rows, int64_t& row0, int64_t& n_global) {
-  if (p->d.world_size > 1 && !p->comm)
+  if (p->use_nccl && !p->comm)
     throw Status(FKK_ERR_STATE, "the communicator was aborted by an earlier failure; recreate the plan");
   fkk::exchange_rows(*p->coll, n_rows, &row0, &n_global);
 }

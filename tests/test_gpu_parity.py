@@ -350,3 +350,27 @@ def test_q_ties_take_the_lowest_pixel(torch_cuda, fkk, cfg2):
     assert np.all(q % 2 == 0), q
     out = O.fkk_ec(Id2.astype(np.float64), Iref.astype(np.float64), 40, O.Params())
     assert np.array_equal(q, out["q"])
+
+
+def test_nccl_backend_one_rank(torch_cuda, fkk, cfg2):
+    """The NCCL collective backend (dlopen'ed libnccl, ncclCommInitRank, the row-count / extremes
+    all-gathers, the Gram and X all-reduces, the flags max-reduce and the deadline-polled syncs) over a
+    1-rank communicator on this GPU: the same results as the local backend, errors still reported and
+    the plan reusable, for the Gram and the range-finder SVD."""
+    I, Iref = cfg2
+    I = I[:20000]
+    Id, Rd = _dev(torch_cuda, I), _dev(torch_cuda, Iref)
+    for svd in ("gram", "range_finder"):
+        loc = fkk.Plan(1000, 40, I.shape[0], svd=svd)
+        nc = fkk.Plan(1000, 40, I.shape[0], svd=svd, world_size=1, rank=0, nccl_id=fkk.fkk_get_nccl_unique_id())
+        K0 = loc.transform(Id, Rd).cpu().numpy()
+        K1 = nc.transform(Id, Rd).cpu().numpy()
+        assert np.array_equal(loc.stage("Q"), nc.stage("Q"))
+        assert np.max(np.abs(K1 - K0)) <= 1e-6 * np.max(np.abs(K0))
+        bad = I[:2000].copy()
+        bad[3, 5] = np.nan
+        with pytest.raises(fkk.FkkError) as e:
+            nc.transform(_dev(torch_cuda, bad), Rd)
+        assert e.value.name == "FKK_ERR_NONFINITE_INPUT"
+        K2 = nc.transform(Id, Rd).cpu().numpy()
+        assert np.max(np.abs(K2 - K0)) <= 1e-6 * np.max(np.abs(K0))
