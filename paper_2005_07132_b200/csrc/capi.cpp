@@ -172,6 +172,7 @@ struct fkk_plan {
   int64_t direct_batch = 0;
   float *phi = nullptr, *phierr = nullptr;
   int* als_solves = nullptr;   // ALS solves summed over the spectra of the direct calls (diagnostic)
+  unsigned* als_ctr = nullptr;  // the direct ALS launches' dynamic spectrum counter
   // host-buffer variants (lazy)
   void* d_in_cube = nullptr;
   size_t d_in_cube_bytes = 0;
@@ -201,7 +202,7 @@ struct fkk_plan {
     if (stream) cudaStreamSynchronize(stream);
     void* ptrs[] = {flags, inv_ref, ref64, tw32, pmap, tw64, A, gram_part, G, colsum, f64, f32, V64, W, US, ext_val,
                     ext_idx, ext_out_val, ext_out_idx, q_dev, X, Vt_f, Hv, P, Phi_err, XtX, XtPhi, Phi_pec, HPhi,
-                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, rf_omega, rf_part, rf_Z, rf_Zq, rf_Z2, rf_SY, rf_S, rf_T, rf_U, rf_lam,
+                    tmp, Vsec, ridge_work, lam, Bi, bimg, wimg, eig_work, lam_d, gtc_tiles, gtc_tile_of, gtc_part, apre, phi, phierr, als_solves, als_ctr, rf_omega, rf_part, rf_Z, rf_Zq, rf_Z2, rf_SY, rf_S, rf_T, rf_U, rf_lam,
                     rf_wimg, rf_Y, rf_tiles, rf_fallback, d_in_cube,
                     d_out_cube, d_ref_buf};
     for (void* p : ptrs) if (p) cudaFree(p);
@@ -292,6 +293,7 @@ struct fkk_plan {
     phierr = dalloc<float>((size_t)direct_batch * M);
     als_solves = dalloc<int>(1);
     FKK_CUDA_CHECK(cudaMemset(als_solves, 0, sizeof(int)));
+    als_ctr = dalloc<unsigned>(1);
   }
 };
 
@@ -881,7 +883,7 @@ void direct_run(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_
     fkk::launch_direct_phase(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->tw32,
                              p->pmap, p->phi, p->flags, s);
     p->mark("kk_phase");
-    fkk::launch_als_rows(p->phi, 0, nb, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->phierr, 0, s, p->als_solves);
+    fkk::launch_als_rows(p->phi, 0, nb, M, p->d.als_lambda, p->d.als_p, p->d.als_iters, p->phierr, 0, s, p->als_solves, p->als_ctr);
     p->mark("als");
     fkk::launch_direct_finish(in, p->in_f64, nb, M, p->inv_ref, p->ref64, (float)p->d.ratio_floor, p->L, p->tw32,
                               p->pmap, p->phi, p->phierr, p->sg_half, out, p->d.out_layout == FKK_OUT_IMAG_F32, s);

@@ -58,8 +58,9 @@ void launch_add_f64(const double* a, const double* b, double* out, int64_t n, cu
 void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
                          float floor, int L, const float2* tw, const int* pmap, float* phi, int* flags, cudaStream_t s);
 // ALS on rows of y (fp32 or fp64, row-major n x M) -> z (fp32 or fp64); state: 3*M*nb doubles, nb = 32*ceil(n/32)
+// ctr (nullable, one unsigned of device memory): warps take spectra from it dynamically (reset here)
 void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s, int* solves = nullptr);
+                     cudaStream_t s, int* solves = nullptr, unsigned* ctr = nullptr);
 void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
                           float floor, int L, const float2* tw, const int* pmap, const float* phi, const float* phierr,
                           int sg_half, void* out, int out_imag_only, cudaStream_t s);
@@ -67,7 +68,7 @@ size_t direct_finish_smem(int M, int L);
 // warp-partitioned fp64 ALS (k_als.cu), state in shared memory; false if M is out of its range
 size_t als_part_smem(int M, int y_f64);
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s, int* solves = nullptr);
+                     cudaStream_t s, int* solves = nullptr, unsigned* ctr = nullptr);
 
 // ---- factorized path
 // Gram partials (k_gram.cu): 128 x 128 tiles of the upper triangle, nsplit row segments each.

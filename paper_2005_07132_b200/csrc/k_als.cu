@@ -135,7 +135,7 @@ __device__ __forceinline__ double& fld(unsigned char* rowp, int off, int s) {
 template <typename TY, typename TZ, typename MT>
 __global__ void __launch_bounds__(NL * WPC_MAX, 1)
     als_seg_kernel(const TY* __restrict__ y, int64_t n, int M, int T, int P, uint32_t tcols, double lam, double p,
-                   int iters, TZ* __restrict__ z, int* __restrict__ solves) {
+                   int iters, TZ* __restrict__ z, int* __restrict__ solves, unsigned* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char shm_all[];
   __shared__ uint32_t tmem_base_s;
   using RL = RowLayout<TY>;
@@ -162,7 +162,15 @@ __global__ void __launch_bounds__(NL * WPC_MAX, 1)
   const double lam2 = lam * lam, lam6 = 6.0 * lam, lamm4 = -4.0 * lam;
   int solves_local = 0;
 
-  for (int64_t row = (int64_t)blockIdx.x * wpc + warp; row < n; row += (int64_t)gridDim.x * wpc) {
+  // spectra: from the launch's counter when given (the solve count varies 2..10 per spectrum, so a static
+  // stride left the slowest warps ~10% behind the mean), else a static stride
+  auto next_row = [&](int64_t cur) -> int64_t {
+    if (!ctr) return cur < 0 ? (int64_t)blockIdx.x * wpc + warp : cur + (int64_t)gridDim.x * wpc;
+    unsigned v = 0;
+    if (s == 0) v = atomicAdd(ctr, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  for (int64_t row = next_row(-1); row < n; row = next_row(row)) {
     const TY* yr = y + row * (int64_t)M;
     __syncwarp();
     // lane s reads its own segment (L1 serves the strided lanes from the row's cached lines); the
@@ -529,7 +537,7 @@ size_t als_part_smem(int M, int y_f64) {
 }
 
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s, int* solves) {
+                     cudaStream_t s, int* solves, unsigned* ctr) {
   if (M < 8 || n <= 0) return false;
   int dev = 0, sms = 148, maxsm = 0;
   cudaGetDevice(&dev);
@@ -545,7 +553,8 @@ bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, dou
   {                                                                                                   \
     auto kf = g.T - 2 <= 64 ? als_seg_kernel<TY, TZ, unsigned long long> : als_seg_kernel<TY, TZ, unsigned __int128>; \
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));   \
-    kf<<<(unsigned)gr, NL * g.wpc, sm, s>>>((const TY*)y, n, M, g.T, g.P, g.cols, lam, p, iters, (TZ*)z, solves); \
+    if (ctr) FKK_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));                              \
+    kf<<<(unsigned)gr, NL * g.wpc, sm, s>>>((const TY*)y, n, M, g.T, g.P, g.cols, lam, p, iters, (TZ*)z, solves, ctr); \
   }
   if (y_f64 && z_f64) FKK_ALS_SEG(double, double)
   else if (!y_f64 && !z_f64) FKK_ALS_SEG(float, float)

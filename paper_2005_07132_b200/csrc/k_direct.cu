@@ -471,9 +471,9 @@ void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const floa
 }
 
 void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,
-                     cudaStream_t s, int* solves) {
+                     cudaStream_t s, int* solves, unsigned* ctr) {
   if (n <= 0) return;
-  if (!launch_als_part(y, y_f64, n, M, lam, p, iters, z, z_f64, s, solves))
+  if (!launch_als_part(y, y_f64, n, M, lam, p, iters, z, z_f64, s, solves, ctr))
     throw Status(10, "ALS: M must be in [8, 4096] and its segment state must fit in shared memory");
 }
 
