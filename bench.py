@@ -173,6 +173,29 @@ def run_ours(args) -> dict:
     stage_ms = {kk: v / args.steps for kk, v in stage_acc.items()}
     value = N / (t / 1e3)
 
+    # per-run parity diagnostics of the last timed transform (outside the timed region):
+    # the eigengap at k and the GPU eigenvalues against a host fp64 eigvalsh of the same G, the
+    # argmax/argmin margins of the US columns that decide q, the size of q, clamped / non-finite inputs
+    diag = None
+    if world == 1:
+        G_h = plan.stage("G")
+        lam_h = np.linalg.eigvalsh(G_h)[::-1]
+        s_gpu = plan.stage("S")[:k]
+        s_h = np.sqrt(np.maximum(lam_h[:k], 0.0))
+        US_h = plan.stage("US")[:n_loc, :k]
+        two = np.partition(US_h, [n_loc - 2, n_loc - 1], axis=0)[-2:]      # 2nd largest, largest
+        low = np.partition(US_h, [0, 1], axis=0)[:2]                        # smallest, 2nd smallest
+        scale = np.max(np.abs(US_h), axis=0)
+        diag = {"eigengap_k_rel": float((lam_h[k - 1] - lam_h[k]) / lam_h[k - 1]),
+                "sigma_k_over_sigma_1": float(s_h[k - 1] / s_h[0]),
+                "max_abs_ds_over_s1_gpu_vs_host_eigvalsh": float(np.max(np.abs(s_gpu - s_h)) / s_h[0]),
+                "argmax_margin_min_rel": float(np.min((two[1] - two[0]) / scale)),
+                "argmin_margin_min_rel": float(np.min((low[1] - low[0]) / scale)),
+                "n_q": int(plan.stage("Q").size),
+                "clamped_inputs": int(np.count_nonzero(I_h < 1e-6 * Iref_h[None, :])),
+                "nonfinite_inputs": int(np.count_nonzero(~np.isfinite(I_h)))}
+        del G_h, US_h
+
     # roofline of the Gram (F2, tcgen05 3xTF32): algorithmic flops N*M^2 (the syrk: M(M+1)/2 unique
     # products x 2 flops, rounded to M^2) per pass; 3xTF32 issues three TF32 products per fp32-equivalent
     # product, so its fp32-equivalent peak is the TF32 peak / 3.  The denominator is
@@ -433,7 +456,7 @@ def run_ours(args) -> dict:
         "config": {"workload": f"{args.workload}: fKK-EC transform of {N:,} x {M} (k={k}), fp32 cube, complex64 out",
                    "n_spectra": N, "n_freq": M, "rank_k": k, "parallelism": f"pixel shards x{world}",
                    "l2": "inputs larger than L2 (cube 2.81 GB, output 5.62 GB)"},
-        "roofline": roofline, "stage_ms": stage_ms, "clocks": clocks,
+        "roofline": roofline, "stage_ms": stage_ms, "clocks": clocks, "parity_diagnostics": diag,
         "gpu_launches": int(launches),
         "direct_kk": direct_kk,
         "ml_apply": ml, "e2e": e2e, "conventional": conv, "range_finder": rfo,
