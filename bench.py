@@ -257,6 +257,7 @@ def run_ours(args) -> dict:
     td = _max_over_ranks(e0.elapsed_time(e1) / nd, world)
     solves = pdir.als_solves() / (nd * n_loc)
     del pdir
+    plan.direct(I, Iref, out)          # (the plan's first direct call allocates its phi / phi_err scratch)
     plan.direct(I, Iref, out)
     dstage = plan.stage_times()
     # rooflines of the direct path: ALS against the FP64 pipe (algorithmic flops
