@@ -64,7 +64,7 @@ void launch_als_rows(const void* y, int y_f64, int64_t n, int M, double lam, dou
 void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
                           float floor, int L, const float2* tw, const int* pmap, const float* phi, const float* phierr,
                           int sg_half, void* out, int out_imag_only, cudaStream_t s);
-size_t direct_finish_smem(int M, int L);
+size_t direct_finish_smem(int M, int L, bool pf);
 // warp-partitioned fp64 ALS (k_als.cu), state in shared memory; false if M is out of its range
 size_t als_part_smem(int M, int y_f64);
 bool launch_als_part(const void* y, int y_f64, int64_t n, int M, double lam, double p, int iters, void* z, int z_f64,

@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "fft_r16.cuh"
 #include "fkk_internal.h"
 
@@ -29,6 +32,31 @@ __device__ __forceinline__ float log_ratio_elem(const TIn v, const float inv_ref
     float r = (float)v * inv_ref;
     return 0.5f * __logf(fmaxf(r, floor));   // hardware log (<= 2 ulp; reading A27)
   }
+}
+
+// one-dimensional bulk copy global -> shared (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WB_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WB_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // fp64 reciprocal: MUFU seed + two Newton steps (~1 ulp)
@@ -163,18 +191,21 @@ __device__ __forceinline__ SgK sg_k(int h) {
   k.iK2 = 1.0 / k.K2;
   return k;
 }
-__device__ __forceinline__ double sg_eval(double Q0, double Q1, double Q2, int c, int j, const SgK& k) {
+// branch-free form: at j = c the linear and quadratic terms are exact zeros
+__device__ __forceinline__ double sg_eval_full(double Q0, double Q1, double Q2, int c, int j, const SgK& k) {
   const double cd = (double)c;
   const double S0 = Q0, S1 = Q1 - cd * Q0, S2 = Q2 - 2.0 * cd * Q1 + cd * cd * Q0;
   const double c0 = (k.K4 * S0 - k.K2 * S2) * k.idet;
-  if (c == j) return c0;
   const double c2 = (k.n * S2 - k.K2 * S0) * k.idet;
   const double c1 = S1 * k.iK2;
   const double d = (double)(j - c);
-  return c0 + c1 * d + c2 * d * d;
+  return fma(fma(c2, d, c1), d, c0);
 }
 
-template <typename TIn, int LOG2L>
+// PF: the phi_err rows of the NEXT pair are bulk-copied into a staging buffer while this pair's SG
+// trend runs, and this pair's I / phi rows are prefetched into L2 before its transforms (fp32 input,
+// M % 4 == 0).
+template <typename TIn, int LOG2L, bool PF>
 __global__ void __launch_bounds__(threads_of<LOG2L>(), (2048 / threads_of<LOG2L>()) * FKK_DIRECT_MINB / 16)
 direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* __restrict__ inv_ref,
                      const double* __restrict__ ref64, float floor, const float2* __restrict__ tw,
@@ -188,7 +219,9 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   float2* Y = X + PADL;
   double* pre = reinterpret_cast<double*>(Y + PADL);   // [NT + 1][6]: chunk prefixes (3 moments x 2 rows)
   double* red = pre + 6 * (NT + 1);                    // [NW][8] scan / min scratch
-  float* e0 = reinterpret_cast<float*>(Y);             // phi_err rows (consumed by the forward pass)
+  float* S = reinterpret_cast<float*>(red + NW * 8);   // PF: staged phi_err rows [2][M]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(S + 2 * M);
+  float* e0 = PF ? S : reinterpret_cast<float*>(Y);    // phi_err rows (consumed by the forward pass)
   float* e1 = e0 + M;
   float* hb = reinterpret_cast<float*>(Y) + 2 * M;     // H{phi_err} rows (written by the inverse pass)
   float* y0 = reinterpret_cast<float*>(X);             // Re K' rows (after the transforms)
@@ -198,16 +231,46 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   const int j0 = tid * C;
   const SgK sgk = sg_k(h);
   const int64_t npairs = (n + 1) >> 1;
+  const uint32_t rowb = (uint32_t)M * 4u;
+  auto issue = [&](int64_t pr) {   // thread 0: bulk copies of pair pr's phi_err rows into S
+    const int64_t r0 = 2 * pr;
+    const bool two = r0 + 1 < n;
+    mbar_expect(bar, two ? 2 * rowb : rowb);
+    bulk_row(S, phierr + r0 * (int64_t)M, rowb, bar);
+    if (two) bulk_row(S + M, phierr + (r0 + 1) * (int64_t)M, rowb, bar);
+  };
+  if constexpr (PF) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && (int64_t)blockIdx.x < npairs) issue(blockIdx.x);
+  }
+  uint32_t ph = 0;
   for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
     const int64_t r0 = 2 * pr, r1 = r0 + 1;
     const bool has1 = r1 < n;
     const int64_t o0 = r0 * (int64_t)M, o1 = has1 ? r1 * (int64_t)M : o0;
-    for (int j = tid; j < M; j += NT) {
-      e0[j] = phierr[o0 + j];
-      e1[j] = phierr[o1 + j];
+    if constexpr (PF) {
+      if (tid == 0) {   // read after the transforms: in L2 by then
+        prefetch_l2(I + o0, rowb);
+        prefetch_l2(phi + o0, rowb);
+        if (has1) {
+          prefetch_l2(I + o1, rowb);
+          prefetch_l2(phi + o1, rowb);
+        }
+      }
+      mbar_wait_parity(bar, ph);
+      ph ^= 1u;
+    } else {
+      for (int j = tid; j < M; j += NT) {
+        e0[j] = phierr[o0 + j];
+        e1[j] = phierr[o1 + j];
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    hilbert_pair<LOG2L>(tw, pmap, M, X, Y, e0, e1, [&](int j, float a, float b) {
+    hilbert_pair<LOG2L>(tw, pmap, M, X, Y, e0, has1 || !PF ? e1 : e0, [&](int j, float a, float b) {
       hb[j] = a;
       hb[M + j] = b;
     });
@@ -225,11 +288,13 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
         const float4* ip = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(I) + o + j0);
         const float4* rp = reinterpret_cast<const float4*>(inv_ref + j0);
         const float4* pp4 = reinterpret_cast<const float4*>(phi + o + j0);
-        const float4* ep4 = reinterpret_cast<const float4*>(phierr + o + j0);
+        const float4* ep4 = PF ? reinterpret_cast<const float4*>(S + ((r && has1) ? M : 0) + j0)
+                               : reinterpret_cast<const float4*>(phierr + o + j0);
         const float4* hp4 = reinterpret_cast<const float4*>(hb + r * M + j0);
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
-          const float4 x = __ldcs(ip + h2), ir = rp[h2], f = __ldcs(pp4 + h2), e = __ldcs(ep4 + h2), hh = hp4[h2];
+          const float4 x = __ldcs(ip + h2), ir = rp[h2], f = __ldcs(pp4 + h2), e = PF ? ep4[h2] : __ldcs(ep4 + h2),
+                       hh = hp4[h2];
           const float xs[4] = {x.x, x.y, x.z, x.w}, is[4] = {ir.x, ir.y, ir.z, ir.w};
           const float fs[4] = {f.x, f.y, f.z, f.w}, es[4] = {e.x, e.y, e.z, e.w}, hs[4] = {hh.x, hh.y, hh.z, hh.w};
 #pragma unroll
@@ -247,7 +312,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
           if (c < C && j < M) {
             va[c] = log_ratio_elem<TIn>(I[o + j], inv_ref[j], ref64[j], floor);
             vh[c] = hb[r * M + j];
-            vp[c] = phi[o + j] - phierr[o + j];
+            vp[c] = phi[o + j] - (PF ? S[((r && has1) ? M : 0) + j] : phierr[o + j]);
           }
         }
       }
@@ -296,6 +361,12 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       for (int q = 0; q < 6; ++q) red[wid * 8 + q] = inc[q];
     }
     __syncthreads();
+    if constexpr (PF) {   // every thread has read this pair's staged rows: stage the next pair
+      if (tid == 0 && pr + gridDim.x < npairs) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(pr + gridDim.x);
+      }
+    }
     double off[6] = {0, 0, 0, 0, 0, 0};
     for (int w2 = 0; w2 < wid; ++w2) {
 #pragma unroll
@@ -308,16 +379,23 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       for (int q = 0; q < 6; ++q) pre[NT * 6 + q] = off[q] + inc[q];
     }
     __syncthreads();
-    // prefix at idx in [0, M] = chunk prefix + partial terms
+    // prefix at idx in [0, M] from the nearest chunk boundary: forward terms from t C, or backward
+    // terms from (t + 1) C, at most C / 2 <= 4 of them (a fixed, predicated loop: no divergence)
     auto prefix = [&](int r, int idx, double& P0, double& P1, double& P2) {
-      int t = idx / C;
-      if (t > NT) t = NT;
-      P0 = pre[t * 6 + 3 * r];
-      P1 = pre[t * 6 + 3 * r + 1];
-      P2 = pre[t * 6 + 3 * r + 2];
+      const int t = idx / C, rem = idx - t * C;
+      const bool back = 2 * rem > C && t < NT;
+      const int tb = back ? t + 1 : t;
+      P0 = pre[tb * 6 + 3 * r];
+      P1 = pre[tb * 6 + 3 * r + 1];
+      P2 = pre[tb * 6 + 3 * r + 2];
       const float* yy = r ? y1 : y0;
-      for (int i = t * C; i < idx; ++i) {
-        const double v = (double)yy[i], di = (double)i;
+      const int i0 = back ? idx : t * C;
+      const int nterm = back ? C - rem : rem;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        const float fv = (u < nterm && i < M) ? yy[i < M ? i : M - 1] : 0.f;
+        const double v = back ? -(double)fv : (double)fv, di = (double)i;
         P0 += v;
         P1 = fma(di, v, P1);
         P2 = fma(di * di, v, P2);
@@ -333,7 +411,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
       double Q0 = 0, Q1 = 0, Q2 = 0;
       int cprev = j0 < h ? h : j0;
       if (cprev > M - 1 - h) cprev = M - 1 - h;
-      if (j0 < M) {
+      {   // (threads past M compute a valid, unused window)
         double A0, A1, A2, B0, B1, B2;
         prefix(r, cprev + h + 1, A0, A1, A2);
         prefix(r, cprev - h, B0, B1, B2);
@@ -341,25 +419,25 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
         Q1 = A1 - B1;
         Q2 = A2 - B2;
       }
+      // every thread runs the same instructions for its 8 channel slots (predicated, no divergence:
+      // the edge threads' centres stay, the interior threads' slide; a stay adds zero terms)
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int j = j0 + c;
-        tr[r][c] = 0.f;
-        if (c < C && j < M) {
-          int cc = j < h ? h : j;
-          if (cc > M - 1 - h) cc = M - 1 - h;
-          if (cc != cprev) {   // slide by one channel
-            const int ia = cc + h, ib = cprev - h;
-            const double va = (double)yy[ia], vb = (double)yy[ib], da = (double)ia, db = (double)ib;
-            Q0 += va - vb;
-            Q1 += da * va - db * vb;
-            Q2 += da * da * va - db * db * vb;
-          }
-          cprev = cc;
-          const double Tv = sg_eval(Q0, Q1, Q2, cc, j, sgk);
-          tmin[r] = fmin(tmin[r], Tv);
-          tr[r][c] = (float)rcp64(Tv);   // 1/T, unless the spectrum falls back to the mean
-        }
+        int cc = j < h ? h : j;
+        if (cc > M - 1 - h) cc = M - 1 - h;
+        const bool sl = cc != cprev;
+        const int ia = cc + h, ib = cprev - h;   // both inside [0, M) for any centre in [h, M-1-h]
+        const float fa = yy[ia], fb = yy[ib];
+        const double va = sl ? (double)fa : 0.0, vb = sl ? (double)fb : 0.0, da = (double)ia, db = (double)ib;
+        Q0 += va - vb;
+        Q1 += da * va - db * vb;
+        Q2 += da * da * va - db * db * vb;
+        cprev = cc;
+        const double Tv = sg_eval_full(Q0, Q1, Q2, cc, j, sgk);
+        const bool ok = c < C && j < M;
+        tmin[r] = ok ? fmin(tmin[r], Tv) : tmin[r];
+        tr[r][c] = ok ? (float)rcp64(Tv) : 0.f;   // 1/T, unless the spectrum falls back to the mean
       }
     }
     // min of the trend per spectrum (fallback to the scalar mean if <= 0, reading A9)
@@ -442,13 +520,23 @@ void with_log2(int log2L, F&& f) {
 
 }  // namespace
 
+// direct_finish prefetch pipeline (PF) for fp32 rows of a multiple of 4 channels (measured: 13.5 against
+// 14.0 ms per cfg3 pass; the same staging in direct_phase measured slower, 5.53 against 5.40 ms);
+// FKK_DIRECT_PREFETCH=0 turns it off
+inline bool direct_pf(int in_f64, int M) {
+  static const int env = [] {
+    const char* e = getenv("FKK_DIRECT_PREFETCH");
+    return e ? atoi(e) : 1;
+  }();
+  return env != 0 && !in_f64 && M % 4 == 0;
+}
+
 size_t direct_phase_smem(int L) { return 2 * (size_t)fft16::padded_len(L) * sizeof(float2); }
-size_t direct_finish_smem(int M, int L) {
-  (void)M;
+size_t direct_finish_smem(int M, int L, bool pf) {
   const int T = L / 16;
   const int NT = T < 32 ? 32 : T;
   return 2 * (size_t)fft16::padded_len(L) * sizeof(float2) + (size_t)6 * (NT + 1) * sizeof(double) +
-         (size_t)(NT / 32) * 8 * sizeof(double);
+         (size_t)(NT / 32) * 8 * sizeof(double) + (pf ? 2 * (size_t)M * sizeof(float) + 16 : 0);
 }
 
 void launch_direct_phase(const void* I, int in_f64, int64_t n, int M, const float* inv_ref, const double* ref64,
@@ -483,20 +571,22 @@ void launch_direct_finish(const void* I, int in_f64, int64_t n, int M, const flo
   if (n <= 0) return;
   // one thread per 16 FFT points holds at most 8 channels of each row
   if (2 * M > L) throw Status(10, "direct path: the FFT length must be at least 2 M");
-  const size_t smem = direct_finish_smem(M, L);
+  const bool pf = direct_pf(in_f64, M);
+  const size_t smem = direct_finish_smem(M, L, pf);
   const int64_t npairs = (n + 1) / 2;
-  auto launch = [&](auto lt, auto in_tag) {
+  auto launch = [&](auto lt, auto in_tag, auto pf_tag) {
     constexpr int LG = decltype(lt)::v;
     using TIn = decltype(in_tag);
-    auto kf = direct_finish_kernel<TIn, LG>;
+    auto kf = direct_finish_kernel<TIn, LG, decltype(pf_tag)::value>;
     constexpr int NT = threads_of<LG>();
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = occupancy_grid((const void*)kf, NT, smem, npairs);
     kf<<<grid, NT, smem, s>>>(reinterpret_cast<const TIn*>(I), n, M, inv_ref, ref64, floor, tw, pmap, phi, phierr,
                               sg_half, out, out_imag_only);
   };
-  if (in_f64) with_log2(ilog2(L), [&](auto lt) { launch(lt, double{}); });
-  else with_log2(ilog2(L), [&](auto lt) { launch(lt, float{}); });
+  if (in_f64) with_log2(ilog2(L), [&](auto lt) { launch(lt, double{}, std::false_type{}); });
+  else if (pf) with_log2(ilog2(L), [&](auto lt) { launch(lt, float{}, std::true_type{}); });
+  else with_log2(ilog2(L), [&](auto lt) { launch(lt, float{}, std::false_type{}); });
   check_launch("direct_finish");
 }
 
