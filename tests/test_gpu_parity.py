@@ -54,6 +54,20 @@ def test_direct_cfg1_f64_input(torch_cuda, fkk, cfg1, pad, rows):
     assert _rel_inf(K, K_or) <= 1e-5
 
 
+@pytest.mark.parametrize("rows", [1, 33, 301])
+def test_direct_cfg1_f32_input_odd_rows(torch_cuda, fkk, cfg1, rows):
+    """fp32 input takes direct_finish's prefetch pipeline (next pair's phi_err rows bulk-copied into a
+    staging buffer, a lone last row without a partner): odd row counts, 1e-5 against the oracle run on
+    the same fp32 values."""
+    I, Iref = cfg1
+    I32 = I[:rows].astype(np.float32)
+    R32 = Iref.astype(np.float32)
+    K_or = O.kk_direct(I32.astype(np.float64), R32.astype(np.float64), O.Params())
+    plan = fkk.Plan(512, 12, rows, in_dtype="f32")
+    K = plan.direct(_dev(torch_cuda, I32), _dev(torch_cuda, R32)).cpu().numpy()
+    assert _rel_inf(K, K_or) <= 1e-5
+
+
 def test_direct_cfg2_sample_f32(torch_cuda, fkk):
     I, Iref, _ = generate(CONFIGS["cfg2"])
     rng = np.random.default_rng(0)
