@@ -466,10 +466,11 @@ void create_plan(const fkk_plan_desc* d, fkk_plan* p) {
     // CTA pairs (256 x 256 tiles) when they add no channel padding over 128 x 128 tiles: after the
     // batched fp64 flush they are faster (3.50 vs 3.61 ms at cfg3)
     int mode = ((M + 127) / 128) % 2 == 0 ? 1 : 0;
-    if (const char* ev = getenv("FKK_GRAM_MODE")) mode = atoi(ev) & 3;
+    // modes: 0 1-CTA image Gram, 1 CTA-pair image Gram, 2 fp32-A 1-CTA Gram (f64 input, loopback shards)
+    if (const char* ev = getenv("FKK_GRAM_MODE")) mode = std::min(2, std::max(0, atoi(ev)));   // A/B and tests
     if ((mode == 0 || mode == 1) && (d->in_dtype || d->loopback_shards > 1)) mode = 2;   // image needs fp32, 1 shard
     p->gram_mode = mode;
-    p->gtc_pair = mode == 1 || mode == 3;
+    p->gtc_pair = mode == 1;
     if (p->gtc_pair) fkk::gram_tc2_tiles(M, tl, tof, p->gtc_nTj);
     else fkk::gram_tc_tiles(M, tl, tof, p->gtc_nTj);
     p->gtc_ntiles = (int)tl.size();
@@ -694,10 +695,6 @@ void svd_stage(fkk_plan* p, const void* d_icars, int64_t n_rows, const void* d_i
       const int64_t nr = std::max<int64_t>(r1 - r0, 1);
       if (pre) {
         gram_from_image(p, n_rows, nr, sh > 0, s);
-      } else if (p->gtc_pair) {
-        const int ns = std::min(p->gtc_nsplit, fkk::gram_tc2_splits(p->gtc_ntiles, nr));
-        fkk::launch_gram_tc2(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);
-        fkk::launch_gram_tc2_reduce(p->gtc_part, p->gtc_ntiles, ns, M, p->gtc_tile_of, p->gtc_nTj, p->G, sh > 0, s);
       } else {
         const int ns = std::min(p->gtc_nsplit, fkk::gram_tc_splits(p->gtc_ntiles, nr));
         fkk::launch_gram_tc(p->A + r0 * (int64_t)M, r1 - r0, M, p->gtc_tiles, p->gtc_ntiles, ns, p->gtc_part, s);

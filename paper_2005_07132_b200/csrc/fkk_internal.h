@@ -96,12 +96,10 @@ void launch_gram_pre2(const unsigned char* Apre, int64_t n, const int2* d_tiles,
                       double* partials, cudaStream_t s);
 void launch_gram_pre(const unsigned char* Apre, int64_t n, const int2* d_tiles, int ntiles, int nsplit,
                      double* partials, cudaStream_t s);
-// tcgen05 3xTF32 Gram on CTA pairs (k_gram_tc2.cu): 256 x 256 tiles (cta_group::2) x row splits.
+// CTA-pair tile list, split count and split reduction (k_gram_tc2.cu) used by the image-fed pair Gram above
 void gram_tc2_tiles(int M, std::vector<int2>& tiles, std::vector<int>& tile_of, int& nT);
 int gram_tc2_splits(int ntiles, int64_t n);
 size_t gram_tc2_partial_doubles(int ntiles, int nsplit);
-void launch_gram_tc2(const float* A, int64_t n, int M, const int2* d_tiles, int ntiles, int nsplit, double* partials,
-                     cudaStream_t s);
 void launch_gram_tc2_reduce(const double* partials, int ntiles, int nsplit, int M, const int* d_tile_of, int nT,
                             double* G, int accumulate, cudaStream_t s);
 // Projection US = A0 W (k_project.cu) with per-block column extremes [blk][c][2].
