@@ -150,12 +150,12 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
     float S[128];
 #pragma unroll
     for (int q = 0; q < 128; ++q) S[q] = 0.f;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit b: phase of accumulator b (bit mask, not an indexed array)
     bool first = true;
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
-      tc::mbar_wait(&acc_full[b], ph[b]);
-      ph[b] ^= 1;
+      tc::mbar_wait(&acc_full[b], ((ph >> b) & 1u));
+      ph ^= 1u << b;
       tc::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 128 * chalf);
 #pragma unroll
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
       constexpr uint32_t idesc = tc::make_idesc_tf32(T2, T2, false, false);
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t eph[2] = {0, 0};
+      uint32_t eph = 0;   // bit b: phase of acc_empty[b]
       const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), LBO, SBO);
       unsigned long long w_full = 0, w_peer = 0, w_acc = 0;   // dbg cycle split
       const unsigned long long t_start = clock64();
@@ -201,9 +201,9 @@ __global__ void __launch_bounds__(NTHR, 1) gram_pre2_kernel(const unsigned char*
         const int b = (int)(pidx & 1);
         if (pidx >= 2) {
           const unsigned long long c0 = dbg ? clock64() : 0;
-          wait_cluster(&acc_empty[b], eph[b]);
+          wait_cluster(&acc_empty[b], ((eph >> b) & 1u));
           if (dbg) w_acc += clock64() - c0;
-          eph[b] ^= 1;
+          eph ^= 1u << b;
           tc::tc_fence_after();
         }
         const uint32_t d = tmem + 256 * b;

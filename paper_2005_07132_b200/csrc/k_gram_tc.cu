@@ -143,12 +143,12 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
     float S[64];
 #pragma unroll
     for (int q = 0; q < 64; ++q) S[q] = 0.f;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit b: phase of accumulator b (bit mask, not an indexed array)
     bool first = true;
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
-      tc::mbar_wait(&acc_full[b], ph[b]);
-      ph[b] ^= 1;
+      tc::mbar_wait(&acc_full[b], ((ph >> b) & 1u));
+      ph ^= 1u << b;
       tc::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 64 * chalf);
 #pragma unroll
@@ -188,14 +188,14 @@ gram_tc_kernel(const float* __restrict__ A, int64_t n, int M, const int2* __rest
     constexpr uint32_t idesc = tc::make_idesc_tf32(GT, GT, false, false);
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t eph[2] = {0, 0};
+    uint32_t eph = 0;   // bit b: phase of acc_empty[b]
     const uint32_t sbase = tc::smem_u32(smem);
     const uint64_t d00 = tc::make_sdesc(sbase, GLBO, GSBO);
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
       if (pidx >= 2) {
-        tc::mbar_wait(&acc_empty[b], eph[b]);
-        eph[b] ^= 1;
+        tc::mbar_wait(&acc_empty[b], ((eph >> b) & 1u));
+        eph ^= 1u << b;
         tc::tc_fence_after();
       }
       const uint32_t d_hi = tmem + 256 * b, d_mid = d_hi + 128;
@@ -382,12 +382,12 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
     float S[64];
 #pragma unroll
     for (int q = 0; q < 64; ++q) S[q] = 0.f;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit b: phase of accumulator b (bit mask, not an indexed array)
     bool first = true;
     for (int64_t pidx = 0; pidx < nper; ++pidx) {
       const int b = (int)(pidx & 1);
-      tc::mbar_wait(&acc_full[b], ph[b]);
-      ph[b] ^= 1;
+      tc::mbar_wait(&acc_full[b], ((ph >> b) & 1u));
+      ph ^= 1u << b;
       tc::tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(256 * b + 64 * chalf);
 #pragma unroll
@@ -428,7 +428,7 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
     constexpr uint32_t idesc = tc::make_idesc_tf32(GT, GT, false, false);
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t eph[2] = {0, 0};
+    uint32_t eph = 0;   // bit b: phase of acc_empty[b]
     const uint64_t d00 = tc::make_sdesc(tc::smem_u32(smem), GLBO, GSBO);
     unsigned long long w_full = 0, w_acc = 0;   // dbg: cycles waiting for operands / for the epilogue
     const unsigned long long t_start = clock64();
@@ -436,9 +436,9 @@ gram_pre_kernel(const unsigned char* __restrict__ Apre, int64_t n, int64_t nq, c
       const int b = (int)(pidx & 1);
       if (pidx >= 2) {
         const unsigned long long c0 = dbg ? clock64() : 0;
-        tc::mbar_wait(&acc_empty[b], eph[b]);
+        tc::mbar_wait(&acc_empty[b], ((eph >> b) & 1u));
         if (dbg) w_acc += clock64() - c0;
-        eph[b] ^= 1;
+        eph ^= 1u << b;
         tc::tc_fence_after();
       }
       const uint32_t d_hi = tmem + 256 * b, d_mid = d_hi + 128;

@@ -150,12 +150,12 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
   } else if (warp < 12) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 8;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit s: phase of slot s (bit mask: an indexed array lives in local memory)
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = (int)(it % nbuf);
-      tc::mbar_wait(&acc_full[b], ph[b]);
-      ph[b] ^= 1;
+      tc::mbar_wait(&acc_full[b], (ph >> b) & 1u);
+      ph ^= 1u << b;
       tc::tc_fence_after();
       const int row = ew * 32 + lane;
       const int64_t p = t * PTM + row;
@@ -246,11 +246,11 @@ project_tc_kernel(const float* __restrict__ A, int64_t n, int M, const float* __
     };
     for (int64_t q = 0; q < PSTAGES - 1 && q < npos; ++q) issue_w(q);
     int stage = 0;
-    uint32_t phase = 0, ae[2] = {0, 0};
+    uint32_t phase = 0, ae = 0;   // ae bit b: phase of accumulator b
     int64_t it = 0, pos = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = (int)(it % nbuf);
-      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], ae[b]); ae[b] ^= 1; tc::tc_fence_after(); }
+      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], (ae >> b) & 1u); ae ^= 1u << b; tc::tc_fence_after(); }
       const uint32_t dset = tmem + (uint32_t)(b * setc);
       const uint32_t dx = dset + nseg * kp;
       for (int st = 0; st < nst; ++st, ++pos) {
@@ -490,12 +490,12 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
   } else if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------ epilogue (as project_tc_kernel)
     const int ew = warp - 8;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit s: phase of slot s (bit mask: an indexed array lives in local memory)
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = (int)(it % nbuf);
-      tc::mbar_wait(&acc_full[b], ph[b]);
-      ph[b] ^= 1;
+      tc::mbar_wait(&acc_full[b], (ph >> b) & 1u);
+      ph ^= 1u << b;
       tc::tc_fence_after();
       const int row = ew * 32 + lane;
       const int64_t p = t * PTM + row;
@@ -564,11 +564,11 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
     // ------------------------------------------------------------ MMA issue (A from TMEM, W from smem)
     const uint32_t idesc = tc::make_idesc_tf32(PTM, kp, false, false);
     Ring rw, rt;
-    uint32_t ae[2] = {0, 0};
+    uint32_t ae = 0;   // bit b: phase of accumulator b
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int b = (int)(it % nbuf);
-      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], ae[b]); ae[b] ^= 1; tc::tc_fence_after(); }
+      if (it >= nbuf) { tc::mbar_wait(&acc_empty[b], (ae >> b) & 1u); ae ^= 1u << b; tc::tc_fence_after(); }
       const uint32_t dset = tmem + (uint32_t)(b * setc);
       const uint32_t dx = dset + nseg * kp;
       for (int st = 0; st < nst; ++st, rw.next(NW), rt.next(NA)) {

@@ -36,7 +36,10 @@ constexpr int RT_THREADS = 128 + RT_EPI + 64;   // + MMA warp + B loader warp
 constexpr int A_LBO = 128;        // unpadded (the A tile is stored once per tile; conflicts there are cheap)
 constexpr int B_LBO = 128;
 static_assert(A_LBO == B_LBO, "the MMA loop advances both descriptors by the same K offset");
-constexpr int RT_NBUF = 2;        // epilogue output boxes per part (double buffer)
+#ifndef FKK_RT_NBUF
+#define FKK_RT_NBUF 3
+#endif
+constexpr int RT_NBUF = FKK_RT_NBUF;   // epilogue output boxes per part (a store may lag RT_NBUF - 1 chunks)
 
 struct RtGeom {
   int kr, nch, N, nchunks;
@@ -126,12 +129,12 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     // ------------------------------------------------------------ producers: US tile -> TMEM
     const int r = tid;                                        // pixel row = TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    uint32_t ph[2] = {0, 0};
+    uint32_t ph = 0;   // bit s: phase of slot s (bit mask: an indexed array lives in local memory)
     int64_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int a = (int)(it % nas);
-      tc::mbar_wait(&a_empty[a], ph[a] ^ 1);
-      ph[a] ^= 1;
+      tc::mbar_wait(&a_empty[a], ((ph >> a) & 1u) ^ 1u);
+      ph ^= 1u << a;
       tc::tc_fence_after();
       const int64_t p = t * RTM + r;
       const float* src = US + p * (int64_t)ldus;
@@ -163,13 +166,13 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     const bool issuer = lg == 0 && lane == 0;
     const uint32_t bar_id = 1 + half;            // named barrier of the 128 threads of this part
     if (issuer) tma::prefetch_map(&tmap_out);
-    uint32_t ph[4] = {0, 0, 0, 0};
+    uint32_t ph = 0;   // bit b: phase of accumulator b (a bit mask: a dynamically indexed array lived in local memory)
     int64_t gq = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
         const int b = (int)(gq & 3);
-        tc::mbar_wait(&acc_full[b], ph[b]);
-        ph[b] ^= 1;
+        tc::mbar_wait(&acc_full[b], (ph >> b) & 1u);
+        ph ^= 1u << b;
         tc::tc_fence_after();
         const uint32_t tb = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b * g.N + half * 2 * nq);
         // box buffer of this chunk must have been read by its store from RT_NBUF chunks ago
@@ -229,7 +232,7 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     const uint32_t idesc = tc::make_idesc_tf32(RTM, g.N, false, false);
     const uint32_t sb = tc::smem_u32(bst);
     const uint64_t db00 = tc::make_sdesc(sb, B_LBO, g.b_sbo);
-    uint32_t a_ph[2] = {0, 0}, bf_ph = 0, ae_ph[4] = {0, 0, 0, 0};   // bit s: phase of stage s
+    uint32_t a_ph = 0, bf_ph = 0, ae_ph = 0;   // bit s: phase of stage / slot / accumulator s
     int64_t it = 0;
     int64_t gq = 0;
     const int nks = g.kr / 8;
@@ -237,8 +240,8 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     //  tensor pipe gets chunk gq's MMAs while chunk gq-1's are still executing)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int a = (int)(it % nas);
-      tc::mbar_wait(&a_full[a], a_ph[a]);
-      a_ph[a] ^= 1;
+      tc::mbar_wait(&a_full[a], (a_ph >> a) & 1u);
+      a_ph ^= 1u << a;
       tc::tc_fence_after();
       const uint32_t tah = tmem_a + (uint32_t)(a * 2 * g.kr), tal = tah + (uint32_t)g.kr;
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
@@ -246,7 +249,7 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
         tc::mbar_wait(&b_full[s], (bf_ph >> s) & 1);
         bf_ph ^= 1u << s;
         const int b = (int)(gq & 3);
-        if (gq >= 4) { tc::mbar_wait(&acc_empty[b], ae_ph[b]); ae_ph[b] ^= 1; }
+        if (gq >= 4) { tc::mbar_wait(&acc_empty[b], (ae_ph >> b) & 1u); ae_ph ^= 1u << b; }
         tc::tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * g.N);
         const uint64_t dbh0 = tc::sdesc_add(db00, (uint32_t)(s * g.b_stage));
