@@ -229,7 +229,11 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int C = (M + NT - 1) / NT;
   const int j0 = tid * C;
-  const SgK sgk = sg_k(h);
+  // the SG constants live in shared memory and are loaded for the trend section only (held in
+  // registers across the whole pair loop they added to the finish kernel's spills)
+  __shared__ SgK sgk_s;
+  if (tid == 0) sgk_s = sg_k(h);
+  __syncthreads();
   const int64_t npairs = (n + 1) >> 1;
   const uint32_t rowb = (uint32_t)M * 4u;
   auto issue = [&](int64_t pr) {   // thread 0: bulk copies of pair pr's phi_err rows into S
@@ -434,7 +438,7 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
         Q1 += da * va - db * vb;
         Q2 += da * da * va - db * db * vb;
         cprev = cc;
-        const double Tv = sg_eval_full(Q0, Q1, Q2, cc, j, sgk);
+        const double Tv = sg_eval_full(Q0, Q1, Q2, cc, j, sgk_s);
         const bool ok = c < C && j < M;
         tmin[r] = ok ? fmin(tmin[r], Tv) : tmin[r];
         tr[r][c] = ok ? (float)rcp64(Tv) : 0.f;   // 1/T, unless the spectrum falls back to the mean
