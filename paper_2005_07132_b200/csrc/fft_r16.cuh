@@ -18,6 +18,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#ifndef FKK_FFT_TWIDDLE_POW2
+#define FKK_FFT_TWIDDLE_POW2 1
+#endif
+
 namespace fkk {
 namespace fft16 {
 
@@ -134,12 +138,38 @@ __device__ __forceinline__ void pass(const float2* __restrict__ tw, Load&& load,
     for (int r = 0; r < R; ++r) v[r] = load(b + r * (L / R));
     const int k = b & (NS - 1);
     if constexpr (NS > 1) {
+#if FKK_FFT_TWIDDLE_POW2
+      // the power-of-two twiddles w^1, w^2, w^4, w^8 from the table, the rest as products of at most
+      // three of them (fewer loads and live registers; <= 3 extra roundings per twiddle)
+      float2 wp[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if ((1 << e) < R) {
+          wp[e] = __ldg(tw + (1 << e) * k * STEP);
+          if (INV) wp[e].y = -wp[e].y;
+        }
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        float2 w = make_float2(1.f, 0.f);
+        bool first = true;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (r & (1 << e)) {
+            w = first ? wp[e] : cmulf(w, wp[e]);
+            first = false;
+          }
+        }
+        v[r] = cmulf(v[r], w);
+      }
+#else
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         float2 w = __ldg(tw + r * k * STEP);
         if (INV) w.y = -w.y;
         v[r] = cmulf(v[r], w);
       }
+#endif
     }
     dft<R, INV>(v);
     const int base = (b - k) * R + k;
