@@ -64,6 +64,7 @@ class ClockSampler:
         self.gpu = gpu
         self.rows: list[list[str]] = []
         self.proc = None
+        self.start = 0
 
     def __enter__(self):
         try:
@@ -72,8 +73,15 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to emit its first row; a 0.2 s timed region could end
+            # before it (one run came back "unsampled"): wait for the sampler to be live, then count
+            # only the rows that arrive from here on (the timed region)
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.start = len(self.rows)
         return self
 
     def _read(self):
@@ -89,8 +97,10 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[self.start:] or self.rows[-1:]   # (a region shorter than one 20 ms period: the last row)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.rows = rows
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
