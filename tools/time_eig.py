@@ -1,4 +1,4 @@
-"""Eig-stage timing of the cfg3 transform: mean stage split over `reps` transforms after a warm-up
+"""Stage timing of the cfg3 transform (the eig stage and the rest): mean stage split over `reps` transforms after a warm-up
 (plan stage events).  python tools/time_eig.py [rows] [reps]"""
 import os
 import sys
@@ -24,5 +24,5 @@ for _ in range(reps):
     torch.cuda.synchronize()
     for k, v in plan.stage_times().items():
         acc[k] = acc.get(k, 0.0) + v / reps
-print(f"LL={os.environ.get('FKK_TRIDIAG_LL', '1')} stages " + ", ".join(f"{k} {v:.3f}" for k, v in acc.items())
+print("stages " + ", ".join(f"{k} {v:.3f}" for k, v in acc.items())
       + f"; total {sum(acc.values()):.3f} ms")
