@@ -352,7 +352,8 @@ void launch_dgemm_small(int m, int n, int kk, const double* A, int lda, int ta, 
 void launch_ridge(const double* C, int k, const double* R, int ncol, double ridge_rel, double* Phi, double* lam_out,
                   double* work, int* flags, cudaStream_t s) {
   double* Lw = work;
-  const size_t sm = k <= 80 ? (size_t)2 * k * k * sizeof(double) : 0;
+  // squarings and factor in shared memory up to 200 KB (k <= 114; k = 100 ran them in global memory: 1.5 ms)
+  const size_t sm = (size_t)2 * k * k * sizeof(double) <= 200 * 1024 ? (size_t)2 * k * k * sizeof(double) : 0;
   int have_lam = 0;
   constexpr int CL = 8;
   const size_t lsm = (3 * (size_t)k * k + 2 * CL) * sizeof(double);

@@ -539,8 +539,18 @@ int gram_tc_splits(int ntiles, int64_t n) {
   int ns = std::max(1, sms / std::max(1, ntiles));
   // fewer than two tiles per SM (cfg4: 13 blocks, 91 tiles): equal pixel ranges for at least four waves
   // of CTAs -- one CTA per tile left 57 of 148 SMs idle (cfg4 at 1M rows: 18.6 ms with 1 range per
-  // tile, 13.1 with 3, 12.8 with 8; 8 to 24 ranges within 1% at 2M rows)
-  if (2 * ntiles > sms) ns = (4 * sms + ntiles - 1) / ntiles;
+  // tile, 13.1 with 3, 12.8 with 8, 14.2 with 7; 8 to 24 ranges within 1% at 2M rows)
+  if (2 * ntiles > sms) {   // and a last wave at least 95% full (91 tiles: 8 ranges = 4.92 waves, not 7 = 4.30)
+    const int lo = (4 * sms + ntiles - 1) / ntiles, hi = 2 * lo;
+    double best = 0.0;
+    ns = lo;
+    for (int c = lo; c <= hi; ++c) {
+      const int64_t ctas = (int64_t)ntiles * c, waves = (ctas + sms - 1) / sms;
+      const double eff = (double)ctas / (double)(waves * sms);
+      if (eff > best + 1e-9) { best = eff; ns = c; }
+      if (eff >= 0.95) break;
+    }
+  }
   if (const char* ev = getenv("FKK_GRAM_SPLITS")) ns = std::max(1, atoi(ev));   // A/B only
   const int64_t by_rows = std::max<int64_t>(1, n / 1024);
   return (int)std::min<int64_t>(ns, by_rows);
