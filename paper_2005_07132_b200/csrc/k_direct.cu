@@ -227,7 +227,10 @@ direct_finish_kernel(const TIn* __restrict__ I, int64_t n, int M, const float* _
   float* y0 = reinterpret_cast<float*>(X);             // Re K' rows (after the transforms)
   float* y1 = y0 + M;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int C = (M + NT - 1) / NT;
+  // L = 4096 (256 threads): 8 channels per thread when M is a multiple of 8 (the float4 path; cfg4's
+  // M = 1600 takes 200 threads x 8 instead of 229 x 7 scalar: 144 -> 136 ms per 4M spectra); shorter
+  // transforms keep ceil(M / NT) (the generalised rule cost cfg3 0.7 ms: other register allocation)
+  const int C = (NT >= 256 && M % 8 == 0 && M <= 8 * NT) ? 8 : (M + NT - 1) / NT;   // (NT < 256: as before)
   const int j0 = tid * C;
   // the SG constants live in shared memory and are loaded for the trend section only (held in
   // registers across the whole pair loop they added to the finish kernel's spills)
