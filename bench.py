@@ -375,13 +375,13 @@ def run_ours(args) -> dict:
         e1.record(stream)
         _barrier(world)
         tm1 = _max_over_ranks(e0.elapsed_time(e1), world)
-        # independent batches alternate over two streams (two plans, two output buffers): one batch's
+        # independent batches rotate over three streams (three plans, three output buffers): one batch's
         # projection fills the SMs the other's reconstruction tail leaves idle
-        papply2 = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local)
-        oa2 = torch.empty_like(oa)
-        sts = [torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)]
-        plans2, outs2 = [papply, papply2], [oa, oa2]
-        for b in range(2):
+        nst = int(os.environ.get("FKK_BENCH_ML_STREAMS", "3"))   # (A/B knob; 2 / 3 / 4: 0.1248 / 0.1225 / 0.1229 ms)
+        plans2 = [papply] + [fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local) for _ in range(nst - 1)]
+        outs2 = [oa] + [torch.empty_like(oa) for _ in range(nst - 1)]
+        sts = [torch.cuda.Stream(device=local) for _ in range(nst)]
+        for b in range(nst):
             with torch.cuda.stream(sts[b]):
                 plans2[b].apply(basis, Ia[:batch], outs2[b])
         torch.cuda.synchronize()
@@ -391,8 +391,8 @@ def run_ours(args) -> dict:
             st.wait_event(e0)
         for i, b0 in enumerate(range(0, a1 - a0, batch)):
             nbb = min(batch, a1 - a0 - b0)
-            with torch.cuda.stream(sts[i & 1]):
-                plans2[i & 1].apply(basis, Ia[b0:b0 + nbb], outs2[i & 1][:nbb])
+            with torch.cuda.stream(sts[i % nst]):
+                plans2[i % nst].apply(basis, Ia[b0:b0 + nbb], outs2[i % nst][:nbb])
         for st in sts:
             ev = torch.cuda.Event()
             ev.record(st)
@@ -400,14 +400,14 @@ def run_ours(args) -> dict:
         e1.record(stream)
         _barrier(world)
         tm = _max_over_ranks(e0.elapsed_time(e1), world)
-        del papply2, oa2
+        del plans2[1:], outs2[1:]
         nbytes = 12.0 * (a1 - a0) * ap.n_freq           # read the cube (4 B) + write complex64 K (8 B) per element
         gbs = nbytes / (tm / 1e3) / 1e9
         ptime = fkk.Plan(ap.n_freq, ap.rank_k, batch, device=local, timing=True)   # per-kernel split of one full batch
         ptime.apply(basis, Ia[:batch], oa)
         ptime.apply(basis, Ia[:batch], oa)
         ml = {"value": ap.n_pixels / (tm / 1e3), "unit": "spectra/s", "ms_per_pass": tm,
-              "batches": nb, "ms_per_batch": tm / max(nb, 1), "streams": 2, "ms_per_batch_one_stream": tm1 / max(nb, 1),
+              "batches": nb, "ms_per_batch": tm / max(nb, 1), "streams": nst, "ms_per_batch_one_stream": tm1 / max(nb, 1),
               "workload": "cfg5: apply 703,026 x 1000 (k=40) in 50,000-spectrum batches",
               "stage_ms_full_batch": ptime.stage_times(),
               "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
