@@ -20,6 +20,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fkk_internal.h"
 #include "tc_common.cuh"
@@ -40,6 +41,8 @@ static_assert(A_LBO == B_LBO, "the MMA loop advances both descriptors by the sam
 #define FKK_RT_NBUF 3
 #endif
 constexpr int RT_NBUF = FKK_RT_NBUF;   // epilogue output boxes per part (a store may lag RT_NBUF - 1 chunks)
+constexpr int RT_NBOX_PAIR = 4;        // pair mode: two pair slots of two boxes per part
+__host__ __device__ constexpr int rt_nbox(bool pair) { return pair ? RT_NBOX_PAIR : RT_NBUF; }
 
 struct RtGeom {
   int kr, nch, N, nchunks;
@@ -47,10 +50,21 @@ struct RtGeom {
   int b_sbo, b_part, b_stage;     // part = hi or lo block, stage = hi + lo
 };
 
-__host__ __device__ inline RtGeom rt_geom(int k, int M) {
+// Channels per chunk: 32 (N = 64 TMEM columns per accumulator) unless 16 is what buys a second A
+// slot (64 < kr <= 96: 4 x 32 + 2 x 2 kr <= 512).  For 96 < kr <= 128 both leave one A slot, and
+// 16-channel chunks only double the epilogue's per-chunk barriers / stores and halve the MMA N
+// (cfg4, k = 100: 4 channels per thread between two barriers).  FKK_RT_NCH=16|32 forces (A/B only).
+inline int rt_pick_nch(int k) {
+  const int kr = (k + 7) / 8 * 8;
+  static const int force = getenv("FKK_RT_NCH") ? atoi(getenv("FKK_RT_NCH")) : 0;
+  if ((force == 16 || force == 32) && (force == 16 || kr <= 128)) return force;
+  return (kr <= 64 || (kr > 96 && kr <= 128)) ? 32 : 16;
+}
+
+__host__ __device__ inline RtGeom rt_geom(int k, int M, int nch) {
   RtGeom g;
   g.kr = (k + 7) / 8 * 8;
-  g.nch = g.kr <= 64 ? 32 : 16;
+  g.nch = nch;
   g.N = 2 * g.nch;
   g.nchunks = (M + g.nch - 1) / g.nch;
   g.a_sbo = (g.kr / 4) * A_LBO;
@@ -91,15 +105,17 @@ __host__ __device__ inline int rt_row_bytes(const RtGeom& g, int imag_only) {
 __host__ __device__ inline int rt_box_region(const RtGeom& g) { return (RTM * (g.nch / RT_PARTS) * 8 + 1023) / 1024 * 1024; }
 
 // RT_BST: B-chunk stages (bulk copies run RT_BST - 1 chunks ahead); 3 when the smem fits, else 2
-template <int RT_BST>
+// PAIR: the epilogue drains two consecutive chunks per step (one barrier pair, one bulk-store group
+// for both; RT_NBOX_PAIR boxes per part = two pair slots) -- half the per-chunk synchronisation
+template <int RT_BST, bool PAIR>
 __global__ void __launch_bounds__(RT_THREADS, 1)
 reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, const float* __restrict__ bimg, int M,
-                      const __grid_constant__ CUtensorMap tmap_out, int imag_only) {   // 0 complex, 1 Im, 2 linear real
+                      const __grid_constant__ CUtensorMap tmap_out, int imag_only, int nch) {   // 0 complex, 1 Im, 2 linear real
   extern __shared__ __align__(1024) unsigned char smem[];
-  const RtGeom g = rt_geom(k, M);
+  const RtGeom g = rt_geom(k, M, nch);
   // [RT_NBUF][2 halves][box]; the TMA swizzle pattern is a function of the smem address -> 1024-align
   unsigned char* stg = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
-  unsigned char* bst = stg + RT_NBUF * RT_PARTS * rt_box_region(g);   // RT_BST stages
+  unsigned char* bst = stg + rt_nbox(PAIR) * RT_PARTS * rt_box_region(g);   // RT_BST stages
   uint64_t* bars = reinterpret_cast<uint64_t*>(bst + RT_BST * g.b_stage);
   uint64_t* a_full = bars;                      // [2] producers -> MMA (count 128)
   uint64_t* a_empty = bars + 2;                 // [2] MMA commit -> producers
@@ -168,6 +184,83 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
     if (issuer) tma::prefetch_map(&tmap_out);
     uint32_t ph = 0;   // bit b: phase of accumulator b (a bit mask: a dynamically indexed array lived in local memory)
     int64_t gq = 0;
+    if constexpr (PAIR) {
+      auto emitp = [&](unsigned char* rowp, const float* v, int j0, int cnt) {
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          if (q >= cnt) break;
+          if (imag_only == 2) {
+            const int byte = (j0 + q) * 4;
+            const int gsn = (byte >> 4) ^ swz;
+            *reinterpret_cast<float2*>(rowp + gsn * 16 + (byte & 15)) = make_float2(v[2 * q], v[2 * q + 2]);
+            continue;
+          }
+          const float2 z0 = cis_exp(v[2 * q], v[2 * q + 1]);
+          const float2 z1 = cis_exp(v[2 * q + 2], v[2 * q + 3]);
+          if (imag_only) {
+            const int byte = (j0 + q) * 4;
+            const int gsn = (byte >> 4) ^ swz;
+            *reinterpret_cast<float2*>(rowp + gsn * 16 + (byte & 15)) = make_float2(z0.y, z1.y);
+          } else {
+            const int gsn = ((j0 + q) >> 1) ^ swz;
+            *reinterpret_cast<float4*>(rowp + gsn * 16) = make_float4(z0.x, z0.y, z1.x, z1.y);
+          }
+        }
+      };
+      const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const int64_t total = my_tiles * g.nchunks;
+      for (int64_t q = 0; q < total; q += 2) {
+        const bool two = q + 1 < total;
+        const int b0 = (int)(q & 3), b1 = (int)((q + 1) & 3);
+        tc::mbar_wait(&acc_full[b0], (ph >> b0) & 1u);
+        ph ^= 1u << b0;
+        if (two) {
+          tc::mbar_wait(&acc_full[b1], (ph >> b1) & 1u);
+          ph ^= 1u << b1;
+        }
+        tc::tc_fence_after();
+        // the pair slot's boxes must have been read by the stores of the pair before last
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(RT_NBOX_PAIR / 2 - 1) : "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        const int slot = (int)((q >> 1) % (RT_NBOX_PAIR / 2));
+        unsigned char* box0 = stg + ((slot * 2) * RT_PARTS + half) * rt_box_region(g);
+        unsigned char* box1 = stg + ((slot * 2 + 1) * RT_PARTS + half) * rt_box_region(g);
+        const uint32_t tb0 = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b0 * g.N + half * 2 * nq);
+        const uint32_t tb1 = two ? tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b1 * g.N + half * 2 * nq) : tb0;
+        if (nq >= 8) {
+          for (int j0 = 0; j0 < nq; j0 += 8) {
+            float v0[16], v1[16];
+            tc::tmem_ld16_x2(tb0 + 2 * j0, tb1 + 2 * j0, v0, v1);   // (a lone last chunk loads its own twice)
+            emitp(box0 + r * rb, v0, j0, 8);
+            if (two) emitp(box1 + r * rb, v1, j0, 8);
+          }
+        } else {
+          float v0[16], v1[16];
+          tc::tmem_ld8(tb0, v0);
+          tc::tmem_ld8(tb1, v1);
+          emitp(box0 + r * rb, v0, 0, 4);
+          if (two) emitp(box1 + r * rb, v1, 0, 4);
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&acc_empty[b0]);
+        if (two) tc::mbar_arrive(&acc_empty[b1]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        if (issuer) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            const int64_t gqu = q + u;
+            const int64_t t = blockIdx.x + (gqu / g.nchunks) * gridDim.x;
+            const int ch = (int)(gqu % g.nchunks);
+            const int c0 = ch * g.nch + half * nq;
+            const int x = imag_only ? c0 : 2 * c0;
+            tma::store_2d(&tmap_out, tc::smem_u32(u == 0 ? box0 : box1), x, (int)(t * RTM));
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    } else
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int ch = 0; ch < g.nchunks; ++ch, ++gq) {
         const int b = (int)(gq & 3);
@@ -291,8 +384,8 @@ reconstruct_tc_kernel(const float* __restrict__ US, int64_t n, int k, int ldus, 
 }
 
 // B image: per chunk ch, part (hi, lo), row r (= 2*local channel + {amp, ph}), K index i.
-__global__ void build_bimg_kernel(const float* __restrict__ Bi, int k, int M, float* __restrict__ bimg) {
-  const RtGeom g = rt_geom(k, M);
+__global__ void build_bimg_kernel(const float* __restrict__ Bi, int k, int M, float* __restrict__ bimg, int nch) {
+  const RtGeom g = rt_geom(k, M, nch);
   const int64_t total = (int64_t)g.nchunks * g.N * g.kr;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % g.kr);
@@ -309,44 +402,51 @@ __global__ void build_bimg_kernel(const float* __restrict__ Bi, int k, int M, fl
   }
 }
 
-size_t rt_smem(int k, int M, int RT_BST) {
-  const RtGeom g = rt_geom(k, M);
-  return (size_t)RT_NBUF * RT_PARTS * rt_box_region(g) + RT_BST * (size_t)g.b_stage + 20 * 8 + 64 + 1024;
+size_t rt_smem(int k, int M, int RT_BST, bool pair) {
+  const RtGeom g = rt_geom(k, M, rt_pick_nch(k));
+  return (size_t)rt_nbox(pair) * RT_PARTS * rt_box_region(g) + RT_BST * (size_t)g.b_stage + 20 * 8 + 64 + 1024;
 }
 
 }  // namespace
 
 size_t reconstruct_tc_bimg_floats(int k, int M) {
-  const RtGeom g = rt_geom(k, M);
+  const RtGeom g = rt_geom(k, M, rt_pick_nch(k));
   return (size_t)g.nchunks * g.b_stage / 4;
 }
 
 void launch_build_bimg(const float* Bi, int k, int M, float* bimg, cudaStream_t s) {
-  build_bimg_kernel<<<256, 256, 0, s>>>(Bi, k, M, bimg);
+  build_bimg_kernel<<<256, 256, 0, s>>>(Bi, k, M, bimg, rt_pick_nch(k));
   check_launch("build_bimg");
 }
 
 void launch_reconstruct_tc(const float* US, int64_t n, int k, int ldus, const float* bimg, int M, void* out,
                            int out_imag_only, cudaStream_t s) {
   if (n <= 0) return;
-  const RtGeom g0 = rt_geom(k, M);
+  const int nch = rt_pick_nch(k);
+  const RtGeom g0 = rt_geom(k, M, nch);
   if (rt_a_base(g0) + 2 * g0.kr > 512) throw Status(10, "reconstruct_tc: k too large for tensor memory");
+  // pair mode when its four boxes per part still leave >= 3 B-chunk stages (cfg3); else one chunk per step
+  static const int force_pair = getenv("FKK_RT_PAIR") ? atoi(getenv("FKK_RT_PAIR")) : -1;   // A/B only
+  bool pair = force_pair != 0 && rt_smem(k, M, force_pair == 1 ? 2 : 3, true) <= 227 * 1024;
   int bst = 4;
-  while (bst > 2 && rt_smem(k, M, bst) > 227 * 1024) --bst;
-  const size_t smem = rt_smem(k, M, bst);
+  while (bst > 2 && rt_smem(k, M, bst, pair) > 227 * 1024) --bst;
+  const size_t smem = rt_smem(k, M, bst, pair);
   if (smem > 227 * 1024) throw Status(10, "reconstruct_tc: k too large for the smem tile");
-  auto kern = bst == 4 ? reconstruct_tc_kernel<4> : bst == 3 ? reconstruct_tc_kernel<3> : reconstruct_tc_kernel<2>;
+  auto kern = pair ? (bst == 4 ? reconstruct_tc_kernel<4, true> : bst == 3 ? reconstruct_tc_kernel<3, true>
+                                                                          : reconstruct_tc_kernel<2, true>)
+                   : (bst == 4 ? reconstruct_tc_kernel<4, false> : bst == 3 ? reconstruct_tc_kernel<3, false>
+                                                                            : reconstruct_tc_kernel<2, false>);
   FKK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t ntiles = (n + RTM - 1) / RTM;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
-  const RtGeom g = rt_geom(k, M);
+  const RtGeom g = rt_geom(k, M, nch);
   const int rb = rt_row_bytes(g, out_imag_only);
   const uint64_t cols = out_imag_only ? (uint64_t)M : 2 * (uint64_t)M;
   const CUtensorMap tm = tma::make_2d_f32(out, (uint64_t)n, cols, cols * 4, RTM, rb / 4, rb);
-  kern<<<grid, RT_THREADS, smem, s>>>(US, n, k, ldus, bimg, M, tm, out_imag_only);
+  kern<<<grid, RT_THREADS, smem, s>>>(US, n, k, ldus, bimg, M, tm, out_imag_only, nch);
   check_launch("reconstruct_tc");
 }
 
