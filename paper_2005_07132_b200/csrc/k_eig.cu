@@ -1563,6 +1563,24 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   launch_eig_topk(G, M, k, work, V, lam_out, flags, s, nullptr);
 }
 
+namespace {
+// per host thread and device: the side stream and fork / join events of the WY-factor kernel
+struct EigSide {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+EigSide& eig_side(int dev) {
+  thread_local EigSide sides[64];
+  EigSide& e = sides[dev & 63];
+  if (!e.st) {
+    FKK_CUDA_CHECK(cudaStreamCreateWithFlags(&e.st, cudaStreamNonBlocking));
+    FKK_CUDA_CHECK(cudaEventCreateWithFlags(&e.fork, cudaEventDisableTiming));
+    FKK_CUDA_CHECK(cudaEventCreateWithFlags(&e.join, cudaEventDisableTiming));
+  }
+  return e;
+}
+}  // namespace
+
 void launch_eig_topk(const double* G, int M, int k, double* work, double* V, double* lam_out, int* flags,
                      cudaStream_t s, double* dbg_det) {
   double* d = work;
@@ -1663,6 +1681,28 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     FKK_CUDA_CHECK(cudaMemcpyAsync(dbg_det, d, 3 * (size_t)M * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return;
   }
+  // WY T factors of the reflector blocks depend only on the tridiagonalisation: on a forked stream
+  // they run beside bisection / inverse iteration / CholQR2 (FKK_WYT_FORK=0: in order, A/B only)
+  static const int bx_mode = getenv("FKK_BACKXFORM_MODE") ? atoi(getenv("FKK_BACKXFORM_MODE")) : 1;   // A/B only
+  static const int wyt_fork = getenv("FKK_WYT_FORK") ? atoi(getenv("FKK_WYT_FORK")) : 1;
+  const bool wy_path = bx_mode == 1 && M >= 3 && M <= 32 * kBxW * 4;
+  const int nrefl = M - 2, nblk = (nrefl + kWyB - 1) / kWyB;
+  double* Tg = A + (size_t)M * M;
+  EigSide* side = nullptr;
+  if (wy_path) {
+    const size_t tsm = (size_t)kWyB * M * sizeof(double);
+    FKK_CUDA_CHECK(cudaFuncSetAttribute(wy_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    cudaStream_t ws = s;
+    if (wyt_fork) {
+      side = &eig_side(dev);
+      FKK_CUDA_CHECK(cudaEventRecord(side->fork, s));
+      FKK_CUDA_CHECK(cudaStreamWaitEvent(side->st, side->fork, 0));
+      ws = side->st;
+    }
+    wy_t_kernel<<<nblk, 256, tsm, ws>>>(A, tau, M, nrefl, Tg);
+    check_launch("eig_wy_t");
+    if (side) FKK_CUDA_CHECK(cudaEventRecord(side->join, side->st));
+  }
   FKK_CUDA_CHECK(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(2 * (size_t)M * sizeof(double))));
   int bth = 128;
@@ -1703,14 +1743,8 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t rsm = ((size_t)(kBxStages + 1) * M + 2 * kBxW) * sizeof(double);
-  static const int bx_mode = getenv("FKK_BACKXFORM_MODE") ? atoi(getenv("FKK_BACKXFORM_MODE")) : 1;   // A/B only
-  if (bx_mode == 1 && M >= 3 && M <= 32 * kBxW * 4) {   // (NPL = 8 would spill the register-cached V block)
-    const int nrefl = M - 2, nblk = (nrefl + kWyB - 1) / kWyB;
-    double* Tg = A + (size_t)M * M;
-    const size_t tsm = (size_t)kWyB * M * sizeof(double);
-    FKK_CUDA_CHECK(cudaFuncSetAttribute(wy_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-    wy_t_kernel<<<nblk, 256, tsm, s>>>(A, tau, M, nrefl, Tg);
-    check_launch("eig_wy_t");
+  if (wy_path) {   // (NPL = 8 would spill the register-cached V block)
+    if (side) FKK_CUDA_CHECK(cudaStreamWaitEvent(s, side->join, 0));
     const int npl = M <= 32 * kBxW * 2 ? 2 : 4;
     const int wsm = kWyB * npl * 32 * kBxW * (int)sizeof(double);   // the prefetched block
     auto kb = npl == 2 ? backxform_wy_kernel<2> : backxform_wy_kernel<4>;

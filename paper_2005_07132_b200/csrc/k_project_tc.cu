@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
 project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, const float* __restrict__ wimg, int kp,
                    float* __restrict__ US, float* __restrict__ ext_val, int64_t* __restrict__ ext_idx, int k,
                    int64_t row_offset, int want_ext, int nbuf, int abase, int NA, const float* __restrict__ inv_ref,
-                   float floor, int ir_smem) {
+                   float floor, int ir_smem, int pseg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int NR = q_nraw(kp), NW = q_nw(kp);
@@ -369,8 +369,7 @@ project_tma_kernel(const __grid_constant__ CUtensorMap amap, int64_t n, int M, c
     tc::fence_mbar_init();
     tma::prefetch_map(&amap);
   }
-  const int nseg = p_nseg(M, kp), setc = p_set_cols(M, kp);
-  const int pseg = p_seg_len(M, kp);
+  const int nseg = (M + pseg - 1) / pseg, setc = (nseg + 1) * kp;
   if (ir_smem)
     for (int c = tid; c < ((M + 31) & ~31); c += blockDim.x) sir[c] = inv_ref[c];
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -708,15 +707,22 @@ void launch_project_tc(const float* A, int64_t n, int M, const float* wimg, int 
     const CUtensorMap amap = tma::make_2d_f32(A, (uint64_t)n, (uint64_t)M, (uint64_t)M * 4, PTM, QKC, 128);
     const int64_t ntiles = (n + PTM - 1) / PTM;
     const int grid = (int)std::min<int64_t>(ntiles, sms);
-    int nbuf = q_nbuf(M, kp), abase = q_abase(M, kp), na = q_na(M, kp);
+    // hi*hi segment length (FKK_PROJECT_SEGLEN: A/B only, a multiple of 32) and the TMEM split it implies
+    int pseg = p_seg_len(M, kp);
+    if (const char* ev = getenv("FKK_PROJECT_SEGLEN")) pseg = std::max(32, atoi(ev) / 32 * 32);
+    const int setc = ((M + pseg - 1) / pseg + 1) * kp;
+    if (setc > 512 - 2 * QKC) throw Status(10, "project_tc: segment length leaves no A slot");
+    int nbuf = ((2 * setc + 127) & ~127) + 2 * 2 * QKC <= 512 ? 2 : 1;
+    int abase = (nbuf * setc + 127) & ~127;
+    int na = std::min(8, (512 - abase) / (2 * QKC));
     if (const char* ev = getenv("FKK_PROJECT_NBUF")) {   // A/B only
       nbuf = 1;
-      abase = (p_set_cols(M, kp) + 127) & ~127;
+      abase = (setc + 127) & ~127;
       na = std::min(8, (512 - abase) / (2 * QKC));
       if (atoi(ev) > 0) na = std::min(na, atoi(ev));
     }
     project_tma_kernel<<<grid, QTHREADS, smem, s>>>(amap, n, M, wimg, kp, US, ext_val, ext_idx, k, row_offset, want_ext,
-                                                    nbuf, abase, na, inv_ref, floor, ir_smem);
+                                                    nbuf, abase, na, inv_ref, floor, ir_smem, pseg);
     check_launch("project_tma");
     return;
   }
