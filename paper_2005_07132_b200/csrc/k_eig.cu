@@ -1234,7 +1234,7 @@ template <int NPL>
 __global__ void __launch_bounds__(32 * kBxW) backxform_wy_kernel(const double* __restrict__ Wk, const double* __restrict__ Tg,
                                                                  int M, int nrefl, int k, const double* __restrict__ Z,
                                                                  const double* __restrict__ lam, double* __restrict__ V,
-                                                                 double* __restrict__ lam_out) {
+                                                                 double* __restrict__ lam_out, int tpre) {
   constexpr int NT = 32 * kBxW;
   __shared__ double red[2][kBxW][kWyB];   // parity-buffered: one barrier pair per block
   __shared__ double wv[2][kWyB];
@@ -1276,6 +1276,14 @@ __global__ void __launch_bounds__(32 * kBxW) backxform_wy_kernel(const double* _
 #pragma unroll
       for (int u = 0; u < NPL; ++u) vr[i][u] = vnext[(i * NPL + u) * NT + tid];
     if (p > 0) prefetch(p - 1);
+    // warp 0's rows of this block's T factor, loaded before the dots and the barrier (an L2 round
+    // trip after the barrier sat on every block's critical path)
+    double trow[kWyB];
+    if (warp == 0) {
+      const double* T = Tg + (int64_t)p * kWyB * kWyB;
+#pragma unroll
+      for (int c = 0; c < kWyB; ++c) trow[c] = (tpre && lane < kWyB && c >= lane) ? __ldg(T + lane * kWyB + c) : 0.0;
+    }
     // w = V^T z: per-thread partials of all dots, lane-transposed warp sums, 8-warp sum
     double part[kWyB];
 #pragma unroll
@@ -1294,13 +1302,13 @@ __global__ void __launch_bounds__(32 * kBxW) backxform_wy_kernel(const double* _
 #pragma unroll
         for (int w2 = 0; w2 < kBxW; ++w2) w += red[p & 1][w2][lane];
       }
-      // w' = T w (T upper triangular): lane r sums T(r, c) w_c for c >= r
-      const double* T = Tg + (int64_t)p * kWyB * kWyB;
+      // w' = T w (T upper triangular): lane r sums T(r, c) w_c for c >= r (trow is zero elsewhere)
       double tw = 0.0;
+      const double* T = Tg + (int64_t)p * kWyB * kWyB;
 #pragma unroll
       for (int c = 0; c < kWyB; ++c) {
         const double wc = __shfl_sync(0xffffffffu, w, c);
-        if (lane < kWyB && c >= lane) tw = fma(__ldg(T + lane * kWyB + c), wc, tw);
+        if (lane < kWyB && c >= lane) tw = fma(tpre ? trow[c] : __ldg(T + lane * kWyB + c), wc, tw);
       }
       if (lane < kWyB) wv[p & 1][lane] = tw;
     }
@@ -1749,7 +1757,8 @@ void launch_eig_topk(const double* G, int M, int k, double* work, double* V, dou
     const int wsm = kWyB * npl * 32 * kBxW * (int)sizeof(double);   // the prefetched block
     auto kb = npl == 2 ? backxform_wy_kernel<2> : backxform_wy_kernel<4>;
     FKK_CUDA_CHECK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm));
-    kb<<<k, 32 * kBxW, wsm, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out);
+    static const int tpre = getenv("FKK_BX_TPRE") ? atoi(getenv("FKK_BX_TPRE")) : 1;   // A/B only
+    kb<<<k, 32 * kBxW, wsm, s>>>(A, Tg, M, nrefl, k, Zf, lam, V, lam_out, tpre);
     check_launch("eig_backxform_wy");
     return;
   }
